@@ -1,0 +1,643 @@
+// mcg_build.cpp — recipe -> device layout (see mcg_build.h).
+//
+// Compiled as plain host C++ with -ffp-contract=off and no -march, exactly
+// like the reference (proj/CMakeLists.txt:4-10), and calling glibc exp where
+// the reference does, so build-time constants match bit for bit.
+#include "mcg_build.h"
+
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <numbers>
+
+#include "mcg_rng.h"
+
+namespace mcg {
+
+namespace {
+
+constexpr double kPi = std::numbers::pi;
+
+[[noreturn]] void engine_error(const std::string& m) { throw Error(MCG_ERR_ENGINE, m); }
+[[noreturn]] void morph_error(const std::string& m) { throw Error(MCG_ERR_MORPHOLOGY, m); }
+
+// HH rate functions (engine.cpp:41-54), host glibc exp
+double hh_alpha_m(double v) {
+  const double x = v + 40.0;
+  if (std::fabs(x) < 1e-7) return 1.0;
+  return 0.1 * x / (1.0 - std::exp(-x / 10.0));
+}
+double hh_beta_m(double v) { return 4.0 * std::exp(-(v + 65.0) / 18.0); }
+double hh_alpha_h(double v) { return 0.07 * std::exp(-(v + 65.0) / 20.0); }
+double hh_beta_h(double v) { return 1.0 / (1.0 + std::exp(-(v + 35.0) / 10.0)); }
+double hh_alpha_n(double v) {
+  const double x = v + 55.0;
+  if (std::fabs(x) < 1e-7) return 0.1;
+  return 0.01 * x / (1.0 - std::exp(-x / 10.0));
+}
+double hh_beta_n(double v) { return 0.125 * std::exp(-(v + 65.0) / 80.0); }
+
+// select_target (engine.cpp:58-74)
+int select_target(int group_size, int policy, int& cursor) {
+  if (group_size <= 0) throw Error(MCG_ERR_TARGETING, "select_target: empty group");
+  switch (policy) {
+    case MCG_POLICY_UNIVALENT:
+      if (group_size != 1)
+        throw Error(MCG_ERR_TARGETING, "select_target: univalent needs a single item");
+      return 0;
+    case MCG_POLICY_ROUND_ROBIN: {
+      const int i = cursor % group_size;
+      cursor = (i + 1) % group_size;
+      return i;
+    }
+    case MCG_POLICY_ROUND_ROBIN_HALT:
+      return cursor % group_size;
+  }
+  throw Error(MCG_ERR_TARGETING, "select_target: unknown policy");
+}
+
+struct KindRT {  // build_kind outputs not stored in McgKind
+  std::vector<double> cap_nF, g_leak, g_leak_rhs, axial, g_na, g_k, cf;
+  std::vector<std::vector<double>> sp_coupling;
+  std::vector<int64_t> ca_delay;  // per placement
+  double c_tot = 0;
+};
+
+// TreeSolver::axial_conductance_uS (tree_solver.cpp:19-30)
+std::vector<double> axial_conductance(const Grid& g, double r_l) {
+  std::vector<double> a(g.size(), 0.0);
+  for (int i = 1; i < g.size(); ++i) {
+    const int p = g.parent[i];
+    const double r = r_l * (0.5 * g.length[i] / g.xs[i] + 0.5 * g.length[p] / g.xs[p]);
+    a[i] = 1.0 / r;
+  }
+  return a;
+}
+
+// TreeSolver::diffusive_coupling (tree_solver.cpp:32-44)
+std::vector<double> diffusive_coupling(const Grid& g, double diffusivity_si) {
+  std::vector<double> b(g.size(), 0.0);
+  if (diffusivity_si <= 0) return b;
+  const double d = diffusivity_si * 1e9;  // units::diff_um2_per_ms
+  for (int i = 1; i < g.size(); ++i) {
+    const int p = g.parent[i];
+    const double r = 0.5 * g.length[i] / (d * g.xs[i]) + 0.5 * g.length[p] / (d * g.xs[p]);
+    b[i] = 1.0 / r;
+  }
+  return b;
+}
+
+}  // namespace
+
+int64_t ceil_steps(double t_ms, double dt_ms) {
+  return static_cast<int64_t>(std::ceil(t_ms / dt_ms - 1e-9));  // engine.cpp:21-23
+}
+
+// discretize (morphology.cpp:67-143)
+Grid discretize(const mcg_kind& k) {
+  const int n = k.n_segments;
+  if (n == 0) morph_error("discretize: empty segment list");
+  if (!(k.target_compartment_um > 0)) morph_error("discretize: target length must be positive");
+  int root = -1;
+  for (int s = 0; s < n; ++s) {
+    if (!(k.seg_length_um[s] > 0) || !(k.seg_radius_um[s] > 0))
+      morph_error("discretize: non-positive segment geometry");
+    if (k.seg_parent_pos[s] < 0 || k.seg_parent_pos[s] > 1)
+      morph_error("discretize: parent_pos outside [0,1]");
+    if (k.seg_parent[s] < 0) {
+      if (root >= 0) morph_error("discretize: multiple roots");
+      root = s;
+    } else if (k.seg_parent[s] >= n) {
+      morph_error("discretize: parent index out of range");
+    }
+  }
+  if (root < 0) morph_error("discretize: no root segment");
+  std::vector<int> order{root};
+  std::vector<char> placed(n, 0);
+  placed[root] = 1;
+  for (std::size_t head = 0; head < order.size(); ++head)
+    for (int s = 0; s < n; ++s)
+      if (!placed[s] && k.seg_parent[s] >= 0 && k.seg_parent[s] == order[head]) {
+        order.push_back(s);
+        placed[s] = 1;
+      }
+  if (static_cast<int>(order.size()) != n) morph_error("discretize: cyclic parent references");
+
+  struct Range { int first = 0, count = 0; };
+  std::vector<Range> ranges(n);
+  Grid g;
+  for (int idx : order) {
+    const double len = k.seg_length_um[idx], rad = k.seg_radius_um[idx];
+    const int count = std::max(1, static_cast<int>(std::ceil(len / k.target_compartment_um - 1e-12)));
+    const double dl = len / count;
+    const double area_xs = kPi * rad * rad;
+    ranges[idx] = {g.size(), count};
+    for (int kk = 0; kk < count; ++kk) {
+      int parent_comp;
+      if (kk > 0) {
+        parent_comp = ranges[idx].first + kk - 1;
+      } else if (k.seg_parent[idx] < 0) {
+        parent_comp = -1;
+      } else {
+        const Range& pr = ranges[k.seg_parent[idx]];
+        const double kf = k.seg_parent_pos[idx] * pr.count - 0.5;
+        int q = static_cast<int>(std::ceil(kf - 0.5));
+        q = std::clamp(q, 0, pr.count - 1);
+        parent_comp = pr.first + q;
+      }
+      g.length.push_back(dl);
+      g.area.push_back(2 * kPi * rad * dl);
+      g.xs.push_back(area_xs);
+      g.volume.push_back(area_xs * dl);
+      g.parent.push_back(parent_comp);
+      g.tag.push_back(k.seg_tag[idx]);
+      g.segment_of.push_back(static_cast<uint32_t>(idx));
+    }
+  }
+  for (double vv : g.volume) g.total_volume += vv;
+  return g;
+}
+
+void partition(const mcg_recipe& r, int world, std::vector<uint32_t>& bounds) {
+  const int n = r.n_cells;
+  bounds.assign(world + 1, 0);
+  bounds[world] = static_cast<uint32_t>(n);
+  if (world <= 1 || n == 0) return;
+  // cost per cell: compartments + synapse instances (placements + connections)
+  std::vector<int64_t> kcost(r.n_kinds, 0);
+  for (int k = 0; k < r.n_kinds; ++k) {
+    int64_t comps = 0;
+    try { comps = discretize(r.kinds[k]).size(); } catch (...) { comps = 1; }
+    int64_t pre = 0;
+    for (int p = 0; p < r.kinds[k].n_placements; ++p) pre += r.kinds[k].placements[p].count;
+    kcost[k] = comps + pre;
+  }
+  std::vector<int64_t> cost(n);
+  for (int c = 0; c < n; ++c)
+    cost[c] = (r.cell_kind[c] < static_cast<uint32_t>(r.n_kinds)) ? kcost[r.cell_kind[c]] : 1;
+  for (int64_t i = 0; i < r.n_connections; ++i)
+    if (r.conn_dst[i] < static_cast<uint32_t>(n)) cost[r.conn_dst[i]] += 1;
+  int64_t total = 0;
+  for (int64_t c : cost) total += c;
+  int64_t acc = 0;
+  int w = 1;
+  for (int c = 0; c < n && w < world; ++c) {
+    acc += cost[c];
+    while (w < world && acc * world >= total * w) bounds[w++] = static_cast<uint32_t>(c + 1);
+  }
+  while (w < world) bounds[w++] = static_cast<uint32_t>(n);
+}
+
+void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
+  const double dt = opt.dt_ms;
+  m.dt = dt;
+  m.seed = opt.seed;
+  m.rank = opt.rank;
+  m.world = opt.world < 1 ? 1 : opt.world;
+  m.n_cells_global = r.n_cells;
+  std::vector<uint32_t> bounds;
+  partition(r, m.world, bounds);
+  m.gid_begin = bounds[m.rank];
+  m.gid_end = bounds[m.rank + 1];
+
+  // ---- kinds (build_kind, engine.cpp:189-278) ----
+  const int nk = r.n_kinds;
+  std::vector<KindRT> krt(nk);
+  m.kinds.resize(nk);
+  m.grids.resize(nk);
+  m.k_sp_off.resize(nk + 1, 0);
+  for (int ki = 0; ki < nk; ++ki) {
+    const mcg_kind& spec = r.kinds[ki];
+    McgKind& K = m.kinds[ki];
+    K = McgKind{};
+    KindRT& k = krt[ki];
+    Grid& g = m.grids[ki];
+    g = discretize(spec);
+    const int n = g.size();
+    K.n = n;
+    k.cap_nF.assign(n, 0.0);
+    k.g_leak.assign(n, 0.0);
+    k.g_leak_rhs.assign(n, 0.0);
+    k.g_na.assign(n, 0.0);
+    k.g_k.assign(n, 0.0);
+    k.axial.assign(n, 0.0);
+    k.cf.assign(n, 0.0);
+    if (spec.membrane == MCG_MEMBRANE_LIF) {
+      const mcg_lif& L = spec.lif;
+      K.dyn = L.exact ? MCG_DYN_LIF_EXACT : MCG_DYN_LIF;
+      if (L.exact && n != 1) engine_error("exact LIF requires a single compartment");
+      double area_tot = 0;
+      for (int i = 0; i < n; ++i) area_tot += g.area[i];
+      k.c_tot = L.tau_mem_ms / L.r_mem_MOhm;
+      for (int i = 0; i < n; ++i) {
+        const double share = g.area[i] / area_tot;
+        k.cap_nF[i] = k.c_tot * share;
+        k.g_leak[i] = share / L.r_mem_MOhm;
+        k.g_leak_rhs[i] = k.g_leak[i] * L.v_rev_mV;
+      }
+      k.axial = axial_conductance(g, L.r_axial_ohm_m);
+      K.ref_steps = ceil_steps(L.t_ref_ms, dt);
+      K.detector_comp = L.detector_comp;
+      K.noise_comp = L.noise_comp;
+      K.threshold = L.v_thresh_mV;
+      K.has_detector = 1;
+      K.has_bg = (L.i_bg_nA != 0.0 || L.sigma_bg_nA_sqrt_ms != 0.0) ? 1 : 0;
+      K.v_rev = L.v_rev_mV;
+      K.r_mem = L.r_mem_MOhm;
+      K.v_reset = L.v_reset_mV;
+      K.i_bg = L.i_bg_nA;
+      K.sig_bg = L.sigma_bg_nA_sqrt_ms / std::sqrt(dt);
+      K.bg_t0 = L.bg_quiet_t0_ms;
+      K.bg_t1 = L.bg_quiet_t1_ms;
+      K.lif_exact_f = std::exp(-dt / L.tau_mem_ms);
+    } else if (spec.membrane == MCG_MEMBRANE_HH) {
+      const mcg_hh& H = spec.hh;
+      K.dyn = MCG_DYN_HH;
+      for (int i = 0; i < n; ++i) {
+        const double a = g.area[i];
+        k.cap_nF[i] = H.c_m * a * 1e-3;
+        k.c_tot += k.cap_nF[i];
+        k.g_leak[i] = H.g_leak * a * 1e-6;
+        k.g_leak_rhs[i] = k.g_leak[i] * H.e_leak_mV;
+        if (g.tag[i] == MCG_REGION_SOMA) {
+          k.g_na[i] = H.g_na * a * 1e-6;
+          k.g_k[i] = H.g_k * a * 1e-6;
+        }
+      }
+      k.axial = axial_conductance(g, H.r_axial_ohm_m);
+      K.detector_comp = H.detector_comp;
+      K.threshold = H.threshold_mV;
+      K.has_detector = 1;
+      K.e_na = H.e_na_mV;
+      K.e_k = H.e_k_mV;
+    } else {
+      K.dyn = MCG_DYN_NONE;
+    }
+    if (K.dyn != MCG_DYN_NONE)
+      for (int i = 0; i < n; ++i) k.cf[i] = k.c_tot / k.cap_nF[i];
+
+    K.n_species = spec.n_species;
+    K.sps_idx = spec.sps_idx;
+    K.prp_idx = spec.prp_idx;
+    for (int s = 0; s < spec.n_species; ++s)
+      k.sp_coupling.push_back(diffusive_coupling(g, spec.species[s].diffusivity));
+
+    K.n_groups = spec.n_placements;
+    K.spec0 = static_cast<int32_t>(m.specs.size());
+    for (int p = 0; p < spec.n_placements; ++p) {
+      const mcg_placement& pl = spec.placements[p];
+      const mcg_syn_spec& sy = pl.syn;
+      McgSpec S{};
+      S.kind = sy.kind;
+      S.comp = pl.comp;
+      S.count = pl.count;
+      S.f_decay = std::exp(-dt / sy.tau_syn_ms);
+      S.e_rev = sy.e_rev_mV;
+      S.tau_pre = sy.stdp.tau_pre_ms;
+      S.tau_post = sy.stdp.tau_post_ms;
+      S.a_pre = sy.stdp.a_pre_uS;
+      S.a_post = sy.stdp.a_post_uS;
+      S.wmax = sy.stdp.wmax_uS;
+      S.dw_plus = sy.homeo.dw_plus_nA;
+      S.dw_minus = sy.homeo.dw_minus_nA;
+      S.h_wmax = sy.homeo.wmax_nA;
+      const mcg_stc_params& P = sy.stc;
+      S.h0 = P.h0_mV;
+      S.tau_h = P.tau_h_ms;
+      S.theta_p = P.theta_p;
+      S.theta_d = P.theta_d;
+      S.gamma_p = P.gamma_p;
+      S.gamma_d = P.gamma_d;
+      S.sigma = P.sigma_pl_mV;
+      S.f_int = P.f_int;
+      S.tau_z = P.tau_z_ms;
+      S.theta_tag = P.theta_tag_mV;
+      S.cf = std::exp(-dt / P.tau_c_ms);
+      S.nz1 = P.sigma_pl_mV * std::sqrt(double(1) / P.tau_h_ms) * std::sqrt(dt);
+      S.nz2 = P.sigma_pl_mV * std::sqrt(double(2) / P.tau_h_ms) * std::sqrt(dt);
+      S.cpre_s = P.c_pre * sy.calcium_scale;
+      S.cpost_s = P.c_post * sy.calcium_scale;
+      int64_t d = 0;
+      if (sy.kind == MCG_SYN_STC_CHARGE) {
+        d = ceil_steps(P.t_c_delay_ms, dt);
+        if (spec.prp_enabled) {  // make_prp_synthesis (mechanisms.hpp:258-262)
+          K.prp_theta_star = P.theta_pro_mV / g.total_volume;
+          K.prp_rate = g.total_volume * P.p_max / P.tau_p_ms;
+        }
+        ++K.n_stc_groups;
+      }
+      if (K.dyn == MCG_DYN_LIF_EXACT &&
+          (sy.kind == MCG_SYN_STATIC_COND || sy.kind == MCG_SYN_STDP_COND))
+        engine_error("exact LIF supports only current/charge synapses");
+      S.ca_delay = d;
+      k.ca_delay.push_back(d);
+      m.specs.push_back(S);
+    }
+    if (spec.prp_enabled) {
+      K.prp_enabled = 1;
+      K.prp_comp = spec.prp_comp;
+      if (spec.sps_idx < 0 || spec.prp_idx < 0)
+        engine_error("synthesis unit needs SPS and PRP species");
+    }
+
+    // flattened per-kind arrays (+ per-step constants hoisted)
+    K.arr = static_cast<int64_t>(m.k_parent.size());
+    for (int i = 0; i < n; ++i) {
+      m.k_parent.push_back(g.parent[i]);
+      m.k_cap_dt.push_back(k.cap_nF[i] / dt);
+      m.k_g_leak.push_back(k.g_leak[i]);
+      m.k_g_leak_rhs.push_back(k.g_leak_rhs[i]);
+      m.k_axial.push_back(k.axial[i]);
+      m.k_g_na.push_back(k.g_na[i]);
+      m.k_g_k.push_back(k.g_k[i]);
+      m.k_cf.push_back(k.cf[i]);
+      m.k_volume.push_back(g.volume[i]);
+    }
+    K.sp_arr = static_cast<int64_t>(m.k_sp_cap_dt.size());
+    m.k_sp_off[ki] = static_cast<int64_t>(m.k_sp_decay_tau.size());
+    for (int s = 0; s < spec.n_species; ++s) {
+      const double tau = spec.species[s].decay_tau_ms;
+      m.k_sp_decay_tau.push_back(tau);
+      for (int i = 0; i < n; ++i) {
+        m.k_sp_cap_dt.push_back(g.volume[i] / dt);
+        m.k_sp_gs.push_back(tau > 0 ? g.volume[i] / tau : 0.0);
+        m.k_sp_coupling.push_back(k.sp_coupling[s][i]);
+        m.k_sp_init.push_back(spec.species[s].init);
+      }
+    }
+    m.k_sp_off[ki + 1] = static_cast<int64_t>(m.k_sp_decay_tau.size());
+  }
+
+  // ---- local cells (engine.cpp:317-348) ----
+  const uint32_t g0 = m.gid_begin, g1 = m.gid_end;
+  for (uint32_t gid = 0; gid < static_cast<uint32_t>(r.n_cells); ++gid)
+    if (r.cell_kind[gid] >= static_cast<uint32_t>(nk)) engine_error("cell kind out of range");
+  const int nl = static_cast<int>(g1 - g0);
+  m.cell_kind.resize(nl);
+  m.comp_off.resize(nl + 1);
+  m.sp_off.resize(nl + 1);
+  m.cg_off.resize(nl + 1);
+  m.det_prev.resize(nl);
+  m.armed.assign(nl, 1);
+  m.refr_until.assign(nl, 0);
+  m.internal_seq.assign(nl, 0);
+  int64_t comps = 0, sps = 0, cgs = 0;
+  for (int c = 0; c < nl; ++c) {
+    const int kid = static_cast<int>(r.cell_kind[g0 + c]);
+    m.cell_kind[c] = kid;
+    const McgKind& K = m.kinds[kid];
+    m.comp_off[c] = comps;
+    m.sp_off[c] = sps;
+    m.cg_off[c] = cgs;
+    comps += K.n;
+    sps += static_cast<int64_t>(K.n) * K.n_species;
+    cgs += K.n_groups;
+  }
+  m.comp_off[nl] = comps;
+  m.sp_off[nl] = sps;
+  m.cg_off[nl] = cgs;
+  m.v.assign(comps, 0.0);
+  m.hh_m.assign(comps, 0.0);
+  m.hh_h.assign(comps, 0.0);
+  m.hh_n.assign(comps, 0.0);
+  m.species.assign(sps, 0.0);
+  for (int c = 0; c < nl; ++c) {
+    const McgKind& K = m.kinds[m.cell_kind[c]];
+    const mcg_kind& spec = r.kinds[m.cell_kind[c]];
+    const int64_t o = m.comp_off[c];
+    if (K.dyn == MCG_DYN_LIF || K.dyn == MCG_DYN_LIF_EXACT) {
+      for (int i = 0; i < K.n; ++i) m.v[o + i] = spec.lif.v_rev_mV;
+      m.det_prev[c] = spec.lif.v_rev_mV;
+    } else if (K.dyn == MCG_DYN_HH) {
+      const double v = spec.hh.v_init_mV;
+      const double mm = hh_alpha_m(v) / (hh_alpha_m(v) + hh_beta_m(v));
+      const double hh = hh_alpha_h(v) / (hh_alpha_h(v) + hh_beta_h(v));
+      const double nn = hh_alpha_n(v) / (hh_alpha_n(v) + hh_beta_n(v));
+      for (int i = 0; i < K.n; ++i) {
+        m.v[o + i] = v;
+        m.hh_m[o + i] = mm;
+        m.hh_h[o + i] = hh;
+        m.hh_n[o + i] = nn;
+      }
+      m.det_prev[c] = v;
+    } else {
+      m.det_prev[c] = 0.0;
+    }
+    for (int s = 0; s < K.n_species; ++s)
+      for (int i = 0; i < K.n; ++i)
+        m.species[m.sp_off[c] + static_cast<int64_t>(s) * K.n + i] = spec.species[s].init;
+  }
+
+  // ---- synapse instances: pre-placed then per connection ----
+  // gather per (local cell, group) instance lists in creation order
+  std::vector<std::vector<int32_t>> inst_comp(cgs);
+  std::vector<std::vector<double>> inst_w(cgs);
+  for (int c = 0; c < nl; ++c) {
+    const McgKind& K = m.kinds[m.cell_kind[c]];
+    for (int gi = 0; gi < K.n_groups; ++gi) {
+      const McgSpec& S = m.specs[K.spec0 + gi];
+      for (int i = 0; i < S.count; ++i) {
+        inst_comp[m.cg_off[c] + gi].push_back(S.comp);
+        inst_w[m.cg_off[c] + gi].push_back(0.0);
+      }
+    }
+  }
+  struct Edge {
+    uint32_t src_key;
+    uint32_t seq;
+    int32_t dst_local, group;
+    uint32_t inst;
+    double w;
+    int64_t delay;
+    int32_t source;  // -1 for cell edges
+  };
+  std::vector<Edge> edges;
+  std::map<std::pair<uint32_t, int32_t>, int> cursors;
+  const int64_t nconn = r.n_connections;
+  for (int64_t ci = 0; ci < nconn; ++ci) {
+    const uint32_t dst = r.conn_dst[ci];
+    if (dst >= static_cast<uint32_t>(r.n_cells)) engine_error("connection dst out of range");
+    const int32_t gi = r.conn_group[ci];
+    const mcg_kind& dspec = r.kinds[r.cell_kind[dst]];
+    if (gi < 0 || gi >= dspec.n_placements)
+      engine_error("connection label '#" + std::to_string(gi) + "' not found");
+    const bool local = dst >= g0 && dst < g1;
+    uint32_t instance = 0;
+    const mcg_placement& pl = dspec.placements[gi];
+    if (local) {
+      const int64_t cg = m.cg_off[dst - g0] + gi;
+      if (pl.count == 0) {
+        inst_comp[cg].push_back(pl.comp);
+        inst_w[cg].push_back(r.conn_weight[ci]);
+        instance = static_cast<uint32_t>(inst_comp[cg].size() - 1);
+      } else {
+        int& cur = cursors[{dst, gi}];
+        instance = static_cast<uint32_t>(
+            select_target(static_cast<int>(inst_comp[cg].size()), r.conn_policy[ci], cur));
+      }
+    } else if (pl.count != 0) {
+      // cursor state is per destination; non-local destinations never matter
+    }
+    const int64_t d = ceil_steps(r.conn_delay_ms[ci], dt);
+    Edge e{0, static_cast<uint32_t>(ci), local ? static_cast<int32_t>(dst - g0) : -1, gi,
+           instance, r.conn_weight[ci], d, -1};
+    if (r.conn_from_source[ci]) {
+      if (r.conn_src[ci] >= static_cast<uint32_t>(r.n_sources))
+        engine_error("connection source out of range");
+      e.src_key = 0xFFFFFFFFu;
+      e.source = static_cast<int32_t>(r.conn_src[ci]);
+    } else {
+      if (r.conn_src[ci] >= static_cast<uint32_t>(r.n_cells))
+        engine_error("connection src out of range");
+      if (r.conn_delay_ms[ci] < dt * (1.0 - 1e-12))
+        engine_error("configuration: dt exceeds a connection delay");
+      if (m.min_delay_steps < 0 || d < m.min_delay_steps) m.min_delay_steps = d;
+      e.src_key = r.conn_src[ci];
+    }
+    if (local) edges.push_back(e);
+  }
+  // rank order: (src_key, seq) — EventOrder (engine.cpp:25-31)
+  std::stable_sort(edges.begin(), edges.end(), [](const Edge& a, const Edge& b) {
+    if (a.src_key != b.src_key) return a.src_key < b.src_key;
+    return a.seq < b.seq;
+  });
+  const int64_t ne = static_cast<int64_t>(edges.size());
+  m.e_dst.resize(ne);
+  m.e_group.resize(ne);
+  m.e_inst.resize(ne);
+  m.e_weight.resize(ne);
+  m.e_delay.resize(ne);
+  m.out_begin.assign(r.n_cells, 0);
+  m.out_end.assign(r.n_cells, 0);
+  std::vector<std::vector<int64_t>> src_lists(r.n_sources);
+  for (int64_t i = 0; i < ne; ++i) {
+    const Edge& e = edges[i];
+    m.e_dst[i] = e.dst_local;
+    m.e_group[i] = e.group;
+    m.e_inst[i] = e.inst;
+    m.e_weight[i] = e.w;
+    m.e_delay[i] = e.delay;
+    m.max_delay_steps = std::max(m.max_delay_steps, e.delay);
+    if (e.source < 0) {
+      if (m.out_end[e.src_key] == 0 && m.out_begin[e.src_key] == 0) m.out_begin[e.src_key] = i;
+      m.out_end[e.src_key] = i + 1;
+    } else {
+      src_lists[e.source].push_back(i);
+    }
+  }
+  m.src_edge_off.assign(r.n_sources + 1, 0);
+  for (int s = 0; s < r.n_sources; ++s) {
+    m.src_edge_off[s + 1] = m.src_edge_off[s] + static_cast<int64_t>(src_lists[s].size());
+    for (int64_t x : src_lists[s]) m.src_edges.push_back(x);
+  }
+
+  // flatten instances
+  m.cgs.resize(cgs);
+  int64_t ninst = 0;
+  for (int64_t cg = 0; cg < cgs; ++cg) ninst += static_cast<int64_t>(inst_comp[cg].size());
+  m.i_comp.resize(ninst);
+  m.i_weight.resize(ninst);
+  m.i_kernel.assign(ninst, 0.0);
+  m.i_stdp_pre.assign(ninst, 0.0);
+  m.i_stdp_post.assign(ninst, 0.0);
+  m.i_stdp_w.assign(ninst, 0.0);
+  m.i_stdp_last.assign(ninst, 0);
+  m.i_homeo_w.assign(ninst, 0.0);
+  m.i_stc_h.assign(ninst, 0.0);
+  m.i_stc_z.assign(ninst, 0.0);
+  m.i_stc_c.assign(ninst, 0.0);
+  m.i_sps_abs.assign(ninst, 0.0);
+  // number of connections per (cg) for fifo sizing
+  std::vector<int64_t> cg_conns(cgs, 0);
+  for (const Edge& e : edges) cg_conns[m.cg_off[e.dst_local] + e.group] += 1;
+  int64_t off = 0;
+  for (int c = 0; c < nl; ++c) {
+    const McgKind& K = m.kinds[m.cell_kind[c]];
+    for (int gi = 0; gi < K.n_groups; ++gi) {
+      const int64_t cg = m.cg_off[c] + gi;
+      const McgSpec& S = m.specs[K.spec0 + gi];
+      McgCellGroup& G = m.cgs[cg];
+      G.inst = off;
+      G.size = static_cast<int32_t>(inst_comp[cg].size());
+      G.active_n = 0;
+      G.spec = K.spec0 + gi;
+      G.fifo = -1;
+      for (int i = 0; i < G.size; ++i) {
+        const int64_t j = off + i;
+        m.i_comp[j] = inst_comp[cg][i];
+        m.i_weight[j] = inst_w[cg][i];
+        if (S.kind == MCG_SYN_STDP_COND) m.i_stdp_w[j] = inst_w[cg][i];
+        if (S.kind == MCG_SYN_HOMEO_CURRENT) m.i_homeo_w[j] = r.kinds[m.cell_kind[c]].placements[gi].syn.homeo.w_init_nA;
+        if (S.kind == MCG_SYN_STC_CHARGE) m.i_stc_h[j] = S.h0;
+      }
+      if (S.kind == MCG_SYN_STC_CHARGE && G.size > 0) {
+        // delayed-calcium queue: at most one entry per delivered event within
+        // the delay window; start generous and let the engine grow it
+        int64_t want = std::max<int64_t>(64, 8 * static_cast<int64_t>(G.size));
+        const int64_t bound = cg_conns[cg] * (S.ca_delay + 1) + 8;
+        want = std::min(want, std::max<int64_t>(bound, 16));
+        int64_t cap = 16;
+        while (cap < want) cap <<= 1;
+        McgFifo F{};
+        F.base = m.fifo_total;
+        F.cap = static_cast<int32_t>(cap);
+        m.fifo_total += cap;
+        G.fifo = static_cast<int32_t>(m.fifos.size());
+        m.fifos.push_back(F);
+      }
+      off += G.size;
+      m.total_syn += G.size;
+      if (S.kind == MCG_SYN_STC_CHARGE) m.stc_syn += G.size;
+    }
+  }
+
+  // ---- sources (generate_source_events, engine.cpp:831-873) ----
+  m.sources.resize(r.n_sources);
+  for (int s = 0; s < r.n_sources; ++s) {
+    const mcg_source& fs = r.sources[s];
+    Source& S = m.sources[s];
+    S.type = fs.type;
+    if (fs.type == MCG_SRC_POISSON) {
+      for (int i = 0; i + 2 < fs.n_values; i += 3) {
+        S.t0.push_back(fs.values[i]);
+        S.t1.push_back(fs.values[i + 1]);
+        S.prob.push_back(fs.values[i + 2] * dt * 1e-3);
+        S.a.push_back(ceil_steps(fs.values[i], dt));
+        S.b.push_back(ceil_steps(fs.values[i + 1], dt));
+      }
+    } else if (fs.type == MCG_SRC_REGULAR) {
+      S.r_t0 = fs.t0_ms;
+      S.r_period = fs.period_ms;
+      S.r_count = fs.count;
+    } else {
+      for (int i = 0; i < fs.n_values; ++i) S.steps.push_back(ceil_steps(fs.values[i], dt));
+    }
+  }
+
+  // ---- probes (engine.cpp:393-403) ----
+  m.probes.resize(r.n_probes);
+  for (int i = 0; i < r.n_probes; ++i) {
+    McgProbe& P = m.probes[i];
+    P.gid = r.probe_gid[i];
+    P.local = (P.gid >= g0 && P.gid < g1) ? static_cast<int32_t>(P.gid - g0) : -1;
+    P.what = r.probe_what[i];
+    P.comp = r.probe_comp[i];
+    P.species = r.probe_species[i];
+    P.group = r.probe_group[i];
+    P.instance = r.probe_instance[i];
+    P.every = r.probe_every[i] < 1 ? 1 : r.probe_every[i];
+    P.out = 0;
+  }
+
+  // ---- totals ----
+  for (int c = 0; c < nl; ++c) {
+    const McgKind& K = m.kinds[m.cell_kind[c]];
+    m.total_comps += K.n;
+    m.species_comps += static_cast<int64_t>(K.n) * K.n_species;
+    if (K.dyn == MCG_DYN_HH)
+      for (int i = 0; i < K.n; ++i)
+        if (m.k_g_na[K.arr + i] != 0.0) ++m.hh_comps;
+  }
+}
+
+}  // namespace mcg

@@ -1,0 +1,105 @@
+// mcg_build.h — host-side materialization of a recipe into the device layout.
+//
+// Restates Engine::Impl::build / build_kind / append_instance
+// (engine.cpp:189-408) and discretize (morphology.cpp:67-143) in C++: the
+// same expressions in the same order, so every constant the kernels consume
+// is bitwise the value the reference computes.  The result is a set of flat
+// host vectors that mcg_engine.cu uploads once.
+#pragma once
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/mcg.h"
+#include "mcg_model.h"
+
+namespace mcg {
+
+struct Error : std::runtime_error {
+  mcg_status code;
+  Error(mcg_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+// CompartmentGrid (morphology.hpp:36-53)
+struct Grid {
+  std::vector<double> length, area, xs, volume;
+  std::vector<int32_t> parent;
+  std::vector<uint8_t> tag;
+  std::vector<uint32_t> segment_of;
+  double total_volume = 0;
+  int size() const { return static_cast<int>(length.size()); }
+};
+
+Grid discretize(const mcg_kind& k);
+int64_t ceil_steps(double t_ms, double dt_ms);
+
+struct Source {
+  int32_t type;
+  std::vector<double> t0, t1, prob;   // poisson windows (prob = rate*dt*1e-3)
+  std::vector<int64_t> a, b;           // poisson window step bounds
+  std::vector<int64_t> steps;          // scripted: ceil_steps of each time
+  double r_t0 = 0, r_period = 0;       // regular
+  int64_t r_count = 0;
+};
+
+struct HostModel {
+  double dt = 0;
+  uint64_t seed = 0;
+  int32_t rank = 0, world = 1;
+  int32_t n_cells_global = 0;
+  uint32_t gid_begin = 0, gid_end = 0;  // local shard [begin, end)
+  int64_t min_delay_steps = -1;
+
+  // kinds
+  std::vector<McgKind> kinds;
+  std::vector<Grid> grids;
+  std::vector<int32_t> k_parent;
+  std::vector<double> k_cap_dt, k_g_leak, k_g_leak_rhs, k_axial, k_g_na, k_g_k, k_cf, k_volume;
+  std::vector<double> k_sp_cap_dt, k_sp_gs, k_sp_coupling, k_sp_init;
+  std::vector<double> k_sp_decay_tau;  // per kind species (for fast-forward)
+  std::vector<int64_t> k_sp_off;       // per kind: offset into k_sp_decay_tau
+  std::vector<McgSpec> specs;
+
+  // local cells
+  std::vector<int32_t> cell_kind;
+  std::vector<int64_t> comp_off, sp_off, cg_off;
+  std::vector<double> v, hh_m, hh_h, hh_n, species;
+  std::vector<double> det_prev;
+  std::vector<int32_t> armed;
+  std::vector<int64_t> refr_until;
+  std::vector<uint32_t> internal_seq;
+
+  // synapse groups and instances
+  std::vector<McgCellGroup> cgs;
+  std::vector<int32_t> i_comp;
+  std::vector<double> i_weight, i_kernel, i_stdp_pre, i_stdp_post, i_stdp_w, i_homeo_w;
+  std::vector<int64_t> i_stdp_last;
+  std::vector<double> i_stc_h, i_stc_z, i_stc_c, i_sps_abs;
+  std::vector<McgFifo> fifos;
+  int64_t fifo_total = 0;
+
+  // edges with a local destination, sorted by (src_key, seq) -> rank
+  std::vector<int32_t> e_dst, e_group;
+  std::vector<uint32_t> e_inst;
+  std::vector<double> e_weight;
+  std::vector<int64_t> e_delay;
+  std::vector<int64_t> out_begin, out_end;  // per global gid
+  std::vector<int64_t> src_edge_off;        // per source CSR into src_edges
+  std::vector<int64_t> src_edges;           // ranks
+  int64_t max_delay_steps = 0;
+
+  std::vector<Source> sources;
+  std::vector<McgProbe> probes;
+
+  // totals (stats)
+  int64_t total_comps = 0, total_syn = 0, stc_syn = 0, hh_comps = 0, species_comps = 0;
+};
+
+// Materialize; throws mcg::Error with the reference's messages.
+void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m);
+
+// Shard assignment: contiguous gid ranges balanced by (compartments +
+// synapse instances); identical on every rank.
+void partition(const mcg_recipe& r, int world, std::vector<uint32_t>& bounds);
+
+}  // namespace mcg

@@ -1,0 +1,300 @@
+// mcg_device.cuh — device-side state view and the per-cell mechanism code.
+//
+// One warp owns one cell for a whole min-delay epoch (cells are independent
+// inside an epoch: engine.cpp:913-942).  Work that the reference does as an
+// order-dependent fold (event delivery, active-list conductance sums, the SPS
+// fold, the Hines sweep) runs on lane 0 in the reference's order; work that
+// is independent per synapse instance (STC early/late phase, kernel decay,
+// STDP/homeostasis/STC post-spike hooks) runs across the 32 lanes.
+//
+// Mechanism ABI mapping (Arbor names -> reference code -> here):
+//   init              Impl::build / append_instance   -> mcg_build.cpp
+//   apply_events      apply_event  (engine.cpp:452)    -> mcg_apply_event
+//   advance_state     step_cell §2 (engine.cpp:575)    -> mcg_advance_*
+//   compute_currents  step_cell §2-3 (:578-664)        -> gsyn / rhs_current folds
+//   post_event        post_event (engine.cpp:515)      -> mcg_post_event
+#pragma once
+#include <stdint.h>
+
+#include "../../include/mcg.h"
+#include "mcg_model.h"
+#include "mcg_rng.h"
+
+#define MCG_FULL 0xffffffffu
+#define MCG_ERR_FLAG_SINGULAR 1
+#define MCG_ERR_FLAG_FIFO 2
+#define MCG_ERR_FLAG_ACTIVE 4
+#define MCG_ERR_FLAG_SPIKES 8
+
+struct McgDev {
+  double dt;
+  uint64_t seed;
+  // kinds
+  const McgKind* kinds;
+  const McgSpec* specs;
+  const int32_t* k_parent;
+  const double *k_cap_dt, *k_g_leak, *k_g_leak_rhs, *k_axial, *k_g_na, *k_g_k, *k_cf, *k_volume;
+  const double *k_sp_cap_dt, *k_sp_gs, *k_sp_coupling;
+  // cells
+  int32_t n_cells;
+  uint32_t gid0;
+  const int32_t* cell_kind;
+  const int64_t *comp_off, *sp_off, *cg_off;
+  double *v, *hh_m, *hh_h, *hh_n, *species, *det_prev;
+  int32_t* armed;
+  int64_t* refr_until;
+  uint32_t* internal_seq;
+  // per-compartment scratch
+  double *s_gsyn, *s_gsyn_rhs, *s_rhs_cur, *s_diag, *s_rhs;
+  // groups, instances
+  McgCellGroup* cgs;
+  McgFifo* fifos;
+  int64_t* fifo_step;
+  uint64_t* fifo_si;
+  const int32_t* i_comp;
+  double *i_weight, *i_kernel;
+  int32_t* i_active;
+  double *i_stdp_pre, *i_stdp_post, *i_stdp_w;
+  int64_t* i_stdp_last;
+  double* i_homeo_w;
+  double *i_stc_h, *i_stc_z, *i_stc_c, *i_sps_abs;
+  // events of this epoch (sorted keys) and the edge table
+  const uint64_t* keys;
+  const int64_t* ev_begin;  // n_cells + 1
+  int64_t* ev_cursor;       // n_cells
+  int32_t rank_bits, step_bits;
+  int64_t key_base;         // step of key step-field 0
+  const int32_t* e_dst;
+  const int32_t* e_group;
+  const uint32_t* e_inst;
+  const double* e_weight;
+  const int64_t* e_delay;
+  // spikes of this epoch: [cell][sp_cap]
+  int32_t sp_cap;
+  int32_t* sp_count;
+  int64_t* sp_step;
+  double* sp_t;
+  // probes: per-cell CSR of probe indices, per-probe output
+  const McgProbe* probes;
+  const int32_t* probe_off;
+  const int32_t* probe_idx;
+  double* trace_buf;
+  const int64_t* trace_base;  // per probe
+  int64_t call_first;         // first step of the current advance call
+  // status
+  int32_t* err;
+  unsigned long long* delivered;
+};
+
+__device__ __forceinline__ unsigned mcg_lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// stdp_decay (mechanisms.hpp:35-38)
+__device__ __forceinline__ void mcg_stdp_decay(double& pre, double& post, const McgSpec& S,
+                                               double gap) {
+  pre *= mcg_exp(-gap / S.tau_pre);
+  post *= mcg_exp(-gap / S.tau_post);
+}
+
+// ---- apply_events (engine.cpp:452-513); lane 0 only -----------------------
+__device__ void mcg_apply_event(const McgDev& D, const McgKind& K, int c, int64_t cg0,
+                                int64_t co, int32_t group, uint32_t inst, double w, int etype,
+                                bool refractory, int64_t s) {
+  McgCellGroup& G = D.cgs[cg0 + group];
+  const McgSpec& S = D.specs[G.spec];
+  const int64_t j = G.inst + inst;
+  switch (S.kind) {
+    case MCG_SYN_STATIC_CHARGE:
+      if (!refractory && w != 0.0) {
+        const int comp = D.i_comp[j];
+        D.v[co + comp] += w * D.k_cf[K.arr + comp];
+      }
+      break;
+    case MCG_SYN_STATIC_COND:
+    case MCG_SYN_STATIC_CURRENT:
+      if (w != 0.0) {
+        if (D.i_kernel[j] == 0.0) {
+          if (G.active_n >= G.size) atomicOr(D.err, MCG_ERR_FLAG_ACTIVE);
+          else D.i_active[G.inst + G.active_n++] = static_cast<int32_t>(inst);
+        }
+        D.i_kernel[j] += w;
+      }
+      break;
+    case MCG_SYN_STDP_COND: {
+      double pre = D.i_stdp_pre[j], post = D.i_stdp_post[j];
+      const double gap = double(s - D.i_stdp_last[j]) * D.dt;
+      if (gap > 0) mcg_stdp_decay(pre, post, S, gap);
+      D.i_stdp_last[j] = s;
+      pre += S.a_pre;  // stdp_on_pre
+      const double ww = D.i_stdp_w[j] + post;
+      D.i_stdp_pre[j] = pre;
+      D.i_stdp_post[j] = post;
+      D.i_stdp_w[j] = ww;
+      const double weff = fmin(fmax(ww, 0.0), S.wmax);
+      if (weff != 0.0) {
+        if (D.i_kernel[j] == 0.0) {
+          if (G.active_n >= G.size) atomicOr(D.err, MCG_ERR_FLAG_ACTIVE);
+          else D.i_active[G.inst + G.active_n++] = static_cast<int32_t>(inst);
+        }
+        D.i_kernel[j] += weff;
+      }
+      break;
+    }
+    case MCG_SYN_HOMEO_CURRENT: {
+      const double hw = fmin(D.i_homeo_w[j] + S.dw_plus, S.h_wmax);
+      D.i_homeo_w[j] = hw;
+      if (hw != 0.0) {
+        if (D.i_kernel[j] == 0.0) {
+          if (G.active_n >= G.size) atomicOr(D.err, MCG_ERR_FLAG_ACTIVE);
+          else D.i_active[G.inst + G.active_n++] = static_cast<int32_t>(inst);
+        }
+        D.i_kernel[j] += hw;
+      }
+      break;
+    }
+    case MCG_SYN_STC_CHARGE: {
+      if (etype == 1) {
+        D.i_stc_c[j] += S.cpre_s;  // stc_on_pre_calcium
+      } else {
+        // delayed calcium: internal event at s + delay, seq = internal_seq++
+        McgFifo& F = D.fifos[G.fifo];
+        if (F.tail - F.head >= F.cap) {
+          atomicOr(D.err, MCG_ERR_FLAG_FIFO);
+        } else {
+          const int64_t slot = F.base + (F.tail % F.cap);
+          D.fifo_step[slot] = s + S.ca_delay;
+          D.fifo_si[slot] = (uint64_t(D.internal_seq[c]) << 32) | uint64_t(inst);
+          ++F.tail;
+        }
+        ++D.internal_seq[c];
+        if (!refractory) {
+          const int comp = D.i_comp[j];
+          const double tw = D.i_stc_h[j] + S.h0 * D.i_stc_z[j];
+          D.v[co + comp] += tw * w * D.k_cf[K.arr + comp];
+        }
+      }
+      break;
+    }
+  }
+}
+
+// solve_tree (tree_solver.cpp:46-74), lane 0; returns false if singular
+__device__ bool mcg_solve_tree(int n, const int32_t* par, const double* cap, const double* gs,
+                               const double* coup, const double* rhs, double* v, double* diag,
+                               double* r2) {
+  for (int i = 0; i < n; ++i) {
+    diag[i] = cap[i] + gs[i];
+    r2[i] = cap[i] * v[i] + rhs[i];
+  }
+  for (int i = 1; i < n; ++i) {
+    diag[i] += coup[i];
+    diag[par[i]] += coup[i];
+  }
+  for (int i = n - 1; i >= 1; --i) {
+    if (diag[i] <= 0.0) return false;
+    const double f = coup[i] / diag[i];
+    diag[par[i]] -= f * coup[i];
+    r2[par[i]] += f * r2[i];
+  }
+  if (diag[0] <= 0.0) return false;
+  v[0] = r2[0] / diag[0];
+  for (int i = 1; i < n; ++i) v[i] = (r2[i] + coup[i] * v[par[i]]) / diag[i];
+  return true;
+}
+
+// HH rates (engine.cpp:41-54) with the glibc-faithful exp
+__device__ __forceinline__ double mcg_hh_am(double v) {
+  const double x = v + 40.0;
+  if (fabs(x) < 1e-7) return 1.0;
+  return 0.1 * x / (1.0 - mcg_exp(-x / 10.0));
+}
+__device__ __forceinline__ double mcg_hh_bm(double v) { return 4.0 * mcg_exp(-(v + 65.0) / 18.0); }
+__device__ __forceinline__ double mcg_hh_ah(double v) { return 0.07 * mcg_exp(-(v + 65.0) / 20.0); }
+__device__ __forceinline__ double mcg_hh_bh(double v) {
+  return 1.0 / (1.0 + mcg_exp(-(v + 35.0) / 10.0));
+}
+__device__ __forceinline__ double mcg_hh_an(double v) {
+  const double x = v + 55.0;
+  if (fabs(x) < 1e-7) return 0.1;
+  return 0.01 * x / (1.0 - mcg_exp(-x / 10.0));
+}
+__device__ __forceinline__ double mcg_hh_bn(double v) {
+  return 0.125 * mcg_exp(-(v + 65.0) / 80.0);
+}
+
+// STC early/late phase of one instance (mechanisms.hpp:213-242, engine.cpp:624-644)
+// returns true if |h-h0| changed; *delta is the SPS increment
+__device__ __forceinline__ bool mcg_stc_instance(const McgDev& D, const McgSpec& S, int64_t j,
+                                                 uint32_t gid, int gi, int i, int64_t s,
+                                                 const double* prp_base, const double* vol_k,
+                                                 double* delta, int* comp_out) {
+  double h = D.i_stc_h[j];
+  double z = D.i_stc_z[j];
+  double cc = D.i_stc_c[j];
+  const bool up = cc > S.theta_p, dn = cc > S.theta_d;
+  double nrm = 0.0;
+  if (S.sigma != 0.0 && (up || dn)) {
+    const mcg_key key = mcg_make_key(D.seed, gid, (2ull << 32) | uint64_t(gi), uint64_t(i));
+    nrm = mcg_normal_for(&key, static_cast<uint64_t>(s));
+  }
+  // stc_early_step
+  const int crossings = int(up) + int(dn);
+  double d = 0.1 * (S.h0 - h);
+  if (up) d += S.gamma_p * (10.0 - h);
+  if (dn) d -= S.gamma_d * h;
+  double dh = d / S.tau_h * D.dt;
+  if (crossings > 0 && S.sigma != 0.0) dh += (crossings == 1 ? S.nz1 : S.nz2) * nrm;
+  h += dh;
+  const int comp = D.i_comp[j];
+  *comp_out = comp;
+  const double na = fabs(h - S.h0);
+  bool changed = false;
+  if (na != D.i_sps_abs[j]) {
+    *delta = (na - D.i_sps_abs[j]) / vol_k[comp];
+    D.i_sps_abs[j] = na;
+    changed = true;
+  }
+  // stc_late_step
+  if (prp_base) {
+    const double prp = prp_base[comp];
+    if (!(prp <= 0.0)) {
+      double dd = 0.0;
+      if (h - S.h0 > S.theta_tag) dd += (1.0 - z);
+      if (S.h0 - h > S.theta_tag) dd -= (z + 0.5);
+      z += prp * S.f_int * dd * D.dt / S.tau_z;
+    }
+  }
+  cc *= S.cf;
+  D.i_stc_h[j] = h;
+  D.i_stc_z[j] = z;
+  D.i_stc_c[j] = cc;
+  return changed;
+}
+
+// probe_value (engine.cpp:795-829)
+__device__ double mcg_probe_value(const McgDev& D, const McgKind& K, int c, const McgProbe& P) {
+  const int64_t co = D.comp_off[c];
+  if (P.what == MCG_PROBE_VOLTAGE) return (K.dyn == MCG_DYN_NONE) ? 0.0 : D.v[co + P.comp];
+  if (P.what == MCG_PROBE_SPECIES)
+    return D.species[D.sp_off[c] + int64_t(P.species) * K.n + P.comp];
+  const McgCellGroup& G = D.cgs[D.cg_off[c] + P.group];
+  const McgSpec& S = D.specs[G.spec];
+  const int64_t j = G.inst + P.instance;
+  switch (P.what) {
+    case MCG_PROBE_SYN_WEIGHT:
+      switch (S.kind) {
+        case MCG_SYN_STDP_COND: return D.i_stdp_w[j];
+        case MCG_SYN_HOMEO_CURRENT: return D.i_homeo_w[j];
+        case MCG_SYN_STC_CHARGE: return D.i_stc_h[j] + S.h0 * D.i_stc_z[j];
+        default: return D.i_weight[j];
+      }
+    case MCG_PROBE_SYN_H: return D.i_stc_h[j];
+    case MCG_PROBE_SYN_Z: return D.i_stc_z[j];
+    case MCG_PROBE_SYN_C: return D.i_stc_c[j];
+    case MCG_PROBE_SYN_KERNEL: return D.i_kernel[j];
+    default: return 0.0;
+  }
+}

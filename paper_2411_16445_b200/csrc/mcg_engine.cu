@@ -1,0 +1,1028 @@
+// mcg_engine.cu — host orchestration of the B200 engine and the C ABI
+// (include/mcg.h).
+//
+// Engine::advance_to (engine.cpp:909-945) becomes, per min-delay epoch:
+//   A  k_source_fire + k_spike_outdeg  -> one small D2H read of the counters
+//   B  k_write_*_events, CUB radix sort of the 64-bit event keys, k_offsets
+//   C  k_epoch: every cell, every step of the epoch, one warp per cell
+//   D  ordered spike compaction (CUB scan + k_spike_write), leftover carry
+// All state stays resident in HBM; the host sees only counters, and spikes /
+// traces / cell state when asked (the lazily-synced mirror of engine.hpp).
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "mcg_build.h"
+#include "mcg_kernels.cuh"
+
+namespace mcg {
+
+namespace {
+
+thread_local std::string g_last_error;
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error(MCG_ERR_CUDA, std::string("cuda: ") + what + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+  void alloc(size_t count) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = count;
+    if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void upload(const std::vector<T>& v, cudaStream_t st) {
+    alloc(std::max<size_t>(v.size(), 1));
+    if (!v.empty())
+      CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+  }
+  // grow, keeping the first `keep` elements
+  void grow(size_t count, size_t keep, cudaStream_t st) {
+    if (count <= n) return;
+    T* q = nullptr;
+    CK(cudaMalloc(&q, count * sizeof(T)));
+    if (p && keep) CK(cudaMemcpyAsync(q, p, keep * sizeof(T), cudaMemcpyDeviceToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    if (p) cudaFree(p);
+    p = q;
+    n = count;
+  }
+};
+
+int bits_for(uint64_t v) {  // bits needed to represent values in [0, v]
+  int b = 1;
+  while (b < 63 && (v >> b) != 0) ++b;
+  return b;
+}
+
+// counters block (device, mirrored to pinned host memory once per epoch)
+enum {
+  C_FIRE = 0,
+  C_SRC_EV = 1,
+  C_SPK_EV = 2,
+  C_LEFT = 3,
+  C_EP_SPK = 4,
+  C_LOG = 5,
+  C_WCUR = 6,
+  C_DELIVERED = 7,
+  C_N = 8
+};
+
+}  // namespace
+
+struct Engine {
+  HostModel m;
+  cudaStream_t st = nullptr;
+  int device = 0;
+  int64_t step = 0;
+  int64_t free_epoch = 1024;  // epoch length when there are no cell-to-cell edges
+  int64_t max_epoch = 1;
+
+  // device model
+  DBuf<McgKind> d_kinds;
+  DBuf<McgSpec> d_specs;
+  DBuf<int32_t> d_k_parent;
+  DBuf<double> d_k_cap_dt, d_k_g_leak, d_k_g_leak_rhs, d_k_axial, d_k_g_na, d_k_g_k, d_k_cf,
+      d_k_volume, d_k_sp_cap_dt, d_k_sp_gs, d_k_sp_coupling;
+  DBuf<int32_t> d_cell_kind;
+  DBuf<int64_t> d_comp_off, d_sp_off, d_cg_off;
+  DBuf<double> d_v, d_hh_m, d_hh_h, d_hh_n, d_species, d_det_prev;
+  DBuf<int32_t> d_armed;
+  DBuf<int64_t> d_refr;
+  DBuf<uint32_t> d_iseq;
+  DBuf<double> d_s_gsyn, d_s_gsyn_rhs, d_s_rhs_cur, d_s_diag, d_s_rhs;
+  DBuf<McgCellGroup> d_cgs;
+  DBuf<McgFifo> d_fifos;
+  DBuf<int64_t> d_fifo_step;
+  DBuf<uint64_t> d_fifo_si;
+  DBuf<int32_t> d_i_comp, d_i_active;
+  DBuf<double> d_i_weight, d_i_kernel, d_i_stdp_pre, d_i_stdp_post, d_i_stdp_w, d_i_homeo_w,
+      d_i_stc_h, d_i_stc_z, d_i_stc_c, d_i_sps_abs;
+  DBuf<int64_t> d_i_stdp_last;
+  // edges
+  DBuf<int32_t> d_e_dst, d_e_group;
+  DBuf<uint32_t> d_e_inst;
+  DBuf<double> d_e_weight;
+  DBuf<int64_t> d_e_delay, d_out_begin, d_out_end, d_src_edge_off, d_src_edges;
+  int32_t rank_bits = 1, step_bits = 1, dst_bits = 1;
+  // sources
+  DBuf<McgSrcTask> d_tasks;
+  DBuf<int64_t> d_scripted;
+  DBuf<int32_t> d_fire_src;
+  DBuf<int64_t> d_fire_step;
+  int32_t n_tasks = 0;
+  int64_t fire_cap = 0;
+  // events
+  DBuf<uint64_t> d_keys_work, d_keys_sorted;
+  DBuf<int64_t> d_ev_begin, d_ev_cursor, d_left, d_left_scan;
+  DBuf<unsigned char> d_cub_tmp;
+  int64_t key_base = 0;
+  // spikes
+  int32_t sp_cap = 1;
+  DBuf<int32_t> d_sp_count;
+  DBuf<int64_t> d_sp_step, d_sp_scan;
+  DBuf<double> d_sp_t;
+  DBuf<uint32_t> d_ep_gid;
+  DBuf<int64_t> d_ep_step;
+  DBuf<double> d_log_t;
+  DBuf<uint32_t> d_log_gid;
+  // probes
+  DBuf<McgProbe> d_probes;
+  DBuf<int32_t> d_probe_off, d_probe_idx;
+  DBuf<double> d_trace;
+  DBuf<int64_t> d_trace_base;
+  std::vector<std::vector<std::pair<double, double>>> traces;
+  // status
+  DBuf<unsigned long long> d_ctr;
+  DBuf<int32_t> d_err;
+  unsigned long long* h_ctr = nullptr;
+  int32_t* h_err = nullptr;
+  // host spike mirror
+  std::vector<double> spk_t;
+  std::vector<uint32_t> spk_gid;
+  int64_t log_count = 0;   // device log length at the last sync
+  int64_t host_synced = 0; // mirrored prefix
+  // stats
+  mcg_stats stats{};
+  bool timing = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool ev_pending = false;
+
+  McgDev dev{};
+
+  ~Engine() {
+    if (h_ctr) cudaFreeHost(h_ctr);
+    if (h_err) cudaFreeHost(h_err);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (st) cudaStreamDestroy(st);
+  }
+
+  int32_t n_local() const { return static_cast<int32_t>(m.cell_kind.size()); }
+
+  void init(const mcg_recipe& r, const mcg_options& opt) {
+    device = opt.device;
+    CK(cudaSetDevice(device));
+    build_model(r, opt, m);
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CK(cudaMallocHost(&h_ctr, C_N * sizeof(unsigned long long)));
+    CK(cudaMallocHost(&h_err, sizeof(int32_t)));
+    CK(cudaEventCreate(&ev0));
+    CK(cudaEventCreate(&ev1));
+    const int nl = n_local();
+    // epoch bounds
+    free_epoch = std::clamp<int64_t>((int64_t(1) << 22) / std::max(nl, 1), 16, 4096);
+    max_epoch = m.min_delay_steps > 0 ? m.min_delay_steps : free_epoch;
+    sp_cap = static_cast<int32_t>(max_epoch);
+    // key layout: dst | step | rank
+    const int64_t ne = static_cast<int64_t>(m.e_dst.size());
+    rank_bits = bits_for(static_cast<uint64_t>(std::max<int64_t>(ne, 1)));
+    dst_bits = bits_for(static_cast<uint64_t>(std::max(nl, 1)));
+    int64_t max_step_rel = m.max_delay_steps + 2 * max_epoch + 2;
+    step_bits = bits_for(static_cast<uint64_t>(max_step_rel));
+    if (rank_bits + step_bits + dst_bits > 64)
+      throw Error(MCG_ERR_ENGINE, "event key exceeds 64 bits (too many edges/cells/delay steps)");
+
+    d_kinds.upload(m.kinds, st);
+    d_specs.upload(m.specs, st);
+    d_k_parent.upload(m.k_parent, st);
+    d_k_cap_dt.upload(m.k_cap_dt, st);
+    d_k_g_leak.upload(m.k_g_leak, st);
+    d_k_g_leak_rhs.upload(m.k_g_leak_rhs, st);
+    d_k_axial.upload(m.k_axial, st);
+    d_k_g_na.upload(m.k_g_na, st);
+    d_k_g_k.upload(m.k_g_k, st);
+    d_k_cf.upload(m.k_cf, st);
+    d_k_volume.upload(m.k_volume, st);
+    d_k_sp_cap_dt.upload(m.k_sp_cap_dt, st);
+    d_k_sp_gs.upload(m.k_sp_gs, st);
+    d_k_sp_coupling.upload(m.k_sp_coupling, st);
+    d_cell_kind.upload(m.cell_kind, st);
+    d_comp_off.upload(m.comp_off, st);
+    d_sp_off.upload(m.sp_off, st);
+    d_cg_off.upload(m.cg_off, st);
+    d_v.upload(m.v, st);
+    d_hh_m.upload(m.hh_m, st);
+    d_hh_h.upload(m.hh_h, st);
+    d_hh_n.upload(m.hh_n, st);
+    d_species.upload(m.species, st);
+    d_det_prev.upload(m.det_prev, st);
+    d_armed.upload(m.armed, st);
+    d_refr.upload(m.refr_until, st);
+    d_iseq.upload(m.internal_seq, st);
+    const size_t nc = std::max<size_t>(m.v.size(), 1) + 1;
+    d_s_gsyn.alloc(nc);
+    d_s_gsyn_rhs.alloc(nc);
+    d_s_rhs_cur.alloc(nc);
+    d_s_diag.alloc(nc);
+    d_s_rhs.alloc(nc);
+    d_cgs.upload(m.cgs, st);
+    d_fifos.upload(m.fifos, st);
+    d_fifo_step.alloc(std::max<int64_t>(m.fifo_total, 1));
+    d_fifo_si.alloc(std::max<int64_t>(m.fifo_total, 1));
+    d_i_comp.upload(m.i_comp, st);
+    d_i_active.alloc(std::max<size_t>(m.i_comp.size(), 1));
+    d_i_weight.upload(m.i_weight, st);
+    d_i_kernel.upload(m.i_kernel, st);
+    d_i_stdp_pre.upload(m.i_stdp_pre, st);
+    d_i_stdp_post.upload(m.i_stdp_post, st);
+    d_i_stdp_w.upload(m.i_stdp_w, st);
+    d_i_stdp_last.upload(m.i_stdp_last, st);
+    d_i_homeo_w.upload(m.i_homeo_w, st);
+    d_i_stc_h.upload(m.i_stc_h, st);
+    d_i_stc_z.upload(m.i_stc_z, st);
+    d_i_stc_c.upload(m.i_stc_c, st);
+    d_i_sps_abs.upload(m.i_sps_abs, st);
+    d_e_dst.upload(m.e_dst, st);
+    d_e_group.upload(m.e_group, st);
+    d_e_inst.upload(m.e_inst, st);
+    d_e_weight.upload(m.e_weight, st);
+    d_e_delay.upload(m.e_delay, st);
+    d_out_begin.upload(m.out_begin, st);
+    d_out_end.upload(m.out_end, st);
+    d_src_edge_off.upload(m.src_edge_off, st);
+    d_src_edges.upload(m.src_edges, st);
+
+    // source tasks
+    std::vector<McgSrcTask> tasks;
+    std::vector<int64_t> scripted;
+    fire_cap = 0;
+    for (size_t s = 0; s < m.sources.size(); ++s) {
+      const Source& S = m.sources[s];
+      if (S.type == MCG_SRC_POISSON) {
+        for (size_t w = 0; w < S.prob.size(); ++w) {
+          McgSrcTask T{};
+          T.source = static_cast<int32_t>(s);
+          T.type = MCG_SRC_POISSON;
+          T.window = static_cast<int32_t>(w);
+          T.a = S.a[w];
+          T.b = S.b[w];
+          T.prob = S.prob[w];
+          tasks.push_back(T);
+          fire_cap += max_epoch;
+        }
+      } else if (S.type == MCG_SRC_REGULAR) {
+        McgSrcTask T{};
+        T.source = static_cast<int32_t>(s);
+        T.type = MCG_SRC_REGULAR;
+        T.r_t0 = S.r_t0;
+        T.r_period = S.r_period;
+        T.r_count = S.r_count;
+        tasks.push_back(T);
+        fire_cap += max_epoch + 4;
+      } else {
+        McgSrcTask T{};
+        T.source = static_cast<int32_t>(s);
+        T.type = MCG_SRC_SCRIPTED;
+        T.a = static_cast<int64_t>(scripted.size());
+        for (int64_t x : S.steps) scripted.push_back(x);
+        T.b = static_cast<int64_t>(scripted.size());
+        tasks.push_back(T);
+        fire_cap += static_cast<int64_t>(S.steps.size());
+      }
+    }
+    n_tasks = static_cast<int32_t>(tasks.size());
+    d_tasks.upload(tasks, st);
+    d_scripted.upload(scripted, st);
+    fire_cap = std::max<int64_t>(fire_cap, 1);
+    d_fire_src.alloc(fire_cap);
+    d_fire_step.alloc(fire_cap);
+
+    // events and spikes
+    d_keys_work.alloc(1024);
+    d_keys_sorted.alloc(1024);
+    d_ev_begin.alloc(nl + 1);
+    d_ev_cursor.alloc(std::max(nl, 1));
+    d_left.alloc(std::max(nl, 1));
+    d_left_scan.alloc(std::max(nl, 1));
+    d_sp_count.alloc(std::max(nl, 1));
+    d_sp_scan.alloc(std::max(nl, 1));
+    d_sp_step.alloc(static_cast<size_t>(std::max(nl, 1)) * sp_cap);
+    d_sp_t.alloc(static_cast<size_t>(std::max(nl, 1)) * sp_cap);
+    d_ep_gid.alloc(static_cast<size_t>(std::max(nl, 1)) * sp_cap);
+    d_ep_step.alloc(static_cast<size_t>(std::max(nl, 1)) * sp_cap);
+    d_log_t.alloc(4096);
+    d_log_gid.alloc(4096);
+    ensure_cub(1024);
+
+    // probes: per-cell CSR over local probes
+    std::vector<int32_t> poff(nl + 1, 0), pidx;
+    for (const auto& P : m.probes)
+      if (P.local >= 0) ++poff[P.local + 1];
+    for (int c = 0; c < nl; ++c) poff[c + 1] += poff[c];
+    pidx.resize(poff[nl]);
+    {
+      std::vector<int32_t> fill(poff.begin(), poff.end() - 1);
+      for (size_t p = 0; p < m.probes.size(); ++p)
+        if (m.probes[p].local >= 0) pidx[fill[m.probes[p].local]++] = static_cast<int32_t>(p);
+    }
+    d_probes.upload(m.probes, st);
+    d_probe_off.upload(poff, st);
+    d_probe_idx.upload(pidx, st);
+    d_trace.alloc(1);
+    d_trace_base.alloc(std::max<size_t>(m.probes.size(), 1));
+    traces.assign(m.probes.size(), {});
+
+    d_ctr.alloc(C_N);
+    d_err.alloc(1);
+    CK(cudaMemsetAsync(d_ctr.p, 0, C_N * sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(d_err.p, 0, sizeof(int32_t), st));
+    CK(cudaMemsetAsync(d_sp_count.p, 0, std::max(nl, 1) * sizeof(int32_t), st));
+    CK(cudaStreamSynchronize(st));
+
+    stats.total_comps = m.total_comps;
+    stats.total_synapses = m.total_syn;
+    stats.stc_synapses = m.stc_syn;
+    stats.hh_comps = m.hh_comps;
+    stats.species_comps = m.species_comps;
+    refresh_dev();
+  }
+
+  void ensure_cub(int64_t n) {
+    size_t need = 0, need2 = 0;
+    CK(cub::DeviceRadixSort::SortKeys(nullptr, need, d_keys_work.p, d_keys_sorted.p,
+                                      static_cast<int>(n), 0, 64, st));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, need2, d_sp_count.p, d_sp_scan.p,
+                                     std::max(n_local(), 1), st));
+    size_t need3 = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, need3, d_left.p, d_left_scan.p,
+                                     std::max(n_local(), 1), st));
+    need = std::max(need, std::max(need2, need3));
+    if (need > d_cub_tmp.n) d_cub_tmp.alloc(need * 2);
+  }
+
+  void refresh_dev() {
+    McgDev& D = dev;
+    D.dt = m.dt;
+    D.seed = m.seed;
+    D.kinds = d_kinds.p;
+    D.specs = d_specs.p;
+    D.k_parent = d_k_parent.p;
+    D.k_cap_dt = d_k_cap_dt.p;
+    D.k_g_leak = d_k_g_leak.p;
+    D.k_g_leak_rhs = d_k_g_leak_rhs.p;
+    D.k_axial = d_k_axial.p;
+    D.k_g_na = d_k_g_na.p;
+    D.k_g_k = d_k_g_k.p;
+    D.k_cf = d_k_cf.p;
+    D.k_volume = d_k_volume.p;
+    D.k_sp_cap_dt = d_k_sp_cap_dt.p;
+    D.k_sp_gs = d_k_sp_gs.p;
+    D.k_sp_coupling = d_k_sp_coupling.p;
+    D.n_cells = n_local();
+    D.gid0 = m.gid_begin;
+    D.cell_kind = d_cell_kind.p;
+    D.comp_off = d_comp_off.p;
+    D.sp_off = d_sp_off.p;
+    D.cg_off = d_cg_off.p;
+    D.v = d_v.p;
+    D.hh_m = d_hh_m.p;
+    D.hh_h = d_hh_h.p;
+    D.hh_n = d_hh_n.p;
+    D.species = d_species.p;
+    D.det_prev = d_det_prev.p;
+    D.armed = d_armed.p;
+    D.refr_until = d_refr.p;
+    D.internal_seq = d_iseq.p;
+    D.s_gsyn = d_s_gsyn.p;
+    D.s_gsyn_rhs = d_s_gsyn_rhs.p;
+    D.s_rhs_cur = d_s_rhs_cur.p;
+    D.s_diag = d_s_diag.p;
+    D.s_rhs = d_s_rhs.p;
+    D.cgs = d_cgs.p;
+    D.fifos = d_fifos.p;
+    D.fifo_step = d_fifo_step.p;
+    D.fifo_si = d_fifo_si.p;
+    D.i_comp = d_i_comp.p;
+    D.i_weight = d_i_weight.p;
+    D.i_kernel = d_i_kernel.p;
+    D.i_active = d_i_active.p;
+    D.i_stdp_pre = d_i_stdp_pre.p;
+    D.i_stdp_post = d_i_stdp_post.p;
+    D.i_stdp_w = d_i_stdp_w.p;
+    D.i_stdp_last = d_i_stdp_last.p;
+    D.i_homeo_w = d_i_homeo_w.p;
+    D.i_stc_h = d_i_stc_h.p;
+    D.i_stc_z = d_i_stc_z.p;
+    D.i_stc_c = d_i_stc_c.p;
+    D.i_sps_abs = d_i_sps_abs.p;
+    D.keys = d_keys_sorted.p;
+    D.ev_begin = d_ev_begin.p;
+    D.ev_cursor = d_ev_cursor.p;
+    D.rank_bits = rank_bits;
+    D.step_bits = step_bits;
+    D.key_base = key_base;
+    D.e_dst = d_e_dst.p;
+    D.e_group = d_e_group.p;
+    D.e_inst = d_e_inst.p;
+    D.e_weight = d_e_weight.p;
+    D.e_delay = d_e_delay.p;
+    D.sp_cap = sp_cap;
+    D.sp_count = d_sp_count.p;
+    D.sp_step = d_sp_step.p;
+    D.sp_t = d_sp_t.p;
+    D.probes = d_probes.p;
+    D.probe_off = d_probe_off.p;
+    D.probe_idx = d_probe_idx.p;
+    D.trace_buf = d_trace.p;
+    D.trace_base = d_trace_base.p;
+    D.err = d_err.p;
+    D.delivered = d_ctr.p + C_DELIVERED;
+  }
+
+  McgSrcDev src_dev() {
+    McgSrcDev S{};
+    S.tasks = d_tasks.p;
+    S.n_tasks = n_tasks;
+    S.scripted_steps = d_scripted.p;
+    S.src_edge_off = d_src_edge_off.p;
+    S.src_edges = d_src_edges.p;
+    S.fire_src = d_fire_src.p;
+    S.fire_step = d_fire_step.p;
+    S.fire_cap = fire_cap;
+    S.ctr = d_ctr.p;
+    S.err = d_err.p;
+    return S;
+  }
+
+  McgEvDev ev_dev() {
+    McgEvDev E{};
+    E.keys = d_keys_work.p;
+    E.wcur = d_ctr.p + C_WCUR;
+    E.rank_bits = rank_bits;
+    E.step_bits = step_bits;
+    E.base = key_base;
+    E.e_dst = d_e_dst.p;
+    E.e_delay = d_e_delay.p;
+    E.out_begin = d_out_begin.p;
+    E.out_end = d_out_end.p;
+    return E;
+  }
+
+  void launched(int k = 1) { stats.kernel_launches += k; }
+
+  void check_err() {
+    if (*h_err == 0) return;
+    const int e = *h_err;
+    *h_err = 0;
+    CK(cudaMemsetAsync(d_err.p, 0, sizeof(int32_t), st));
+    if (e & MCG_ERR_FLAG_SINGULAR) throw Error(MCG_ERR_NUMERIC, "tree solve: singular system");
+    if (e & MCG_ERR_FLAG_FIFO) throw Error(MCG_ERR_ENGINE, "internal event queue overflow");
+    if (e & MCG_ERR_FLAG_ACTIVE) throw Error(MCG_ERR_ENGINE, "active synapse list overflow");
+    if (e & MCG_ERR_FLAG_SPIKES) throw Error(MCG_ERR_ENGINE, "spike/firing buffer overflow");
+  }
+
+  // counters -> host (the one synchronization point per epoch)
+  void sync_counters() {
+    CK(cudaMemcpyAsync(h_ctr, d_ctr.p, C_N * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_err, d_err.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (ev_pending) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, ev0, ev1));
+      stats.epoch_kernel_ms += ms;
+      ev_pending = false;
+    }
+    stats.events_delivered = static_cast<int64_t>(h_ctr[C_DELIVERED]);
+    log_count = static_cast<int64_t>(h_ctr[C_LOG]);
+    check_err();
+  }
+
+  void run_epoch(int64_t s0, int64_t s1) {
+    const int nl = n_local();
+    const int64_t len = s1 - s0;
+    // ---- A: count this epoch's source firings and the previous epoch's fan-out
+    CK(cudaMemsetAsync(d_ctr.p + C_FIRE, 0, 3 * sizeof(unsigned long long), st));
+    if (n_tasks > 0) {
+      const int64_t nt = int64_t(n_tasks) * len;
+      k_source_fire<<<static_cast<unsigned>((nt + 255) / 256), 256, 0, st>>>(src_dev(), m.seed,
+                                                                          m.dt, s0, s1);
+      launched();
+    }
+    const int64_t max_ep = static_cast<int64_t>(nl) * sp_cap;
+    if (max_ep > 0) {
+      k_spike_outdeg<<<static_cast<unsigned>((max_ep + 255) / 256), 256, 0, st>>>(
+          d_ep_gid.p, d_ctr.p + C_EP_SPK, d_out_begin.p, d_out_end.p, d_ctr.p + C_SPK_EV);
+      launched();
+    }
+    sync_counters();
+    const int64_t n_left = static_cast<int64_t>(h_ctr[C_LEFT]);
+    const int64_t n_fire = static_cast<int64_t>(h_ctr[C_FIRE]);
+    const int64_t n_new = static_cast<int64_t>(h_ctr[C_SRC_EV] + h_ctr[C_SPK_EV]);
+    const int64_t n_tot = n_left + n_new;
+    const int64_t n_ep = static_cast<int64_t>(h_ctr[C_EP_SPK]);
+    if (n_fire > fire_cap) throw Error(MCG_ERR_ENGINE, "source firing buffer overflow");
+    if (static_cast<size_t>(n_tot) > d_keys_work.n) {
+      const size_t cap = static_cast<size_t>(n_tot) * 2;
+      d_keys_work.grow(cap, static_cast<size_t>(n_left), st);
+      d_keys_sorted.alloc(cap);
+      ensure_cub(static_cast<int64_t>(cap));
+    }
+    const int64_t log_need = log_count + max_ep;
+    if (static_cast<size_t>(log_need) > d_log_t.n) {
+      const size_t cap = static_cast<size_t>(log_need) * 2;
+      d_log_t.grow(cap, static_cast<size_t>(log_count), st);
+      d_log_gid.grow(cap, static_cast<size_t>(log_count), st);
+    }
+    // ---- B: write keys, sort, offsets
+    key_base = s0;
+    h_ctr[C_WCUR] = static_cast<unsigned long long>(n_left);
+    CK(cudaMemcpyAsync(d_ctr.p + C_WCUR, &h_ctr[C_WCUR], sizeof(unsigned long long),
+                       cudaMemcpyHostToDevice, st));
+    McgEvDev E = ev_dev();
+    if (n_fire > 0) {
+      const int64_t thr = n_fire * 32;
+      k_write_source_events<<<static_cast<unsigned>((thr + 127) / 128), 128, 0, st>>>(E, src_dev(),
+                                                                                  n_fire);
+      launched();
+    }
+    if (n_ep > 0 && h_ctr[C_SPK_EV] > 0) {
+      const int64_t thr = n_ep * 32;
+      k_write_spike_events<<<static_cast<unsigned>((thr + 127) / 128), 128, 0, st>>>(
+          E, d_ep_gid.p, d_ep_step.p, d_ctr.p + C_EP_SPK);
+      launched();
+    }
+    const int end_bit = rank_bits + step_bits + dst_bits;
+    if (n_tot > 0) {
+      size_t tb = d_cub_tmp.n;
+      CK(cub::DeviceRadixSort::SortKeys(d_cub_tmp.p, tb, d_keys_work.p, d_keys_sorted.p,
+                                        static_cast<int>(n_tot), 0, end_bit, st));
+      launched(4);
+    }
+    k_offsets<<<(nl + 1 + 255) / 256, 256, 0, st>>>(d_keys_sorted.p, n_tot, nl,
+                                                     rank_bits + step_bits, d_ev_begin.p,
+                                                     d_ev_cursor.p);
+    launched();
+    // ---- C: the epoch
+    refresh_dev();
+    dev.key_base = key_base;
+    if (nl > 0) {
+      if (timing) CK(cudaEventRecord(ev0, st));
+      k_epoch<<<(nl * 32 + 127) / 128, 128, 0, st>>>(dev, s0, s1);
+      if (timing) {
+        CK(cudaEventRecord(ev1, st));
+        ev_pending = true;
+      }
+      launched();
+      stats.epoch_kernel_launches += 1;
+      // ---- D: ordered spike compaction, leftover carry
+      size_t tb = d_cub_tmp.n;
+      CK(cub::DeviceScan::ExclusiveSum(d_cub_tmp.p, tb, d_sp_count.p, d_sp_scan.p, nl, st));
+      k_spike_write<<<(nl + 127) / 128, 128, 0, st>>>(dev, d_sp_scan.p, d_ep_gid.p, d_ep_step.p,
+                                                      d_log_t.p, d_log_gid.p,
+                                                      d_ctr.p + C_EP_SPK, d_ctr.p + C_LOG);
+      k_spike_total<<<1, 1, 0, st>>>(d_sp_count.p, d_sp_scan.p, nl, d_ctr.p + C_EP_SPK,
+                                     d_ctr.p + C_LOG);
+      k_left_count<<<(nl + 255) / 256, 256, 0, st>>>(d_ev_begin.p, d_ev_cursor.p, nl, d_left.p);
+      tb = d_cub_tmp.n;
+      CK(cub::DeviceScan::ExclusiveSum(d_cub_tmp.p, tb, d_left.p, d_left_scan.p, nl, st));
+      k_leftover<<<(nl * 32 + 127) / 128, 128, 0, st>>>(
+          d_keys_sorted.p, d_ev_begin.p, d_ev_cursor.p, d_left_scan.p, nl, d_keys_work.p,
+          static_cast<uint64_t>(len) << rank_bits);
+      k_left_total<<<1, 1, 0, st>>>(d_left.p, d_left_scan.p, nl, d_ctr.p + C_LEFT);
+      launched(7);
+    }
+    stats.epochs += 1;
+    stats.steps += len;
+  }
+
+  // probe sample counts for steps [a, b)
+  void probes_begin(int64_t a, int64_t b, bool forced, int64_t n_forced) {
+    std::vector<int64_t> base(m.probes.size(), 0);
+    int64_t tot = 0;
+    for (size_t p = 0; p < m.probes.size(); ++p) {
+      const McgProbe& P = m.probes[p];
+      base[p] = tot;
+      if (P.local < 0) continue;
+      int64_t cnt;
+      if (forced) cnt = n_forced;
+      else {
+        const int64_t m0 = (a + P.every) / P.every, m1 = b / P.every;
+        cnt = m1 >= m0 ? m1 - m0 + 1 : 0;
+      }
+      tot += cnt;
+    }
+    if (static_cast<size_t>(tot) > d_trace.n) d_trace.alloc(static_cast<size_t>(tot) * 2);
+    if (!m.probes.empty())
+      CK(cudaMemcpyAsync(d_trace_base.p, base.data(), base.size() * sizeof(int64_t),
+                         cudaMemcpyHostToDevice, st));
+    probe_base_host = base;
+    probe_total = tot;
+    dev.trace_buf = d_trace.p;
+    dev.call_first = a;
+  }
+  std::vector<int64_t> probe_base_host;
+  int64_t probe_total = 0;
+
+  void probes_end(int64_t a, int64_t b, bool forced, int64_t n_forced, int64_t per) {
+    if (probe_total == 0) return;
+    std::vector<double> buf(probe_total);
+    CK(cudaMemcpyAsync(buf.data(), d_trace.p, probe_total * sizeof(double), cudaMemcpyDeviceToHost,
+                       st));
+    CK(cudaStreamSynchronize(st));
+    for (size_t p = 0; p < m.probes.size(); ++p) {
+      const McgProbe& P = m.probes[p];
+      if (P.local < 0) continue;
+      const int64_t o = probe_base_host[p];
+      if (forced) {
+        for (int64_t q = 0; q < n_forced; ++q) {
+          const int64_t s = a + (q + 1) * per - 1;  // sample_probes(cell, step_-1, true)
+          traces[p].emplace_back((double(s) + 1.0) * m.dt, buf[o + q]);
+        }
+      } else {
+        const int64_t m0 = (a + P.every) / P.every, m1 = b / P.every;
+        for (int64_t mm = m0; mm <= m1; ++mm) {
+          const int64_t s = mm * P.every - 1;
+          traces[p].emplace_back((double(s) + 1.0) * m.dt, buf[o + (mm - m0)]);
+        }
+      }
+    }
+  }
+
+  void advance_to(double t_ms) {
+    const int64_t target = ceil_steps(t_ms, m.dt);
+    if (step >= target) return;
+    probes_begin(step, target, false, 0);
+    refresh_dev();
+    const int64_t a = step;
+    while (step < target) {
+      const int64_t epoch = m.min_delay_steps > 0 ? m.min_delay_steps : free_epoch;
+      const int64_t s1 = std::min(target, step + epoch);
+      dev.call_first = a;
+      run_epoch(step, s1);
+      step = s1;
+    }
+    sync_counters();
+    probes_end(a, target, false, 0, 1);
+  }
+
+  void fast_forward_to(double t_ms, double coarse_dt_ms) {
+    const double dt = m.dt;
+    const int64_t per = static_cast<int64_t>(std::llround(coarse_dt_ms / dt));
+    if (per < 1 || std::fabs(double(per) * dt - coarse_dt_ms) > 1e-9 * coarse_dt_ms)
+      throw Error(MCG_ERR_ENGINE, "fast-forward: coarse dt must be a multiple of dt");
+    const int64_t target = ceil_steps(t_ms, dt);
+    if ((target - step) % per != 0)
+      throw Error(MCG_ERR_ENGINE, "fast-forward: span must be a multiple of coarse dt");
+    // pending: undelivered keys, unexpanded spikes with fan-out, queued calcium
+    CK(cudaMemsetAsync(d_ctr.p + C_SPK_EV, 0, sizeof(unsigned long long), st));
+    const int nl = n_local();
+    const int64_t max_ep = static_cast<int64_t>(nl) * sp_cap;
+    if (max_ep > 0) {
+      k_spike_outdeg<<<static_cast<unsigned>((max_ep + 255) / 256), 256, 0, st>>>(
+          d_ep_gid.p, d_ctr.p + C_EP_SPK, d_out_begin.p, d_out_end.p, d_ctr.p + C_SPK_EV);
+      launched();
+    }
+    CK(cudaMemsetAsync(d_err.p, 0, sizeof(int32_t), st));
+    const int nf = static_cast<int>(m.fifos.size());
+    if (nf > 0) {
+      k_ff_pending<<<(nf + 255) / 256, 256, 0, st>>>(dev, nf, d_err.p);
+      launched();
+    }
+    sync_counters_raw();
+    const bool fifo_pending = *h_err != 0;
+    *h_err = 0;
+    CK(cudaMemsetAsync(d_err.p, 0, sizeof(int32_t), st));
+    if (h_ctr[C_LEFT] > 0 || h_ctr[C_SPK_EV] > 0 || fifo_pending)
+      throw Error(MCG_ERR_ENGINE, "fast-forward: pending undelivered spikes");
+    const int64_t ncg = static_cast<int64_t>(m.cgs.size());
+    refresh_dev();
+    if (ncg > 0) {
+      k_ff_reset<<<static_cast<unsigned>((ncg + 127) / 128), 128, 0, st>>>(dev, ncg);
+      launched();
+    }
+    const int64_t n_coarse = (target - step) / per;
+    if (n_coarse <= 0) return;
+    const double dtc = coarse_dt_ms;
+    std::vector<double> fh(m.specs.size(), 0.0);
+    for (size_t i = 0; i < m.specs.size(); ++i) fh[i] = std::exp(-0.1 * dtc / m.specs[i].tau_h);
+    std::vector<double> cap_ff(m.k_sp_cap_dt.size());
+    for (size_t k = 0; k < m.kinds.size(); ++k) {
+      const McgKind& K = m.kinds[k];
+      for (int s = 0; s < K.n_species; ++s)
+        for (int i = 0; i < K.n; ++i)
+          cap_ff[K.sp_arr + int64_t(s) * K.n + i] = m.grids[k].volume[i] / dtc;
+    }
+    DBuf<double> d_fh, d_cap_ff;
+    d_fh.upload(fh, st);
+    d_cap_ff.upload(cap_ff, st);
+    probes_begin(step, target, true, n_coarse);
+    refresh_dev();
+    if (nl > 0) {
+      k_ff<<<(nl * 32 + 127) / 128, 128, 0, st>>>(dev, d_fh.p, d_cap_ff.p, dtc, n_coarse, step,
+                                                  per);
+      launched();
+    }
+    const int64_t a = step;
+    step = target;
+    sync_counters();
+    probes_end(a, target, true, n_coarse, per);
+  }
+
+  void sync_counters_raw() {
+    CK(cudaMemcpyAsync(h_ctr, d_ctr.p, C_N * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_err, d_err.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+
+  void sync_spikes() {
+    sync_counters_raw();
+    log_count = static_cast<int64_t>(h_ctr[C_LOG]);
+    if (host_synced >= log_count) return;
+    const int64_t n = log_count - host_synced;
+    const size_t o = spk_t.size();
+    spk_t.resize(o + n);
+    spk_gid.resize(o + n);
+    CK(cudaMemcpyAsync(spk_t.data() + o, d_log_t.p + host_synced, n * sizeof(double),
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(spk_gid.data() + o, d_log_gid.p + host_synced, n * sizeof(uint32_t),
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    host_synced = log_count;
+  }
+
+  void clear_spikes() {
+    sync_spikes();
+    spk_t.clear();
+    spk_gid.clear();
+    CK(cudaMemsetAsync(d_ctr.p + C_LOG, 0, sizeof(unsigned long long), st));
+    CK(cudaStreamSynchronize(st));
+    log_count = 0;
+    host_synced = 0;
+  }
+
+  int local_of(uint32_t gid) const {
+    if (gid < m.gid_begin || gid >= m.gid_end)
+      throw Error(MCG_ERR_ARGUMENT, "gid not on this shard");
+    return static_cast<int>(gid - m.gid_begin);
+  }
+
+  template <class T>
+  void copy_field(void* out, const T* base, int64_t off, int64_t count, bool write,
+                  const void* in) {
+    if (count <= 0) return;
+    if (write)
+      CK(cudaMemcpyAsync(const_cast<T*>(base) + off, in, count * sizeof(T), cudaMemcpyHostToDevice,
+                         st));
+    else
+      CK(cudaMemcpyAsync(out, base + off, count * sizeof(T), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+
+  void state_io(int field, uint32_t gid, int index, int64_t off, int64_t count, void* out,
+                const void* in, bool write) {
+    const int c = local_of(gid);
+    const McgKind& K = m.kinds[m.cell_kind[c]];
+    const int64_t co = m.comp_off[c];
+    auto comp_range = [&](int64_t lim) {
+      if (off < 0 || count < 0 || off + count > lim) throw Error(MCG_ERR_ARGUMENT, "range out of bounds");
+    };
+    switch (field) {
+      case MCG_FIELD_V: comp_range(K.n); return copy_field(out, d_v.p, co + off, count, write, in);
+      case MCG_FIELD_HH_M: comp_range(K.n); return copy_field(out, d_hh_m.p, co + off, count, write, in);
+      case MCG_FIELD_HH_H: comp_range(K.n); return copy_field(out, d_hh_h.p, co + off, count, write, in);
+      case MCG_FIELD_HH_N: comp_range(K.n); return copy_field(out, d_hh_n.p, co + off, count, write, in);
+      case MCG_FIELD_SPECIES:
+        if (index < 0 || index >= K.n_species) throw Error(MCG_ERR_ARGUMENT, "species index");
+        comp_range(K.n);
+        return copy_field(out, d_species.p, m.sp_off[c] + int64_t(index) * K.n + off, count, write, in);
+      case MCG_FIELD_DETECTOR_PREV_V: return copy_field(out, d_det_prev.p, c, 1, write, in);
+      case MCG_FIELD_REFRACTORY_UNTIL: return copy_field(out, d_refr.p, c, 1, write, in);
+      case MCG_FIELD_DETECTOR_ARMED: {
+        int32_t a = 0;
+        if (write) {
+          a = static_cast<int32_t>(*static_cast<const int64_t*>(in));
+          return copy_field<int32_t>(nullptr, d_armed.p, c, 1, true, &a);
+        }
+        copy_field(&a, d_armed.p, c, 1, false, nullptr);
+        *static_cast<int64_t*>(out) = a;
+        return;
+      }
+      case MCG_FIELD_INTERNAL_SEQ: {
+        uint32_t a = 0;
+        if (write) {
+          a = static_cast<uint32_t>(*static_cast<const int64_t*>(in));
+          return copy_field<uint32_t>(nullptr, d_iseq.p, c, 1, true, &a);
+        }
+        copy_field(&a, d_iseq.p, c, 1, false, nullptr);
+        *static_cast<int64_t*>(out) = a;
+        return;
+      }
+      default: break;
+    }
+    if (index < 0 || index >= K.n_groups) throw Error(MCG_ERR_ARGUMENT, "group index");
+    const McgCellGroup& G = m.cgs[m.cg_off[c] + index];
+    comp_range(G.size);
+    const int64_t j = G.inst + off;
+    switch (field) {
+      case MCG_FIELD_SYN_COMP: return copy_field(out, d_i_comp.p, j, count, write, in);
+      case MCG_FIELD_SYN_WEIGHT: return copy_field(out, d_i_weight.p, j, count, write, in);
+      case MCG_FIELD_SYN_KERNEL: return copy_field(out, d_i_kernel.p, j, count, write, in);
+      case MCG_FIELD_STDP_A_PRE: return copy_field(out, d_i_stdp_pre.p, j, count, write, in);
+      case MCG_FIELD_STDP_A_POST: return copy_field(out, d_i_stdp_post.p, j, count, write, in);
+      case MCG_FIELD_STDP_W: return copy_field(out, d_i_stdp_w.p, j, count, write, in);
+      case MCG_FIELD_STDP_LAST: return copy_field(out, d_i_stdp_last.p, j, count, write, in);
+      case MCG_FIELD_HOMEO_W: return copy_field(out, d_i_homeo_w.p, j, count, write, in);
+      case MCG_FIELD_STC_H: return copy_field(out, d_i_stc_h.p, j, count, write, in);
+      case MCG_FIELD_STC_Z: return copy_field(out, d_i_stc_z.p, j, count, write, in);
+      case MCG_FIELD_STC_C: return copy_field(out, d_i_stc_c.p, j, count, write, in);
+      case MCG_FIELD_STC_SPS_ABS: return copy_field(out, d_i_sps_abs.p, j, count, write, in);
+      default: throw Error(MCG_ERR_ARGUMENT, "unknown field");
+    }
+  }
+};
+
+}  // namespace mcg
+
+struct mcg_engine {
+  mcg::Engine e;
+};
+
+namespace {
+template <class F>
+mcg_status guarded(F&& f) {
+  try {
+    f();
+    return MCG_OK;
+  } catch (const mcg::Error& e) {
+    mcg::g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    mcg::g_last_error = e.what();
+    return MCG_ERR_ARGUMENT;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int32_t mcg_abi_version(void) { return MCG_ABI_VERSION; }
+const char* mcg_last_error(void) { return mcg::g_last_error.c_str(); }
+
+mcg_status mcg_create(const mcg_recipe* recipe, const mcg_options* opt, mcg_engine** out) {
+  return guarded([&] {
+    if (!recipe || !opt || !out) throw mcg::Error(MCG_ERR_ARGUMENT, "null argument");
+    *out = nullptr;
+    if (!(opt->dt_ms > 0)) throw mcg::Error(MCG_ERR_ENGINE, "dt must be positive");
+    if (opt->world < 1 || opt->rank < 0 || opt->rank >= opt->world)
+      throw mcg::Error(MCG_ERR_ARGUMENT, "invalid rank/world");
+    auto h = std::make_unique<mcg_engine>();
+    h->e.init(*recipe, *opt);
+    *out = h.release();
+  });
+}
+
+void mcg_destroy(mcg_engine* eng) { delete eng; }
+
+double mcg_time_ms(const mcg_engine* eng) { return double(eng->e.step) * eng->e.m.dt; }
+double mcg_dt_ms(const mcg_engine* eng) { return eng->e.m.dt; }
+int64_t mcg_step(const mcg_engine* eng) { return eng->e.step; }
+int32_t mcg_num_cells(const mcg_engine* eng) { return eng->e.m.n_cells_global; }
+int64_t mcg_min_delay_steps(const mcg_engine* eng) { return eng->e.m.min_delay_steps; }
+
+mcg_status mcg_advance_to(mcg_engine* eng, double t_ms) {
+  return guarded([&] { eng->e.advance_to(t_ms); });
+}
+mcg_status mcg_fast_forward_to(mcg_engine* eng, double t_ms, double coarse_dt_ms) {
+  return guarded([&] { eng->e.fast_forward_to(t_ms, coarse_dt_ms); });
+}
+
+int64_t mcg_num_spikes(mcg_engine* eng) {
+  int64_t n = -1;
+  guarded([&] {
+    eng->e.sync_spikes();
+    n = static_cast<int64_t>(eng->e.spk_t.size());
+  });
+  return n;
+}
+mcg_status mcg_get_spikes(mcg_engine* eng, int64_t first, int64_t count, double* t_ms,
+                          uint32_t* gid) {
+  return guarded([&] {
+    eng->e.sync_spikes();
+    const int64_t n = static_cast<int64_t>(eng->e.spk_t.size());
+    if (first < 0 || count < 0 || first + count > n)
+      throw mcg::Error(MCG_ERR_ARGUMENT, "spike range out of bounds");
+    std::memcpy(t_ms, eng->e.spk_t.data() + first, count * sizeof(double));
+    std::memcpy(gid, eng->e.spk_gid.data() + first, count * sizeof(uint32_t));
+  });
+}
+mcg_status mcg_clear_spikes(mcg_engine* eng) { return guarded([&] { eng->e.clear_spikes(); }); }
+
+int64_t mcg_trace_len(mcg_engine* eng, int32_t probe) {
+  if (probe < 0 || probe >= static_cast<int32_t>(eng->e.traces.size())) return -1;
+  return static_cast<int64_t>(eng->e.traces[probe].size());
+}
+mcg_status mcg_get_trace(mcg_engine* eng, int32_t probe, double* t_ms, double* value) {
+  return guarded([&] {
+    if (probe < 0 || probe >= static_cast<int32_t>(eng->e.traces.size()))
+      throw mcg::Error(MCG_ERR_ARGUMENT, "probe index out of range");
+    const auto& tr = eng->e.traces[probe];
+    for (size_t i = 0; i < tr.size(); ++i) {
+      t_ms[i] = tr[i].first;
+      value[i] = tr[i].second;
+    }
+  });
+}
+
+int32_t mcg_cell_ncomp(const mcg_engine* eng, uint32_t gid) {
+  const auto& E = eng->e;
+  if (gid < E.m.gid_begin || gid >= E.m.gid_end) return -1;
+  return E.m.kinds[E.m.cell_kind[gid - E.m.gid_begin]].n;
+}
+int32_t mcg_cell_ngroups(const mcg_engine* eng, uint32_t gid) {
+  const auto& E = eng->e;
+  if (gid < E.m.gid_begin || gid >= E.m.gid_end) return -1;
+  return E.m.kinds[E.m.cell_kind[gid - E.m.gid_begin]].n_groups;
+}
+int64_t mcg_group_size(const mcg_engine* eng, uint32_t gid, int32_t group) {
+  const auto& E = eng->e;
+  if (gid < E.m.gid_begin || gid >= E.m.gid_end) return -1;
+  const int c = static_cast<int>(gid - E.m.gid_begin);
+  const auto& K = E.m.kinds[E.m.cell_kind[c]];
+  if (group < 0 || group >= K.n_groups) return -1;
+  return E.m.cgs[E.m.cg_off[c] + group].size;
+}
+int32_t mcg_cell_parent(const mcg_engine* eng, uint32_t gid, int32_t comp) {
+  const auto& E = eng->e;
+  if (gid < E.m.gid_begin || gid >= E.m.gid_end) return -2;
+  const auto& K = E.m.kinds[E.m.cell_kind[gid - E.m.gid_begin]];
+  if (comp < 0 || comp >= K.n) return -2;
+  return E.m.k_parent[K.arr + comp];
+}
+
+mcg_status mcg_read_state(mcg_engine* eng, int32_t field, uint32_t gid, int32_t index,
+                          int64_t offset, int64_t count, void* out) {
+  return guarded([&] { eng->e.state_io(field, gid, index, offset, count, out, nullptr, false); });
+}
+mcg_status mcg_write_state(mcg_engine* eng, int32_t field, uint32_t gid, int32_t index,
+                           int64_t offset, int64_t count, const void* in) {
+  return guarded([&] { eng->e.state_io(field, gid, index, offset, count, nullptr, in, true); });
+}
+
+mcg_status mcg_get_stats(mcg_engine* eng, mcg_stats* out) {
+  return guarded([&] {
+    eng->e.sync_counters_raw();
+    eng->e.stats.events_delivered = static_cast<int64_t>(eng->e.h_ctr[mcg::C_DELIVERED]);
+    *out = eng->e.stats;
+  });
+}
+mcg_status mcg_set_timing(mcg_engine* eng, int32_t enabled) {
+  return guarded([&] { eng->e.timing = enabled != 0; });
+}
+
+}  // extern "C"
+
+// ---- device numerics self-test ------------------------------------------------
+__global__ void k_device_math(int32_t func, const double* in, int64_t n, mcg_key key, uint64_t n0,
+                              double* out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s, c;
+  switch (func) {
+    case MCG_MATH_EXP: out[i] = mcg_exp(in[i]); break;
+    case MCG_MATH_LOG: out[i] = mcg_log(in[i]); break;
+    case MCG_MATH_SIN: mcg_sincos(in[i], &s, &c); out[i] = s; break;
+    case MCG_MATH_COS: mcg_sincos(in[i], &s, &c); out[i] = c; break;
+    case MCG_MATH_UNIFORM_FOR: out[i] = mcg_uniform_for(&key, n0 + uint64_t(i)); break;
+    case MCG_MATH_NORMAL_FOR: out[i] = mcg_normal_for(&key, n0 + uint64_t(i)); break;
+    default: out[i] = 0.0;
+  }
+}
+
+extern "C" mcg_status mcg_device_math(int32_t device, int32_t func, const double* in, int64_t n,
+                                      const uint64_t key[4], uint64_t n0, double* out) {
+  return guarded([&] {
+    using mcg::cuda_check;
+    CK(cudaSetDevice(device));
+    if (n <= 0) return;
+    double *din = nullptr, *dout = nullptr;
+    CK(cudaMalloc(&din, n * sizeof(double)));
+    CK(cudaMalloc(&dout, n * sizeof(double)));
+    if (in) CK(cudaMemcpy(din, in, n * sizeof(double), cudaMemcpyHostToDevice));
+    mcg_key k = mcg_make_key(key ? key[0] : 0, key ? key[1] : 0, key ? key[2] : 0,
+                             key ? key[3] : 0);
+    k_device_math<<<static_cast<unsigned>((n + 255) / 256), 256>>>(func, din, n, k, n0, dout);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(out, dout, n * sizeof(double), cudaMemcpyDeviceToHost));
+    cudaFree(din);
+    cudaFree(dout);
+  });
+}

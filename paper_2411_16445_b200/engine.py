@@ -1,0 +1,246 @@
+"""Engine — Python mirror of mcsim::Engine (engine.hpp:126-167) over the C ABI.
+
+    eng = Engine(recipe, EngineOptions(dt_ms=0.5, seed=1))
+    eng.advance_to(1000.0)
+    eng.spikes()            # [SpikeRecord(t_ms, gid)] in the reference's order
+    eng.cell(3).v_mV        # lazily read from HBM
+    eng.fast_forward_to(t, coarse_dt_ms)
+
+Every call goes through include/mcg.h into the sm_100a library; errors come
+back as the reference's exception types with the reference's messages.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional, Tuple
+
+import numpy as np
+
+from . import _abi as A
+from .recipe import (EngineError, FlatRecipe, MorphologyError, NumericError, Recipe,
+                     TargetingError)
+
+
+@dataclass
+class EngineOptions:  # engine.hpp:37-41
+    dt_ms: float = 0.025
+    seed: int = 0
+    workers: int = 1
+
+
+@dataclass
+class SpikeRecord:  # engine.hpp:20-23
+    t_ms: float
+    gid: int
+
+
+_ERR = {A.MCG_ERR_ENGINE: EngineError, A.MCG_ERR_NUMERIC: NumericError,
+        A.MCG_ERR_TARGETING: TargetingError, A.MCG_ERR_MORPHOLOGY: MorphologyError}
+
+
+def _check(status: int):
+    if status != A.MCG_OK:
+        msg = A.lib().mcg_last_error().decode()
+        raise _ERR.get(status, RuntimeError)(msg)
+
+
+class GroupView:
+    """SynGroupRT mirror (engine.hpp:71-85): per-instance arrays read on access."""
+
+    def __init__(self, eng: "Engine", gid: int, index: int, label: str):
+        self._e, self._gid, self._i, self.label = eng, gid, index, label
+
+    def size(self) -> int:
+        return int(A.lib().mcg_group_size(self._e._h, self._gid, self._i))
+
+    def _read(self, field: str, dtype) -> np.ndarray:
+        n = self.size()
+        out = np.empty(n, dtype)
+        if n:
+            _check(A.lib().mcg_read_state(self._e._h, A.FIELD[field], self._gid, self._i, 0, n,
+                                          out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    comp = property(lambda s: s._read("syn_comp", np.int32))
+    weight = property(lambda s: s._read("syn_weight", np.float64))
+    kernel = property(lambda s: s._read("syn_kernel", np.float64))
+    stdp_a_pre = property(lambda s: s._read("stdp_a_pre", np.float64))
+    stdp_a_post = property(lambda s: s._read("stdp_a_post", np.float64))
+    stdp_w = property(lambda s: s._read("stdp_w", np.float64))
+    stdp_last_step = property(lambda s: s._read("stdp_last", np.int64))
+    homeo_w = property(lambda s: s._read("homeo_w", np.float64))
+    stc_h = property(lambda s: s._read("stc_h", np.float64))
+    stc_z = property(lambda s: s._read("stc_z", np.float64))
+    stc_c = property(lambda s: s._read("stc_c", np.float64))
+    sps_abs = property(lambda s: s._read("stc_sps_abs", np.float64))
+
+
+class CellView:
+    """CellRT mirror (engine.hpp:89-115), synced lazily from device state."""
+
+    def __init__(self, eng: "Engine", gid: int):
+        self._e, self.gid = eng, gid
+        L = A.lib()
+        self.ncomp = int(L.mcg_cell_ncomp(eng._h, gid))
+        if self.ncomp < 0:
+            raise EngineError("gid not on this shard")
+        kind = eng._kind_of(gid)
+        labels = [p.label for p in kind.placements] if kind is not None else []
+        ng = int(L.mcg_cell_ngroups(eng._h, gid))
+        self.groups = [GroupView(eng, gid, i, labels[i] if i < len(labels) else "")
+                       for i in range(ng)]
+        self._kind = kind
+
+    def _comp(self, field: str, index: int = 0) -> np.ndarray:
+        out = np.empty(self.ncomp, np.float64)
+        _check(A.lib().mcg_read_state(self._e._h, A.FIELD[field], self.gid, index, 0, self.ncomp,
+                                      out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def _scalar(self, field: str, dtype):
+        out = np.empty(1, dtype)
+        _check(A.lib().mcg_read_state(self._e._h, A.FIELD[field], self.gid, 0, 0, 1,
+                                      out.ctypes.data_as(C.c_void_p)))
+        return out[0]
+
+    @property
+    def v_mV(self) -> np.ndarray:
+        return self._comp("v")
+
+    @property
+    def species(self) -> List[np.ndarray]:
+        n = len(self._kind.species) if self._kind is not None else 0
+        return [self._comp("species", i) for i in range(n)]
+
+    hh_m = property(lambda s: s._comp("hh_m"))
+    hh_h = property(lambda s: s._comp("hh_h"))
+    hh_n = property(lambda s: s._comp("hh_n"))
+    detector_prev_v = property(lambda s: float(s._scalar("detector_prev_v", np.float64)))
+    refractory_until = property(lambda s: int(s._scalar("refractory_until", np.int64)))
+    detector_armed = property(lambda s: bool(s._scalar("detector_armed", np.int64)))
+    internal_seq = property(lambda s: int(s._scalar("internal_seq", np.int64)))
+
+    def find_group(self, label: str) -> int:
+        for i, g in enumerate(self.groups):
+            if g.label == label:
+                return i
+        return -1
+
+    def set_v(self, values):
+        a = np.ascontiguousarray(values, np.float64)
+        _check(A.lib().mcg_write_state(self._e._h, A.FIELD["v"], self.gid, 0, 0, len(a),
+                                       a.ctypes.data_as(C.c_void_p)))
+
+
+class Engine:
+    """B200 engine with mcsim::Engine's public surface."""
+
+    def __init__(self, recipe, options: EngineOptions = EngineOptions(), *, device: int = 0,
+                 rank: int = 0, world: int = 1):
+        L = A.lib()
+        if isinstance(recipe, Recipe):
+            self._flat = recipe.flatten()
+            self._recipe: Optional[Recipe] = recipe
+            view = self._flat.view
+        elif isinstance(recipe, FlatRecipe):
+            self._flat, self._recipe, view = recipe, recipe.recipe, recipe.view
+        else:  # a raw mcg_recipe (e.g. exported by the reference's builders)
+            self._flat, self._recipe, view = recipe, None, recipe
+        opt = A.mcg_options(float(options.dt_ms), int(options.seed) & (2**64 - 1),
+                            int(options.workers), int(device), int(rank), int(world))
+        h = C.c_void_p()
+        _check(L.mcg_create(C.byref(view), C.byref(opt), C.byref(h)))
+        self._h = h
+        self.options = options
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            A.lib().mcg_destroy(h)
+            self._h = None
+
+    def close(self):
+        self.__del__()
+
+    def _kind_of(self, gid: int):
+        if self._recipe is None:
+            return None
+        return self._recipe.kinds[int(self._recipe.cell_kind[gid])]
+
+    # ---- time ----
+    def time_ms(self) -> float:
+        return float(A.lib().mcg_time_ms(self._h))
+
+    def dt_ms(self) -> float:
+        return float(A.lib().mcg_dt_ms(self._h))
+
+    def step(self) -> int:
+        return int(A.lib().mcg_step(self._h))
+
+    def num_cells(self) -> int:
+        return int(A.lib().mcg_num_cells(self._h))
+
+    def min_delay_steps(self) -> int:
+        return int(A.lib().mcg_min_delay_steps(self._h))
+
+    def advance_to(self, t_ms: float):
+        _check(A.lib().mcg_advance_to(self._h, float(t_ms)))
+
+    def fast_forward_to(self, t_ms: float, coarse_dt_ms: float):
+        _check(A.lib().mcg_fast_forward_to(self._h, float(t_ms), float(coarse_dt_ms)))
+
+    # ---- observables ----
+    def spike_arrays(self) -> Tuple[np.ndarray, np.ndarray]:
+        L = A.lib()
+        n = int(L.mcg_num_spikes(self._h))
+        if n < 0:
+            _check(A.MCG_ERR_CUDA)
+        t = np.empty(n, np.float64)
+        g = np.empty(n, np.uint32)
+        if n:
+            _check(L.mcg_get_spikes(self._h, 0, n, t.ctypes.data_as(C.c_void_p),
+                                    g.ctypes.data_as(C.c_void_p)))
+        return t, g
+
+    def spikes(self) -> List[SpikeRecord]:
+        t, g = self.spike_arrays()
+        return [SpikeRecord(float(a), int(b)) for a, b in zip(t, g)]
+
+    def clear_spikes(self):
+        _check(A.lib().mcg_clear_spikes(self._h))
+
+    def cell(self, gid: int) -> CellView:
+        return CellView(self, int(gid))
+
+    def trace_arrays(self, probe: int) -> Tuple[np.ndarray, np.ndarray]:
+        L = A.lib()
+        n = int(L.mcg_trace_len(self._h, probe))
+        if n < 0:
+            raise IndexError("probe index out of range")
+        t = np.empty(n, np.float64)
+        v = np.empty(n, np.float64)
+        if n:
+            _check(L.mcg_get_trace(self._h, probe, t.ctypes.data_as(C.c_void_p),
+                                   v.ctypes.data_as(C.c_void_p)))
+        return t, v
+
+    def traces(self) -> List[List[Tuple[float, float]]]:
+        out = []
+        p = 0
+        while True:
+            n = int(A.lib().mcg_trace_len(self._h, p))
+            if n < 0:
+                break
+            t, v = self.trace_arrays(p)
+            out.append(list(zip(t.tolist(), v.tolist())))
+            p += 1
+        return out
+
+    def stats(self) -> dict:
+        s = A.mcg_stats()
+        _check(A.lib().mcg_get_stats(self._h, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in A.mcg_stats._fields_}
+
+    def set_timing(self, enabled: bool):
+        _check(A.lib().mcg_set_timing(self._h, 1 if enabled else 0))
