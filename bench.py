@@ -1,0 +1,308 @@
+#!/usr/bin/env python3
+"""Benchmark: simulated-seconds per wall-second of the cable-cell integration
+loop (Engine::advance_to) on BASELINE.json configs[2] / SURVEY §8(d) config 3:
+the 2000-neuron multi-compartment (31 comps) recurrent network with synaptic
+tagging and capture, seed 1, dt 0.5 ms, 8-hour protocol (learning at 10 s).
+
+A step = 500 ms of biological time of that protocol (1000 fine steps), in
+order from t = 0: W warm-up steps, then K timed steps (defaults cover the
+spontaneous phase and the onset of the 100 Hz learning stimulus at 10 s).
+
+  value   sim-s/wall-s, device-timed (CUDA events on the engine's stream),
+          network state resident in HBM
+  e2e     same metric through the public API with host buffers: engine
+          construction from the host recipe (H2D), advance over the W+K steps,
+          spikes and final STC weights back to the host (D2H), wall-clocked
+  roofline  the epoch kernel (k_epoch): algorithmic bytes per launch
+          (SURVEY §8(d) B_step x fine steps per epoch) / mean launch duration
+  cpu_baseline  the reference engine (oracle/_ref, compiled from
+          /root/reference) on the same recipe, all host threads, bounded sample
+
+`--impl reference` times the reference's own CPU engine on the same workload
+(rank 0 only) and prints the same JSON line with "impl": "reference".
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+STEP_MS = 500.0
+DT_MS = 0.5
+SEED = 1
+N_CELLS, N_EXC = 2000, 1600
+METRIC = "simulated s per wall s (consolidation network, fine steps)"
+UNIT = "sim-s/wall-s"
+
+
+def workload_config():
+    from paper_2411_16445_b200 import network as N
+    return N.ConsolidationConfig(n_cells=N_CELLS, n_exc=N_EXC, seed=SEED, multi_compartment=True,
+                                 dt_ms=DT_MS)
+
+
+def config_block(n_gpus, l2_note):
+    return {"workload": "config3: consolidation network N=2000 (1600 MC exc x 31 comps + 400 point inh), "
+                        "p=0.1, STC synapses, seed 1, dt 0.5 ms, 8h protocol, step = 500 ms bio",
+            "n_cells": N_CELLS, "compartments": 50000, "dt_ms": DT_MS, "step_bio_ms": STEP_MS,
+            "parallelism": f"cells sharded over {n_gpus} GPU(s)" if n_gpus > 1 else "single GPU",
+            "l2": l2_note}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def measured_peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def traffic_per_launch():
+    p = os.path.join(ROOT, "profiles", "epoch_kernel_dram.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def algorithmic_bytes_per_step(st, events_per_step):
+    """B_step = 16 sum C + 16 S sum C_s + 64 N_stc + 48 C_hh
+    + 16 K_active + 36 sum C_unique + 32 E_step + 24 N_cells (K_active, C_unique = 0 here)."""
+    return (16 * st["total_comps"] + 16 * st["species_comps"] + 64 * st["stc_synapses"]
+            + 48 * st["hh_comps"] + 32 * events_per_step + 24 * N_CELLS)
+
+
+def flush_l2():
+    import torch
+    buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
+    buf.fill_(1.0)
+    torch.cuda.synchronize()
+    del buf
+
+
+def cpu_baseline(recipe_view, sample_ms):
+    """Reference engine (oracle/_ref) on the host cores, bounded sample."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import ref
+    cores = os.cpu_count() or 1
+    e = ref.RefEngine(recipe_view, DT_MS, SEED, cores)
+    t0 = time.perf_counter()
+    e.advance_to(sample_ms)
+    w = time.perf_counter() - t0
+    return {"value": (sample_ms * 1e-3) / w, "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": f"config3 recipe, advance 0 -> {sample_ms:.0f} ms bio, workers={cores}"}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_2411_16445_b200 import network as N
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import ref
+    b = N.build_consolidation_network(workload_config(), True)
+    flat = b.recipe.flatten()
+    cores = os.cpu_count() or 1
+    e = ref.RefEngine(flat.view, DT_MS, SEED, cores)
+    t = 0.0
+    for _ in range(args.warmup):
+        t += STEP_MS
+        e.advance_to(t)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        t += STEP_MS
+        e.advance_to(t)
+    wall = time.perf_counter() - t0
+    val = args.steps * STEP_MS * 1e-3 / wall
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_block(args.gpus, "n/a (CPU)"),
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "reference",
+                             "sample": f"steps {args.warmup}..{args.warmup + args.steps} of 500 ms bio"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_gpu_arm(args):
+    import numpy as np
+    import torch
+    from paper_2411_16445_b200 import Engine, EngineOptions
+    from paper_2411_16445_b200 import network as N
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        raise SystemExit("multi-GPU sharding is not wired into bench.py yet")
+    torch.cuda.set_device(0)
+    cfg = workload_config()
+    b = N.build_consolidation_network(cfg, True)
+    flat = b.recipe.flatten()
+
+    # ---- device-resident timing ----
+    eng = Engine(flat, EngineOptions(DT_MS, SEED), device=0)
+    eng.set_timing(True)
+    t = 0.0
+    for _ in range(args.warmup):
+        t += STEP_MS
+        eng.advance_to(t)
+    flush_l2()
+    s0 = eng.stats()
+    clocks = ClockSampler(0)
+    clocks.start()
+    # device time of each step: the engine's own CUDA events around every
+    # epoch kernel plus a host-synchronized bracket around the whole step
+    wall_steps = []
+    for _ in range(args.steps):
+        flush_l2()
+        torch.cuda.synchronize()
+        a = time.perf_counter()
+        t += STEP_MS
+        eng.advance_to(t)   # returns after the step's last epoch completed
+        wall_steps.append(time.perf_counter() - a)
+    clk = clocks.stop()
+    s1 = eng.stats()
+    # device time: CUDA events recorded on the engine's stream around each
+    # advance_to (mcg_stats.advance_ms); the wall bracket is reported beside it
+    total = (s1["advance_ms"] - s0["advance_ms"]) * 1e-3
+    wall_total = sum(wall_steps)
+    value = args.steps * STEP_MS * 1e-3 / total
+    epochs = s1["epoch_kernel_launches"] - s0["epoch_kernel_launches"]
+    kern_ms = s1["epoch_kernel_ms"] - s0["epoch_kernel_ms"]
+    fine_steps = s1["steps"] - s0["steps"]
+    ev_per_step = (s1["events_delivered"] - s0["events_delivered"]) / max(fine_steps, 1)
+    bstep = algorithmic_bytes_per_step(s1, ev_per_step)
+    steps_per_epoch = fine_steps / max(epochs, 1)
+    per_launch_bytes = bstep * steps_per_epoch
+    mean_launch_s = kern_ms * 1e-3 / max(epochs, 1)
+    peak, peak_kind = measured_peak_hbm()
+    achieved = per_launch_bytes / mean_launch_s / 1e9
+    launches = s1["kernel_launches"] - s0["kernel_launches"]
+
+    # ---- end to end through the public API, host buffers ----
+    e2e_times = []
+    h2d = d2h = 0
+    for _ in range(1):
+        torch.cuda.synchronize()
+        a = time.perf_counter()
+        eng2 = Engine(flat, EngineOptions(DT_MS, SEED), device=0)
+        tt = 0.0
+        for _ in range(args.warmup + args.steps):
+            tt += STEP_MS
+            eng2.advance_to(tt)
+        st, sg = eng2.spike_arrays()
+        hz = [eng2.cell(g).groups[0].stc_h for g in range(0, N_EXC, 1)]
+        e2e_times.append(time.perf_counter() - a)
+        d2h = st.nbytes + sg.nbytes + sum(h.nbytes for h in hz)
+        v = flat.view
+        h2d = (v.n_connections * (1 + 4 + 4 + 4 + 1 + 8 + 8)
+               + s1["total_synapses"] * 8 * 12 + s1["total_comps"] * 8 * 5)
+        eng2.close()
+    e2e_val = (args.warmup + args.steps) * STEP_MS * 1e-3 / min(e2e_times)
+    nsteps_e2e = args.warmup + args.steps
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(flat.view, args.cpu_sample_ms)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference's own recipe builder, seed 1)",
+        "config": config_block(world, "256 MB buffer written between timed steps (flushes L2)"),
+        "compartment_updates_per_s": 50000 * fine_steps / total,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic_per_launch(),
+                     "kernel": "k_epoch", "peak_kind": peak_kind,
+                     "bytes_per_launch": per_launch_bytes, "mean_launch_ms": mean_launch_s * 1e3,
+                     "steps_per_launch": steps_per_epoch},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d / nsteps_e2e),
+                "d2h_bytes_per_step": int(d2h / nsteps_e2e)},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "epoch_kernel_share": kern_ms * 1e-3 / total,
+        "wall_ms_per_step": 1e3 * wall_total / args.steps,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-sample-ms", type=float, default=2000.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

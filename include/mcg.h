@@ -259,6 +259,8 @@ typedef struct {
   int64_t stc_synapses;
   int64_t hh_comps;           /* compartments carrying HH channels            */
   int64_t species_comps;      /* sum over cells of species x compartments     */
+  double advance_ms;          /* CUDA-event time of advance_to calls (engine stream) */
+  int64_t advance_calls;
 } mcg_stats;
 mcg_status mcg_get_stats(mcg_engine* eng, mcg_stats* out);
 /* enable/disable CUDA-event timing of the epoch kernel (adds one event pair per epoch) */
@@ -272,6 +274,16 @@ enum { MCG_MATH_EXP = 0, MCG_MATH_LOG = 1, MCG_MATH_SIN = 2, MCG_MATH_COS = 3,
  * ignored and out[i] = uniform_for/normal_for(key, n0 + i) (rng.cpp:67-84). */
 mcg_status mcg_device_math(int32_t device, int32_t func, const double* in, int64_t n,
                            const uint64_t key[4], uint64_t n0, double* out);
+
+/* ---- recipe materialization on the device --------- */
+
+/* Directed Erdos-Renyi sample of er_connected (network.cpp:34-39):
+ * pair (i, j), i != j, is connected iff uniform_for(key(seed,0,17,0), i*n+j) < p.
+ * Pairs are produced in the reference builder's loop order (i outer, j inner,
+ * network.cpp:548-550) for sources i in [src_begin, src_end).  Call with
+ * src == NULL to get the count in *count; then with arrays of that size. */
+mcg_status mcg_er_connect(int32_t device, uint64_t seed, uint32_t n, double p, uint32_t src_begin,
+                          uint32_t src_end, uint32_t* src, uint32_t* dst, int64_t* count);
 
 #ifdef __cplusplus
 }

@@ -108,7 +108,8 @@ class mcg_stats(C.Structure):
                 ("events_delivered", C.c_int64), ("epoch_kernel_ms", C.c_double),
                 ("epoch_kernel_launches", C.c_int64), ("total_comps", C.c_int64),
                 ("total_synapses", C.c_int64), ("stc_synapses", C.c_int64),
-                ("hh_comps", C.c_int64), ("species_comps", C.c_int64)]
+                ("hh_comps", C.c_int64), ("species_comps", C.c_int64),
+                ("advance_ms", C.c_double), ("advance_calls", C.c_int64)]
 
 
 # field ids (mcg.h)
@@ -123,7 +124,8 @@ EXPORTS = ("mcg_create", "mcg_destroy", "mcg_last_error", "mcg_abi_version", "mc
            "mcg_fast_forward_to", "mcg_num_spikes", "mcg_get_spikes", "mcg_clear_spikes",
            "mcg_trace_len", "mcg_get_trace", "mcg_cell_ncomp", "mcg_cell_ngroups",
            "mcg_group_size", "mcg_cell_parent", "mcg_read_state", "mcg_write_state",
-           "mcg_get_stats", "mcg_set_timing", "mcg_device_math")
+           "mcg_get_stats", "mcg_set_timing", "mcg_device_math",
+           "mcg_er_connect")
 
 _lib = None
 
@@ -160,6 +162,9 @@ def _declare(L):
         "mcg_set_timing": (C.c_int32, [eng, C.c_int32]),
         "mcg_device_math": (C.c_int32, [C.c_int32, C.c_int32, C.c_void_p, C.c_int64,
                                         C.c_void_p, C.c_uint64, C.c_void_p]),
+        "mcg_er_connect": (C.c_int32, [C.c_int32, C.c_uint64, C.c_uint32, C.c_double,
+                                       C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p,
+                                       P(C.c_int64)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -163,7 +163,7 @@ struct Engine {
   // stats
   mcg_stats stats{};
   bool timing = false;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, eva = nullptr, evb = nullptr;
   bool ev_pending = false;
 
   McgDev dev{};
@@ -173,6 +173,8 @@ struct Engine {
     if (h_err) cudaFreeHost(h_err);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (eva) cudaEventDestroy(eva);
+    if (evb) cudaEventDestroy(evb);
     if (st) cudaStreamDestroy(st);
   }
 
@@ -187,6 +189,8 @@ struct Engine {
     CK(cudaMallocHost(&h_err, sizeof(int32_t)));
     CK(cudaEventCreate(&ev0));
     CK(cudaEventCreate(&ev1));
+    CK(cudaEventCreate(&eva));
+    CK(cudaEventCreate(&evb));
     const int nl = n_local();
     // epoch bounds
     free_epoch = std::clamp<int64_t>((int64_t(1) << 22) / std::max(nl, 1), 16, 4096);
@@ -663,6 +667,7 @@ struct Engine {
     probes_begin(step, target, false, 0);
     refresh_dev();
     const int64_t a = step;
+    CK(cudaEventRecord(eva, st));
     while (step < target) {
       const int64_t epoch = m.min_delay_steps > 0 ? m.min_delay_steps : free_epoch;
       const int64_t s1 = std::min(target, step + epoch);
@@ -670,7 +675,14 @@ struct Engine {
       run_epoch(step, s1);
       step = s1;
     }
+    CK(cudaEventRecord(evb, st));
     sync_counters();
+    {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, eva, evb));
+      stats.advance_ms += ms;
+      stats.advance_calls += 1;
+    }
     probes_end(a, target, false, 0, 1);
   }
 
@@ -1024,5 +1036,82 @@ extern "C" mcg_status mcg_device_math(int32_t device, int32_t func, const double
     CK(cudaMemcpy(out, dout, n * sizeof(double), cudaMemcpyDeviceToHost));
     cudaFree(din);
     cudaFree(dout);
+  });
+}
+
+// ---- Erdos-Renyi connectivity on the device ---------------------------------------
+// thread t covers pair indices [t*64, t*64+64) of the row-major (i, j) space
+// restricted to rows [r0, r1); pass 1 counts, pass 2 writes in order.
+#define MCG_ER_CHUNK 64
+__global__ void k_er(uint64_t seed, uint32_t n, double p, uint64_t k0, uint64_t k1,
+                     int64_t* counts, const int64_t* offs, uint32_t* src, uint32_t* dst) {
+  const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t a = k0 + t * MCG_ER_CHUNK;
+  if (a >= k1) return;
+  const uint64_t b = a + MCG_ER_CHUNK < k1 ? a + MCG_ER_CHUNK : k1;
+  const mcg_key key = mcg_make_key(seed, 0, 17, 0);
+  int64_t c = 0, o = offs ? offs[t] : 0;
+  uint64_t x[4];
+  uint64_t blk = ~0ull;
+  for (uint64_t k = a; k < b; ++k) {
+    if ((k >> 2) != blk) {
+      blk = k >> 2;
+      mcg_threefry(&key, blk, x);
+    }
+    const uint32_t i = uint32_t(k / n), j = uint32_t(k % n);
+    if (i == j) continue;
+    const double u = (double)(x[k & 3u] >> 11) * MCG_2POW_M53;
+    if (u < p) {
+      if (src) {
+        src[o + c] = i;
+        dst[o + c] = j;
+      }
+      ++c;
+    }
+  }
+  if (!offs) counts[t] = c;
+}
+
+extern "C" mcg_status mcg_er_connect(int32_t device, uint64_t seed, uint32_t n, double p,
+                                     uint32_t src_begin, uint32_t src_end, uint32_t* src,
+                                     uint32_t* dst, int64_t* count) {
+  return guarded([&] {
+    using mcg::cuda_check;
+    CK(cudaSetDevice(device));
+    const uint64_t k0 = uint64_t(src_begin) * n, k1 = uint64_t(src_end) * n;
+    if (k1 <= k0) {
+      *count = 0;
+      return;
+    }
+    const uint64_t nthr = (k1 - k0 + MCG_ER_CHUNK - 1) / MCG_ER_CHUNK;
+    int64_t *d_cnt = nullptr, *d_off = nullptr;
+    CK(cudaMalloc(&d_cnt, nthr * sizeof(int64_t)));
+    CK(cudaMalloc(&d_off, nthr * sizeof(int64_t)));
+    const unsigned blocks = static_cast<unsigned>((nthr + 255) / 256);
+    k_er<<<blocks, 256>>>(seed, n, p, k0, k1, d_cnt, nullptr, nullptr, nullptr);
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, d_cnt, d_off, static_cast<int64_t>(nthr)));
+    void* tmp = nullptr;
+    CK(cudaMalloc(&tmp, tb));
+    CK(cub::DeviceScan::ExclusiveSum(tmp, tb, d_cnt, d_off, static_cast<int64_t>(nthr)));
+    int64_t last_off = 0, last_cnt = 0;
+    CK(cudaMemcpy(&last_off, d_off + nthr - 1, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&last_cnt, d_cnt + nthr - 1, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    const int64_t total = last_off + last_cnt;
+    if (src && dst && total > 0) {
+      if (*count < total) throw mcg::Error(MCG_ERR_ARGUMENT, "er_connect: output too small");
+      uint32_t *d_src = nullptr, *d_dst = nullptr;
+      CK(cudaMalloc(&d_src, total * sizeof(uint32_t)));
+      CK(cudaMalloc(&d_dst, total * sizeof(uint32_t)));
+      k_er<<<blocks, 256>>>(seed, n, p, k0, k1, d_cnt, d_off, d_src, d_dst);
+      CK(cudaMemcpy(src, d_src, total * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(dst, d_dst, total * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+      cudaFree(d_src);
+      cudaFree(d_dst);
+    }
+    cudaFree(tmp);
+    cudaFree(d_cnt);
+    cudaFree(d_off);
+    *count = total;
   });
 }

@@ -1,0 +1,74 @@
+"""Host-side recipe handling: the Python recipe flattens to exactly the
+recipe the reference builds (checked by running the reference engine on the
+flattened recipe against the reference's own driver)."""
+import numpy as np
+import pytest
+
+import ref
+from recipe_compare import assert_recipes_equal
+from paper_2411_16445_b200 import network as N
+from paper_2411_16445_b200.recipe import (ConnectionSpec, EngineError, LifMembrane,
+                                          PlacementSpec, Recipe, CellKindSpec, SynKind,
+                                          SynSpec, ScriptedSource)
+
+
+def test_stc_single_recipe_drives_reference_to_golden():
+    """build_stc_single (network.cpp:318-349) -> flat -> reference engine ->
+    the run_stc_protocol golden values (STET trial 0)."""
+    cfg = N.StcSingleConfig()
+    times = N.stc_protocol_times(N.StcProtocol.stet, cfg.t_onset_ms)
+    r = N.build_stc_single(cfg, times)
+    t_detailed = np.ceil((times[-1] + 2000.0) / 1000.0) * 1000.0
+    r.kinds[0].membrane.bg_quiet_t0_ms = t_detailed - 500.0
+    r.kinds[0].membrane.bg_quiet_t1_ms = cfg.t_eval_ms
+    flat = r.flatten()
+    e = ref.RefEngine(flat.view, cfg.dt_ms, cfg.seed, 1)
+    e.advance_to(t_detailed)
+    n_coarse = np.floor((cfg.t_eval_ms - t_detailed) / cfg.coarse_dt_ms)
+    e.fast_forward_to(t_detailed + n_coarse * cfg.coarse_dt_ms, cfg.coarse_dt_ms)
+    assert e.read("stc_h", 0, 0)[0] == 4.5449467093946359
+    assert e.read("stc_z", 0, 0)[0] == 0.75323495592946443
+    assert e.read("species", 0, 1)[0] == 0.24731552999708523
+
+
+def test_flatten_roundtrip_through_reference():
+    cfg = N.StcSingleConfig()
+    r = N.build_stc_single(cfg, [10.0, 20.0])
+    flat = r.flatten()
+    back = ref.RefRecipe.from_flat(flat.view)
+    assert_recipes_equal(flat.view, back.view)
+
+
+def test_label_errors_match_reference_messages():
+    kind = CellKindSpec(membrane=LifMembrane(exact=True),
+                        placements=[PlacementSpec("in", SynSpec(kind=SynKind.static_charge))])
+    kind.segments = N.build_consolidation_cell(N.ConsolidationCellParams()).segments
+    r = Recipe(kinds=[kind], cell_kind=[0, 0], sources=[ScriptedSource([1.0])],
+               connections=[ConnectionSpec(False, 0, 1, "nope", 0, 1.0, 5.0)])
+    with pytest.raises(EngineError, match="connection label 'nope' not found"):
+        r.flatten()
+    r.connections = [ConnectionSpec(False, 0, 7, "in", 0, 1.0, 5.0)]
+    with pytest.raises(EngineError, match="connection dst out of range"):
+        r.flatten()
+
+
+def test_grid_layout_matches_reference_discretize():
+    """compartment numbering used by the builders == discretize (31 / 48 comps)."""
+    for d, n in ((N.DendriteSize.small_dendrites, 31), (N.DendriteSize.large_dendrites, 48)):
+        cell = N.build_consolidation_cell(N.ConsolidationCellParams(single_compartment=False,
+                                                                    dendrites=d))
+        g = N.grid_layout(cell.segments, 1.0)
+        assert g.size == n
+        r = Recipe(kinds=[CellKindSpec(segments=cell.segments)], cell_kind=[0])
+        flat = r.flatten()
+        k = flat.view.kinds[0]
+        par = np.empty(64, np.int32)
+        buf = [np.empty(64) for _ in range(4)]
+        cnt = ref.lib().ref_discretize(k, 64, par.ctypes.data, *[b.ctypes.data for b in buf])
+        assert cnt == n
+    # small-dendrite parents
+    cell = N.build_consolidation_cell(N.ConsolidationCellParams(single_compartment=False))
+    g = N.grid_layout(cell.segments, 1.0)
+    assert g.compartment_at(cell.apical_seg, 1.0) == 25
+    assert g.compartment_at(cell.basal_seg, 1.0) == 30
+    assert g.compartment_at(cell.soma_center_seg, 0.5) == 0
