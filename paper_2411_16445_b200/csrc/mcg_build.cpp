@@ -89,6 +89,24 @@ std::vector<double> diffusive_coupling(const Grid& g, double diffusivity_si) {
 
 }  // namespace
 
+bool eliminate_constant(int n, const int32_t* parent, const double* cap, const double* gs,
+                        const double* coupling, double* f, double* d) {
+  for (int i = 0; i < n; ++i) {
+    d[i] = cap[i] + gs[i];
+    f[i] = 0.0;
+  }
+  for (int i = 1; i < n; ++i) {
+    d[i] += coupling[i];
+    d[parent[i]] += coupling[i];
+  }
+  for (int i = n - 1; i >= 1; --i) {
+    if (d[i] <= 0.0) return false;
+    f[i] = coupling[i] / d[i];
+    d[parent[i]] -= f[i] * coupling[i];
+  }
+  return d[0] > 0.0;
+}
+
 int64_t ceil_steps(double t_ms, double dt_ms) {
   return static_cast<int64_t>(std::ceil(t_ms / dt_ms - 1e-9));  // engine.cpp:21-23
 }
@@ -353,16 +371,44 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
       m.k_cf.push_back(k.cf[i]);
       m.k_volume.push_back(g.volume[i]);
     }
+    // LIF-cable V system without active conductances: cap/dt, g_leak + 0.0
+    // (engine.cpp:680-686 with has_gsyn == false)
+    {
+      std::vector<double> capv(n), gsv(n), fv(n, 0.0), dv(n, 0.0);
+      for (int i = 0; i < n; ++i) {
+        capv[i] = k.cap_nF[i] / dt;
+        gsv[i] = k.g_leak[i] + 0.0;
+      }
+      K.v_const = (K.dyn == MCG_DYN_LIF && n > 1 &&
+                   eliminate_constant(n, g.parent.data(), capv.data(), gsv.data(),
+                                      k.axial.data(), fv.data(), dv.data()))
+                      ? 1 : 0;
+      for (int i = 0; i < n; ++i) {
+        m.k_vf.push_back(fv[i]);
+        m.k_vd.push_back(dv[i]);
+      }
+    }
     K.sp_arr = static_cast<int64_t>(m.k_sp_cap_dt.size());
     m.k_sp_off[ki] = static_cast<int64_t>(m.k_sp_decay_tau.size());
+    K.sp_const = 1;
     for (int s = 0; s < spec.n_species; ++s) {
       const double tau = spec.species[s].decay_tau_ms;
       m.k_sp_decay_tau.push_back(tau);
+      std::vector<double> cs(n), gss(n), fs(n, 0.0), ds(n, 0.0);
       for (int i = 0; i < n; ++i) {
-        m.k_sp_cap_dt.push_back(g.volume[i] / dt);
-        m.k_sp_gs.push_back(tau > 0 ? g.volume[i] / tau : 0.0);
+        cs[i] = g.volume[i] / dt;
+        gss[i] = tau > 0 ? g.volume[i] / tau : 0.0;
+        m.k_sp_cap_dt.push_back(cs[i]);
+        m.k_sp_gs.push_back(gss[i]);
         m.k_sp_coupling.push_back(k.sp_coupling[s][i]);
         m.k_sp_init.push_back(spec.species[s].init);
+      }
+      if (n > 1 && !eliminate_constant(n, g.parent.data(), cs.data(), gss.data(),
+                                       k.sp_coupling[s].data(), fs.data(), ds.data()))
+        K.sp_const = 0;
+      for (int i = 0; i < n; ++i) {
+        m.k_sp_f.push_back(fs[i]);
+        m.k_sp_d.push_back(ds[i]);
       }
     }
     m.k_sp_off[ki + 1] = static_cast<int64_t>(m.k_sp_decay_tau.size());

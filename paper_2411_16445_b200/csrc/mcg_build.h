@@ -56,6 +56,8 @@ struct HostModel {
   std::vector<int32_t> k_parent;
   std::vector<double> k_cap_dt, k_g_leak, k_g_leak_rhs, k_axial, k_g_na, k_g_k, k_cf, k_volume;
   std::vector<double> k_sp_cap_dt, k_sp_gs, k_sp_coupling, k_sp_init;
+  std::vector<double> k_vf, k_vd;        // precomputed V elimination (per comp)
+  std::vector<double> k_sp_f, k_sp_d;    // precomputed species elimination
   std::vector<double> k_sp_decay_tau;  // per kind species (for fast-forward)
   std::vector<int64_t> k_sp_off;       // per kind: offset into k_sp_decay_tau
   std::vector<McgSpec> specs;
@@ -94,6 +96,14 @@ struct HostModel {
   // totals (stats)
   int64_t total_comps = 0, total_syn = 0, stc_syn = 0, hh_comps = 0, species_comps = 0;
 };
+
+// Eliminate a constant diagonal exactly as solve_tree does (tree_solver.cpp:
+// 55-70): diag = cap + gs, += coupling (own, then children ascending), then
+// leaves-to-root.  Writes f[i] (i >= 1) and the eliminated diagonal d[i].
+// Returns false if the system is singular (the engine then runs the full
+// solve, which reports the NumericError at the same step as the reference).
+bool eliminate_constant(int n, const int32_t* parent, const double* cap, const double* gs,
+                        const double* coupling, double* f, double* d);
 
 // Materialize; throws mcg::Error with the reference's messages.
 void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m);

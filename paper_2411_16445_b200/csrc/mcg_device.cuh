@@ -44,8 +44,13 @@ struct McgDev {
   int32_t* armed;
   int64_t* refr_until;
   uint32_t* internal_seq;
-  // per-compartment scratch
+  // per-compartment scratch (global fallback for cells too large for smem)
   double *s_gsyn, *s_gsyn_rhs, *s_rhs_cur, *s_diag, *s_rhs;
+  double* s_r2;               // (1 + sp_max) x compartments
+  const double *k_vf, *k_vd, *k_sp_f, *k_sp_d;
+  int32_t sp_max;             // max species per kind
+  int32_t smem_n;             // cells with n <= smem_n are staged in shared memory
+  int32_t smem_stride;        // doubles per warp in dynamic shared memory
   // groups, instances
   McgCellGroup* cgs;
   McgFifo* fifos;
@@ -101,7 +106,7 @@ __device__ __forceinline__ void mcg_stdp_decay(double& pre, double& post, const 
 
 // ---- apply_events (engine.cpp:452-513); lane 0 only -----------------------
 __device__ void mcg_apply_event(const McgDev& D, const McgKind& K, int c, int64_t cg0,
-                                int64_t co, int32_t group, uint32_t inst, double w, int etype,
+                                double* V, int32_t group, uint32_t inst, double w, int etype,
                                 bool refractory, int64_t s) {
   McgCellGroup& G = D.cgs[cg0 + group];
   const McgSpec& S = D.specs[G.spec];
@@ -110,7 +115,7 @@ __device__ void mcg_apply_event(const McgDev& D, const McgKind& K, int c, int64_
     case MCG_SYN_STATIC_CHARGE:
       if (!refractory && w != 0.0) {
         const int comp = D.i_comp[j];
-        D.v[co + comp] += w * D.k_cf[K.arr + comp];
+        V[comp] += w * D.k_cf[K.arr + comp];
       }
       break;
     case MCG_SYN_STATIC_COND:
@@ -173,7 +178,7 @@ __device__ void mcg_apply_event(const McgDev& D, const McgKind& K, int c, int64_
         if (!refractory) {
           const int comp = D.i_comp[j];
           const double tw = D.i_stc_h[j] + S.h0 * D.i_stc_z[j];
-          D.v[co + comp] += tw * w * D.k_cf[K.arr + comp];
+          V[comp] += tw * w * D.k_cf[K.arr + comp];
         }
       }
       break;
@@ -205,6 +210,18 @@ __device__ bool mcg_solve_tree(int n, const int32_t* par, const double* cap, con
   return true;
 }
 
+// solve_tree with a precomputed constant elimination (McgKind::v_const /
+// sp_const): the rhs sweep and back-substitution of tree_solver.cpp:55-73
+// with f[i] = coupling[i]/diag[i] and the eliminated diagonal d[i] taken from
+// mcg::eliminate_constant.  r2 must hold cap[i]*v[i] + rhs[i] on entry.
+__device__ __forceinline__ void mcg_solve_const(int n, const int32_t* par, const double* coup,
+                                                const double* f, const double* d, double* v,
+                                                double* r2) {
+  for (int i = n - 1; i >= 1; --i) r2[par[i]] += f[i] * r2[i];
+  v[0] = r2[0] / d[0];
+  for (int i = 1; i < n; ++i) v[i] = (r2[i] + coup[i] * v[par[i]]) / d[i];
+}
+
 // HH rates (engine.cpp:41-54) with the glibc-faithful exp
 __device__ __forceinline__ double mcg_hh_am(double v) {
   const double x = v + 40.0;
@@ -226,11 +243,18 @@ __device__ __forceinline__ double mcg_hh_bn(double v) {
 }
 
 // STC early/late phase of one instance (mechanisms.hpp:213-242, engine.cpp:624-644)
-// returns true if |h-h0| changed; *delta is the SPS increment
-__device__ __forceinline__ bool mcg_stc_instance(const McgDev& D, const McgSpec& S, int64_t j,
-                                                 uint32_t gid, int gi, int i, int64_t s,
-                                                 const double* prp_base, const double* vol_k,
-                                                 double* delta, int* comp_out) {
+// `changed`: |h-h0| changed; `delta` is then the SPS increment at `comp`
+struct McgStcOut {
+  double delta;
+  int comp;
+  bool changed;
+};
+
+__device__ __forceinline__ McgStcOut mcg_stc_instance(const McgDev& D, const McgSpec& S,
+                                                      int64_t j, uint32_t gid, int gi, int i,
+                                                      int64_t s, const double* prp_base,
+                                                      const double* vol_k) {
+  McgStcOut out{0.0, 0, false};
   double h = D.i_stc_h[j];
   double z = D.i_stc_z[j];
   double cc = D.i_stc_c[j];
@@ -249,13 +273,13 @@ __device__ __forceinline__ bool mcg_stc_instance(const McgDev& D, const McgSpec&
   if (crossings > 0 && S.sigma != 0.0) dh += (crossings == 1 ? S.nz1 : S.nz2) * nrm;
   h += dh;
   const int comp = D.i_comp[j];
-  *comp_out = comp;
+  out.comp = comp;
   const double na = fabs(h - S.h0);
-  bool changed = false;
-  if (na != D.i_sps_abs[j]) {
-    *delta = (na - D.i_sps_abs[j]) / vol_k[comp];
+  const double old = D.i_sps_abs[j];
+  if (na != old) {
+    out.delta = (na - old) / vol_k[comp];
     D.i_sps_abs[j] = na;
-    changed = true;
+    out.changed = true;
   }
   // stc_late_step
   if (prp_base) {
@@ -271,15 +295,14 @@ __device__ __forceinline__ bool mcg_stc_instance(const McgDev& D, const McgSpec&
   D.i_stc_h[j] = h;
   D.i_stc_z[j] = z;
   D.i_stc_c[j] = cc;
-  return changed;
+  return out;
 }
 
 // probe_value (engine.cpp:795-829)
-__device__ double mcg_probe_value(const McgDev& D, const McgKind& K, int c, const McgProbe& P) {
-  const int64_t co = D.comp_off[c];
-  if (P.what == MCG_PROBE_VOLTAGE) return (K.dyn == MCG_DYN_NONE) ? 0.0 : D.v[co + P.comp];
-  if (P.what == MCG_PROBE_SPECIES)
-    return D.species[D.sp_off[c] + int64_t(P.species) * K.n + P.comp];
+__device__ double mcg_probe_value(const McgDev& D, const McgKind& K, int c, const McgProbe& P,
+                                  const double* V, const double* SP) {
+  if (P.what == MCG_PROBE_VOLTAGE) return (K.dyn == MCG_DYN_NONE) ? 0.0 : V[P.comp];
+  if (P.what == MCG_PROBE_SPECIES) return SP[int64_t(P.species) * K.n + P.comp];
   const McgCellGroup& G = D.cgs[D.cg_off[c] + P.group];
   const McgSpec& S = D.specs[G.spec];
   const int64_t j = G.inst + P.instance;

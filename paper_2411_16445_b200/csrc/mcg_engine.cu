@@ -19,7 +19,7 @@
 #include <vector>
 
 #include "mcg_build.h"
-#include "mcg_kernels.cuh"
+#include "mcg_epoch.cuh"
 
 namespace mcg {
 
@@ -108,7 +108,12 @@ struct Engine {
   DBuf<int32_t> d_armed;
   DBuf<int64_t> d_refr;
   DBuf<uint32_t> d_iseq;
-  DBuf<double> d_s_gsyn, d_s_gsyn_rhs, d_s_rhs_cur, d_s_diag, d_s_rhs;
+  DBuf<double> d_s_gsyn, d_s_gsyn_rhs, d_s_rhs_cur, d_s_diag, d_s_rhs, d_s_r2;
+  DBuf<double> d_k_vf, d_k_vd, d_k_sp_f, d_k_sp_d;
+  static constexpr int kSmemMaxComps = 96;  // cells up to this size live in shared memory
+  static constexpr int kBlock = 128;        // 4 warps = 4 cells per block
+  int32_t sp_max = 0, smem_n = 0, smem_stride = 0;
+  size_t smem_bytes = 0;
   DBuf<McgCellGroup> d_cgs;
   DBuf<McgFifo> d_fifos;
   DBuf<int64_t> d_fifo_step;
@@ -238,6 +243,23 @@ struct Engine {
     d_s_rhs_cur.alloc(nc);
     d_s_diag.alloc(nc);
     d_s_rhs.alloc(nc);
+    sp_max = 0;
+    smem_n = 0;
+    for (const McgKind& K : m.kinds) {
+      sp_max = std::max(sp_max, K.n_species);
+      if (K.n <= kSmemMaxComps) smem_n = std::max(smem_n, K.n);
+    }
+    d_s_r2.alloc(nc * (1 + sp_max));
+    d_k_vf.upload(m.k_vf, st);
+    d_k_vd.upload(m.k_vd, st);
+    d_k_sp_f.upload(m.k_sp_f, st);
+    d_k_sp_d.upload(m.k_sp_d, st);
+    smem_stride = (9 + 2 * sp_max) * smem_n;
+    smem_bytes = static_cast<size_t>(smem_stride) * sizeof(double) * (kBlock / 32);
+    CK(cudaFuncSetAttribute(k_epoch, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(smem_bytes)));
+    CK(cudaFuncSetAttribute(k_ff, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(smem_bytes)));
     d_cgs.upload(m.cgs, st);
     d_fifos.upload(m.fifos, st);
     d_fifo_step.alloc(std::max<int64_t>(m.fifo_total, 1));
@@ -411,6 +433,14 @@ struct Engine {
     D.s_rhs_cur = d_s_rhs_cur.p;
     D.s_diag = d_s_diag.p;
     D.s_rhs = d_s_rhs.p;
+    D.s_r2 = d_s_r2.p;
+    D.k_vf = d_k_vf.p;
+    D.k_vd = d_k_vd.p;
+    D.k_sp_f = d_k_sp_f.p;
+    D.k_sp_d = d_k_sp_d.p;
+    D.sp_max = sp_max;
+    D.smem_n = smem_n;
+    D.smem_stride = smem_stride;
     D.cgs = d_cgs.p;
     D.fifos = d_fifos.p;
     D.fifo_step = d_fifo_step.p;
@@ -580,7 +610,7 @@ struct Engine {
     dev.key_base = key_base;
     if (nl > 0) {
       if (timing) CK(cudaEventRecord(ev0, st));
-      k_epoch<<<(nl * 32 + 127) / 128, 128, 0, st>>>(dev, s0, s1);
+      k_epoch<<<(nl * 32 + kBlock - 1) / kBlock, kBlock, smem_bytes, st>>>(dev, s0, s1);
       if (timing) {
         CK(cudaEventRecord(ev1, st));
         ev_pending = true;
@@ -726,21 +756,35 @@ struct Engine {
     const double dtc = coarse_dt_ms;
     std::vector<double> fh(m.specs.size(), 0.0);
     for (size_t i = 0; i < m.specs.size(); ++i) fh[i] = std::exp(-0.1 * dtc / m.specs[i].tau_h);
-    std::vector<double> cap_ff(m.k_sp_cap_dt.size());
+    // species systems at the coarse step: cap = vol/dtc (engine.cpp:1019-1025),
+    // eliminated once with solve_tree's operation order
+    std::vector<double> cap_ff(m.k_sp_cap_dt.size()), f_ff(cap_ff.size()), d_ff(cap_ff.size());
+    std::vector<McgKind> kinds_ff = m.kinds;
     for (size_t k = 0; k < m.kinds.size(); ++k) {
-      const McgKind& K = m.kinds[k];
-      for (int s = 0; s < K.n_species; ++s)
-        for (int i = 0; i < K.n; ++i)
-          cap_ff[K.sp_arr + int64_t(s) * K.n + i] = m.grids[k].volume[i] / dtc;
+      McgKind& K = kinds_ff[k];
+      for (int s = 0; s < K.n_species; ++s) {
+        const int64_t o = K.sp_arr + int64_t(s) * K.n;
+        for (int i = 0; i < K.n; ++i) cap_ff[o + i] = m.grids[k].volume[i] / dtc;
+        if (K.n > 1 && !eliminate_constant(K.n, m.grids[k].parent.data(), cap_ff.data() + o,
+                                           m.k_sp_gs.data() + o, m.k_sp_coupling.data() + o,
+                                           f_ff.data() + o, d_ff.data() + o))
+          K.sp_const = 0;
+      }
     }
-    DBuf<double> d_fh, d_cap_ff;
+    DBuf<double> d_fh, d_cap_ff, d_f_ff, d_d_ff;
+    DBuf<McgKind> d_kinds_ff;
     d_fh.upload(fh, st);
     d_cap_ff.upload(cap_ff, st);
+    d_f_ff.upload(f_ff, st);
+    d_d_ff.upload(d_ff, st);
+    d_kinds_ff.upload(kinds_ff, st);
     probes_begin(step, target, true, n_coarse);
     refresh_dev();
     if (nl > 0) {
-      k_ff<<<(nl * 32 + 127) / 128, 128, 0, st>>>(dev, d_fh.p, d_cap_ff.p, dtc, n_coarse, step,
-                                                  per);
+      McgDev dff = dev;
+      dff.kinds = d_kinds_ff.p;
+      k_ff<<<(nl * 32 + kBlock - 1) / kBlock, kBlock, smem_bytes, st>>>(
+          dff, d_fh.p, d_cap_ff.p, d_f_ff.p, d_d_ff.p, dtc, n_coarse);
       launched();
     }
     const int64_t a = step;

@@ -246,294 +246,6 @@ __device__ __forceinline__ void mcg_post_event(const McgDev& D, const McgKind& K
   }
 }
 
-// species: synthesis source, then implicit diffusion/decay (engine.cpp:721-751)
-__device__ bool mcg_species_update(const McgDev& D, const McgKind& K, int64_t so, int64_t co,
-                                   const double* sp_cap, double* rhs_scratch) {
-  const int n = K.n;
-  bool ok = true;
-  double prod = 0.0;
-  if (K.prp_enabled)
-    prod = (D.species[so + int64_t(K.sps_idx) * n + K.prp_comp] > K.prp_theta_star) ? K.prp_rate
-                                                                                     : 0.0;
-  for (int sp = 0; sp < K.n_species; ++sp) {
-    double* conc = D.species + so + int64_t(sp) * n;
-    const bool is_prp = sp == K.prp_idx;
-    const int64_t ka = K.sp_arr + int64_t(sp) * n;
-    if (n == 1) {
-      const double cap0 = sp_cap[ka];
-      const double gse = D.k_sp_gs[ka];
-      const double r = cap0 * conc[0] + (is_prp ? prod : 0.0);
-      conc[0] = r / (cap0 + gse);
-      continue;
-    }
-    for (int i = 0; i < n; ++i) rhs_scratch[i] = 0.0;
-    if (is_prp && prod != 0.0) rhs_scratch[K.prp_comp] = prod;
-    ok &= mcg_solve_tree(n, D.k_parent + K.arr, sp_cap + ka, D.k_sp_gs + ka,
-                         D.k_sp_coupling + ka, rhs_scratch, conc, D.s_diag + co, D.s_rhs + co);
-  }
-  return ok;
-}
-
-__global__ void __launch_bounds__(128) k_epoch(McgDev D, int64_t s0, int64_t s1) {
-  const int lane = threadIdx.x & 31;
-  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (c >= D.n_cells) return;
-  const McgKind& K = D.kinds[D.cell_kind[c]];
-  const int n = K.n;
-  const int64_t co = D.comp_off[c], so = D.sp_off[c], cg0 = D.cg_off[c];
-  const uint32_t gid = D.gid0 + uint32_t(c);
-  const bool is_lif = K.dyn == MCG_DYN_LIF || K.dyn == MCG_DYN_LIF_EXACT;
-  double* V = D.v + co;
-  double* gsyn = D.s_gsyn + co;
-  double* gsyn_rhs = D.s_gsyn_rhs + co;
-  double* rhs_cur = D.s_rhs_cur + co;
-  const int32_t* par = D.k_parent + K.arr;
-  const uint64_t rank_mask = (1ull << D.rank_bits) - 1;
-  const uint64_t step_mask = (1ull << D.step_bits) - 1;
-  const double* prp_base = (K.prp_idx >= 0) ? D.species + so + int64_t(K.prp_idx) * n : nullptr;
-  double* sps_base = (K.sps_idx >= 0) ? D.species + so + int64_t(K.sps_idx) * n : nullptr;
-  const double* vol_k = D.k_volume + K.arr;
-  const bool stc_seq = sps_base != nullptr && (const double*)sps_base == prp_base;
-  int64_t cur = D.ev_cursor[c];
-  const int64_t end = D.ev_begin[c + 1];
-  int nsp = 0;
-  unsigned long long ndel = 0;
-  bool ok = true;
-
-  for (int64_t s = s0; s < s1; ++s) {
-    const bool refractory = is_lif && s < D.refr_until[c];
-    // ---- 1. deliver due events: inbox, then internal (engine.cpp:549-560)
-    if (lane == 0) {
-      while (cur < end) {
-        const uint64_t key = D.keys[cur];
-        const int64_t st = D.key_base + int64_t((key >> D.rank_bits) & step_mask);
-        if (st > s) break;
-        const int64_t r = int64_t(key & rank_mask);
-        mcg_apply_event(D, K, c, cg0, co, D.e_group[r], D.e_inst[r], D.e_weight[r], 0, refractory,
-                        s);
-        ++cur;
-        ++ndel;
-      }
-      if (K.n_stc_groups > 0) {
-        for (;;) {
-          int best = -1;
-          uint64_t bseq = ~0ull;
-          for (int gi = 0; gi < K.n_groups; ++gi) {
-            const McgCellGroup& G = D.cgs[cg0 + gi];
-            if (G.fifo < 0) continue;
-            const McgFifo& F = D.fifos[G.fifo];
-            if (F.head < F.tail) {
-              const int64_t slot = F.base + (F.head % F.cap);
-              if (D.fifo_step[slot] <= s) {
-                const uint64_t seq = D.fifo_si[slot] >> 32;
-                if (seq < bseq) {
-                  bseq = seq;
-                  best = gi;
-                }
-              }
-            }
-          }
-          if (best < 0) break;
-          McgFifo& F = D.fifos[D.cgs[cg0 + best].fifo];
-          const uint64_t si = D.fifo_si[F.base + (F.head % F.cap)];
-          ++F.head;
-          mcg_apply_event(D, K, c, cg0, co, best, uint32_t(si & 0xffffffffu), 0.0, 1, refractory,
-                          s);
-        }
-      }
-    }
-    __syncwarp();
-
-    // ---- 2. mechanism dynamics and current accumulation (engine.cpp:562-664)
-    const int nr = n > 1 ? n : 1;
-    for (int i = lane; i < nr; i += 32) rhs_cur[i] = 0.0;
-    bool has_gsyn = false, has_current = false;
-    __syncwarp();
-    for (int gi = 0; gi < K.n_groups; ++gi) {
-      McgCellGroup* G = &D.cgs[cg0 + gi];
-      const McgSpec& S = D.specs[G->spec];
-      const int kind = S.kind;
-      if (kind == MCG_SYN_STATIC_COND || kind == MCG_SYN_STDP_COND) {
-        if (G->active_n == 0) continue;
-        if (!has_gsyn) {
-          for (int i = lane; i < n; i += 32) {
-            gsyn[i] = 0.0;
-            gsyn_rhs[i] = 0.0;
-          }
-          has_gsyn = true;
-          __syncwarp();
-        }
-        mcg_decay_active(D, G, S.f_decay, true, gsyn, gsyn_rhs, S.e_rev, lane);
-      } else if (kind == MCG_SYN_STATIC_CURRENT || kind == MCG_SYN_HOMEO_CURRENT) {
-        if (G->active_n == 0) continue;
-        if (mcg_decay_active(D, G, S.f_decay, false, rhs_cur, nullptr, 0.0, lane))
-          has_current = true;
-      } else if (kind == MCG_SYN_STC_CHARGE) {
-        const int size = G->size;
-        const int64_t ib = G->inst;
-        if (stc_seq) {
-          if (lane == 0)
-            for (int i = 0; i < size; ++i) {
-              double delta = 0.0;
-              int comp = 0;
-              if (mcg_stc_instance(D, S, ib + i, gid, gi, i, s, prp_base, vol_k, &delta, &comp))
-                sps_base[comp] += delta;
-            }
-        } else {
-          for (int i0 = 0; i0 < size; i0 += 32) {
-            const int i = i0 + lane;
-            double delta = 0.0;
-            int comp = 0;
-            bool ch = false;
-            if (i < size)
-              ch = mcg_stc_instance(D, S, ib + i, gid, gi, i, s, prp_base, vol_k, &delta, &comp);
-            unsigned mm = __ballot_sync(MCG_FULL, ch);
-            if (sps_base) {
-              while (mm) {
-                const int l = __ffs(mm) - 1;
-                mm &= mm - 1;
-                const double dl = __shfl_sync(MCG_FULL, delta, l);
-                const int cl = __shfl_sync(MCG_FULL, comp, l);
-                if (lane == 0) sps_base[cl] += dl;
-              }
-            }
-          }
-        }
-        __syncwarp();
-      }
-    }
-
-    // background current (engine.cpp:652-664) and membrane update
-    if (lane == 0) {
-      const double ts = double(s) * D.dt;
-      const bool bg_gated = K.bg_t1 > K.bg_t0 && ts >= K.bg_t0 && ts < K.bg_t1;
-      if (is_lif && K.has_bg && !bg_gated) {
-        double ib = K.i_bg;
-        if (K.sig_bg != 0.0) {
-          const mcg_key key = mcg_make_key(D.seed, gid, 1, 0);
-          ib += K.sig_bg * mcg_normal_for(&key, static_cast<uint64_t>(s));
-        }
-        rhs_cur[K.noise_comp] += ib;
-        has_current = true;
-      }
-      // ---- 3. continuous state update (engine.cpp:666-719)
-      if (K.dyn == MCG_DYN_LIF_EXACT) {
-        if (!refractory) {
-          const double vinf = K.v_rev + K.r_mem * rhs_cur[0];
-          V[0] = vinf + (V[0] - vinf) * K.lif_exact_f;
-        }
-      } else if (K.dyn == MCG_DYN_LIF) {
-        if (!refractory) {
-          const double* gl = D.k_g_leak + K.arr;
-          const double* glr = D.k_g_leak_rhs + K.arr;
-          for (int i = 0; i < n; ++i) {
-            const double gs = gl[i] + (has_gsyn ? gsyn[i] : 0.0);
-            const double rr = glr[i] + (has_gsyn ? gsyn_rhs[i] : 0.0) + (has_current ? rhs_cur[i] : 0.0);
-            gsyn[i] = gs;
-            gsyn_rhs[i] = rr;
-          }
-          ok &= mcg_solve_tree(n, par, D.k_cap_dt + K.arr, gsyn, D.k_axial + K.arr, gsyn_rhs, V,
-                               D.s_diag + co, D.s_rhs + co);
-        }
-      } else if (K.dyn == MCG_DYN_HH) {
-        const double* gl = D.k_g_leak + K.arr;
-        const double* glr = D.k_g_leak_rhs + K.arr;
-        const double* gna_k = D.k_g_na + K.arr;
-        const double* gk_k = D.k_g_k + K.arr;
-        double* hm = D.hh_m + co;
-        double* hh = D.hh_h + co;
-        double* hn = D.hh_n + co;
-        const double dt = D.dt;
-        for (int i = 0; i < n; ++i) {
-          const double v = V[i];
-          double gsum = gl[i];
-          double grhs = glr[i];
-          if (gna_k[i] != 0.0) {
-            const double am = mcg_hh_am(v), bm = mcg_hh_bm(v);
-            const double ah = mcg_hh_ah(v), bh = mcg_hh_bh(v);
-            const double an = mcg_hh_an(v), bn = mcg_hh_bn(v);
-            double m = hm[i], h = hh[i], nn = hn[i];
-            m += (am / (am + bm) - m) * (1.0 - mcg_exp(-dt * (am + bm)));
-            h += (ah / (ah + bh) - h) * (1.0 - mcg_exp(-dt * (ah + bh)));
-            nn += (an / (an + bn) - nn) * (1.0 - mcg_exp(-dt * (an + bn)));
-            hm[i] = m;
-            hh[i] = h;
-            hn[i] = nn;
-            const double gna = gna_k[i] * m * m * m * h;
-            const double gk = gk_k[i] * nn * nn * nn * nn;
-            gsum += gna + gk;
-            grhs += gna * K.e_na + gk * K.e_k;
-          }
-          gsyn[i] = gsum + (has_gsyn ? gsyn[i] : 0.0);
-          gsyn_rhs[i] = grhs + (has_gsyn ? gsyn_rhs[i] : 0.0) + (has_current ? rhs_cur[i] : 0.0);
-        }
-        ok &= mcg_solve_tree(n, par, D.k_cap_dt + K.arr, gsyn, D.k_axial + K.arr, gsyn_rhs, V,
-                             D.s_diag + co, D.s_rhs + co);
-      }
-      // species
-      if (K.n_species > 0) ok &= mcg_species_update(D, K, so, co, D.k_sp_cap_dt, rhs_cur);
-    }
-    __syncwarp();
-
-    // ---- 4. spike detection, post-event hook, reset (engine.cpp:753-780)
-    int fired = 0;
-    double t_spike = 0.0;
-    if (lane == 0 && K.has_detector && !refractory) {
-      const double va = V[K.detector_comp];
-      const double vb = D.det_prev[c];
-      if (D.armed[c] && vb < K.threshold && va >= K.threshold) {
-        double f = (va > vb) ? (K.threshold - vb) / (va - vb) : 1.0;
-        f = (f < 0.0) ? 0.0 : ((1.0 < f) ? 1.0 : f);  // std::clamp
-        t_spike = (double(s) + f) * D.dt;
-        fired = 1;
-      }
-    }
-    fired = __shfl_sync(MCG_FULL, fired, 0);
-    if (fired) {
-      if (lane == 0) {
-        if (nsp < D.sp_cap) {
-          D.sp_step[int64_t(c) * D.sp_cap + nsp] = s;
-          D.sp_t[int64_t(c) * D.sp_cap + nsp] = t_spike;
-        } else {
-          atomicOr(D.err, MCG_ERR_FLAG_SPIKES);
-        }
-        ++nsp;
-      }
-      mcg_post_event(D, K, cg0, s, lane);
-      __syncwarp();
-      if (is_lif)
-        for (int i = lane; i < n; i += 32) V[i] = K.v_reset;
-      __syncwarp();
-    }
-    if (lane == 0 && K.has_detector && !refractory) {
-      if (fired) {
-        if (is_lif) D.refr_until[c] = s + 1 + K.ref_steps;
-        else D.armed[c] = 0;
-      } else if (!D.armed[c] && V[K.detector_comp] < K.threshold) {
-        D.armed[c] = 1;
-      }
-      D.det_prev[c] = V[K.detector_comp];
-    }
-    // probes (engine.cpp:785-793)
-    if (lane == 0) {
-      for (int q = D.probe_off[c]; q < D.probe_off[c + 1]; ++q) {
-        const int p = D.probe_idx[q];
-        const McgProbe& P = D.probes[p];
-        if ((s + 1) % P.every != 0) continue;
-        const int64_t m0 = (D.call_first + P.every) / P.every;
-        D.trace_buf[D.trace_base[p] + ((s + 1) / P.every - m0)] = mcg_probe_value(D, K, c, P);
-      }
-    }
-    __syncwarp();
-  }
-  if (lane == 0) {
-    D.ev_cursor[c] = cur;
-    D.sp_count[c] = nsp < D.sp_cap ? nsp : D.sp_cap;
-    if (ndel) atomicAdd(D.delivered, ndel);
-    if (!ok) atomicOr(D.err, MCG_ERR_FLAG_SINGULAR);
-  }
-}
-
 // ---------------------------------------------------------------------------
 // spike compaction and carry-over of undelivered events
 // ---------------------------------------------------------------------------
@@ -607,81 +319,3 @@ __global__ void k_ff_reset(McgDev D, int64_t n_cg) {
   G.active_n = 0;
 }
 
-__global__ void __launch_bounds__(128) k_ff(McgDev D, const double* fh_spec, const double* sp_cap_ff,
-                                            double dtc, int64_t n_coarse, int64_t step0,
-                                            int64_t per) {
-  const int lane = threadIdx.x & 31;
-  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (c >= D.n_cells) return;
-  const McgKind& K = D.kinds[D.cell_kind[c]];
-  const int n = K.n;
-  const int64_t co = D.comp_off[c], so = D.sp_off[c], cg0 = D.cg_off[c];
-  const double* prp_base = (K.prp_idx >= 0) ? D.species + so + int64_t(K.prp_idx) * n : nullptr;
-  double* sps_base = (K.sps_idx >= 0) ? D.species + so + int64_t(K.sps_idx) * n : nullptr;
-  const double* vol_k = D.k_volume + K.arr;
-  const bool stc_seq = sps_base != nullptr && (const double*)sps_base == prp_base;
-  bool ok = true;
-  for (int64_t q = 0; q < n_coarse; ++q) {
-    for (int gi = 0; gi < K.n_groups; ++gi) {
-      const McgCellGroup G = D.cgs[cg0 + gi];
-      const McgSpec& S = D.specs[G.spec];
-      if (S.kind != MCG_SYN_STC_CHARGE) continue;
-      const double fh = fh_spec[G.spec];
-      for (int i0 = 0; i0 < G.size; i0 += (stc_seq ? G.size : 32)) {
-        const int i = stc_seq ? i0 : i0 + lane;
-        bool ch = false;
-        double delta = 0.0;
-        int comp = 0;
-        if (i < G.size && (!stc_seq || lane == 0)) {
-          for (int ii = i; ii < (stc_seq ? G.size : i + 1); ++ii) {
-            const int64_t j = G.inst + ii;
-            double h = S.h0 + (D.i_stc_h[j] - S.h0) * fh;
-            double z = D.i_stc_z[j];
-            const double na = fabs(h - S.h0);
-            comp = D.i_comp[j];
-            if (na != D.i_sps_abs[j]) {
-              delta = (na - D.i_sps_abs[j]) / vol_k[comp];
-              D.i_sps_abs[j] = na;
-              ch = true;
-              if (stc_seq && sps_base) sps_base[comp] += delta;
-            }
-            if (prp_base) {
-              const double prp = prp_base[comp];
-              if (!(prp <= 0.0)) {
-                double dd = 0.0;
-                if (h - S.h0 > S.theta_tag) dd += (1.0 - z);
-                if (S.h0 - h > S.theta_tag) dd -= (z + 0.5);
-                z += prp * S.f_int * dd * dtc / S.tau_z;
-              }
-            }
-            D.i_stc_h[j] = h;
-            D.i_stc_z[j] = z;
-          }
-        }
-        if (!stc_seq) {
-          unsigned mm = __ballot_sync(MCG_FULL, ch);
-          if (sps_base) {
-            while (mm) {
-              const int l = __ffs(mm) - 1;
-              mm &= mm - 1;
-              const double dl = __shfl_sync(MCG_FULL, delta, l);
-              const int cl = __shfl_sync(MCG_FULL, comp, l);
-              if (lane == 0) sps_base[cl] += dl;
-            }
-          }
-        }
-      }
-      __syncwarp();
-    }
-    if (lane == 0) {
-      if (K.n_species > 0) ok &= mcg_species_update(D, K, so, co, sp_cap_ff, D.s_rhs_cur + co);
-      // forced probe sample at step_ - 1 after the coarse step (engine.cpp:1031-1032)
-      for (int qq = D.probe_off[c]; qq < D.probe_off[c + 1]; ++qq) {
-        const int p = D.probe_idx[qq];
-        D.trace_buf[D.trace_base[p] + q] = mcg_probe_value(D, K, c, D.probes[p]);
-      }
-    }
-    __syncwarp();
-  }
-  if (lane == 0 && !ok) atomicOr(D.err, MCG_ERR_FLAG_SINGULAR);
-}

@@ -38,6 +38,12 @@ struct McgKind {
   double lif_exact_f;     // exp(-dt / tau_mem)                  (engine.cpp:671)
   double prp_theta_star, prp_rate;  // PrpSynthesisParams      (mechanisms.hpp:253)
   double e_na, e_k;
+  // Constant-diagonal systems: the Hines elimination of the diagonal does not
+  // depend on the state, so its factors f[i] = coupling[i]/diag[i] and the
+  // eliminated diagonal d[i] are precomputed with solve_tree's own operation
+  // sequence (tree_solver.cpp:55-70).  v_const: the LIF-cable V system when
+  // no conductance synapse is active (gs = g_leak + 0.0); sp_const: species.
+  int32_t v_const, sp_const;
 };
 
 // SynSpec per kind placement (recipe.hpp:82-98) + hoisted constants

@@ -1,0 +1,13 @@
+#!/usr/bin/env bash
+# One GPU session: bench line, ncu launch list, one full ncu capture of k_epoch.
+set -u
+mkdir -p gpurun_out
+python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+tail -c 3000 gpurun_out/bench.json
+ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
+    --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
+    > gpurun_out/ncu_launch.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_epoch -s 30 -c 1 \
+    -o gpurun_out/epoch python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
+    > gpurun_out/ncu_full.log 2>&1
+ls -la gpurun_out
