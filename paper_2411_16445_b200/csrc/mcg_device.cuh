@@ -63,12 +63,19 @@ struct McgDev {
   int64_t* i_stdp_last;
   double* i_homeo_w;
   double *i_stc_h, *i_stc_z, *i_stc_c, *i_sps_abs;
-  // events of this epoch (sorted keys) and the edge table
-  const uint64_t* keys;
-  const int64_t* ev_begin;  // n_cells + 1
-  int64_t* ev_cursor;       // n_cells
-  int32_t rank_bits, step_bits;
-  int64_t key_base;         // step of key step-field 0
+  // per-cell inboxes (mcg_events.cuh): incoming keys of this epoch (unsorted)
+  // and the sorted pending list, double buffered; key = step << rank_bits | rank
+  uint64_t* inc;
+  int32_t* inc_n;
+  int32_t inc_cap;
+  uint64_t* pend;
+  int32_t* pend_sel;
+  int32_t* pend_off;
+  int32_t* pend_n;
+  int32_t pend_cap;
+  int32_t rank_bits;
+  const int64_t* ctl;       // [0] batch base step, [1] target step, [2] epoch length
+  int32_t* abort;
   const int32_t* e_dst;
   const int32_t* e_group;
   const uint32_t* e_inst;
@@ -85,7 +92,6 @@ struct McgDev {
   const int32_t* probe_idx;
   double* trace_buf;
   const int64_t* trace_base;  // per probe
-  int64_t call_first;         // first step of the current advance call
   // status
   int32_t* err;
   unsigned long long* delivered;

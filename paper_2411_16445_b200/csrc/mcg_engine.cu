@@ -1,13 +1,17 @@
 // mcg_engine.cu — host orchestration of the B200 engine and the C ABI
 // (include/mcg.h).
 //
-// Engine::advance_to (engine.cpp:909-945) becomes, per min-delay epoch:
-//   A  k_source_fire + k_spike_outdeg  -> one small D2H read of the counters
-//   B  k_write_*_events, CUB radix sort of the 64-bit event keys, k_offsets
-//   C  k_epoch: every cell, every step of the epoch, one warp per cell
-//   D  ordered spike compaction (CUB scan + k_spike_write), leftover carry
-// All state stays resident in HBM; the host sees only counters, and spikes /
-// traces / cell state when asked (the lazily-synced mirror of engine.hpp).
+// Engine::advance_to (engine.cpp:909-945) runs as batches of min-delay epochs.
+// One batch is a CUDA graph of E epochs, each epoch
+//   k_inbox        source events of the epoch + spike exchange of the previous
+//                  epoch into per-cell incoming buffers        (mcg_events.cuh)
+//   k_epoch        every cell, every step of the epoch, one warp per cell;
+//                  inbox sort + merge at entry                  (mcg_epoch.cuh)
+//   scan + k_spike_write/total   ordered spike compaction     (mcg_events.cuh)
+// Epoch bounds live in device memory, so the graph is replayed unchanged; the
+// host synchronizes once per batch (spike log, overflow/abort flags).  All
+// state stays resident in HBM; cell state, spikes and traces are copied to
+// the host only when asked (the lazily-synced mirror of engine.hpp).
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
@@ -54,16 +58,8 @@ struct DBuf {
     if (!v.empty())
       CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
   }
-  // grow, keeping the first `keep` elements
-  void grow(size_t count, size_t keep, cudaStream_t st) {
-    if (count <= n) return;
-    T* q = nullptr;
-    CK(cudaMalloc(&q, count * sizeof(T)));
-    if (p && keep) CK(cudaMemcpyAsync(q, p, keep * sizeof(T), cudaMemcpyDeviceToDevice, st));
-    CK(cudaStreamSynchronize(st));
-    if (p) cudaFree(p);
-    p = q;
-    n = count;
+  void zero(cudaStream_t st) {
+    if (p) CK(cudaMemsetAsync(p, 0, n * sizeof(T), st));
   }
 };
 
@@ -73,18 +69,22 @@ int bits_for(uint64_t v) {  // bits needed to represent values in [0, v]
   return b;
 }
 
-// counters block (device, mirrored to pinned host memory once per epoch)
-enum {
-  C_FIRE = 0,
-  C_SRC_EV = 1,
-  C_SPK_EV = 2,
-  C_LEFT = 3,
-  C_EP_SPK = 4,
-  C_LOG = 5,
-  C_WCUR = 6,
-  C_DELIVERED = 7,
-  C_N = 8
-};
+// device counters, mirrored to pinned host memory once per batch
+enum { C_EP_SPK = 0, C_LOG = 1, C_DELIVERED = 2, C_N = 4 };
+
+// anything still undelivered: queued keys, unexpanded spikes with local
+// fan-out, or delayed calcium (the fast-forward guard, engine.cpp:958-960)
+__global__ void k_pending(McgDev D, const uint32_t* ep_gid, const unsigned long long* ep_n,
+                          const int64_t* out_begin, const int64_t* out_end, int32_t n_fifos,
+                          int32_t* flag) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < D.n_cells && (D.pend_n[i] > D.pend_off[i] || D.inc_n[i] > 0)) atomicOr(flag, 1);
+  if (i < n_fifos && D.fifos[i].head < D.fifos[i].tail) atomicOr(flag, 1);
+  if (i < static_cast<int64_t>(*ep_n)) {
+    const uint32_t g = ep_gid[i];
+    if (out_end[g] > out_begin[g]) atomicOr(flag, 1);
+  }
+}
 
 }  // namespace
 
@@ -93,15 +93,17 @@ struct Engine {
   cudaStream_t st = nullptr;
   int device = 0;
   int64_t step = 0;
-  int64_t free_epoch = 1024;  // epoch length when there are no cell-to-cell edges
-  int64_t max_epoch = 1;
+  int64_t L = 1;              // epoch length (min_delay_steps, or free_epoch without cell edges)
+  static constexpr int kSmemMaxComps = 96;  // cells up to this size live in shared memory
+  static constexpr int kBlock = 128;        // 4 warps = 4 cells per block
+  static constexpr int kBatch = 32;         // epochs per graph launch
 
   // device model
   DBuf<McgKind> d_kinds;
   DBuf<McgSpec> d_specs;
   DBuf<int32_t> d_k_parent;
   DBuf<double> d_k_cap_dt, d_k_g_leak, d_k_g_leak_rhs, d_k_axial, d_k_g_na, d_k_g_k, d_k_cf,
-      d_k_volume, d_k_sp_cap_dt, d_k_sp_gs, d_k_sp_coupling;
+      d_k_volume, d_k_sp_cap_dt, d_k_sp_gs, d_k_sp_coupling, d_k_vf, d_k_vd, d_k_sp_f, d_k_sp_d;
   DBuf<int32_t> d_cell_kind;
   DBuf<int64_t> d_comp_off, d_sp_off, d_cg_off;
   DBuf<double> d_v, d_hh_m, d_hh_h, d_hh_n, d_species, d_det_prev;
@@ -109,9 +111,6 @@ struct Engine {
   DBuf<int64_t> d_refr;
   DBuf<uint32_t> d_iseq;
   DBuf<double> d_s_gsyn, d_s_gsyn_rhs, d_s_rhs_cur, d_s_diag, d_s_rhs, d_s_r2;
-  DBuf<double> d_k_vf, d_k_vd, d_k_sp_f, d_k_sp_d;
-  static constexpr int kSmemMaxComps = 96;  // cells up to this size live in shared memory
-  static constexpr int kBlock = 128;        // 4 warps = 4 cells per block
   int32_t sp_max = 0, smem_n = 0, smem_stride = 0;
   size_t smem_bytes = 0;
   DBuf<McgCellGroup> d_cgs;
@@ -127,19 +126,19 @@ struct Engine {
   DBuf<uint32_t> d_e_inst;
   DBuf<double> d_e_weight;
   DBuf<int64_t> d_e_delay, d_out_begin, d_out_end, d_src_edge_off, d_src_edges;
-  int32_t rank_bits = 1, step_bits = 1, dst_bits = 1;
+  int32_t rank_bits = 1;
   // sources
   DBuf<McgSrcTask> d_tasks;
   DBuf<int64_t> d_scripted;
-  DBuf<int32_t> d_fire_src;
-  DBuf<int64_t> d_fire_step;
   int32_t n_tasks = 0;
-  int64_t fire_cap = 0;
-  // events
-  DBuf<uint64_t> d_keys_work, d_keys_sorted;
-  DBuf<int64_t> d_ev_begin, d_ev_cursor, d_left, d_left_scan;
-  DBuf<unsigned char> d_cub_tmp;
-  int64_t key_base = 0;
+  // inboxes
+  DBuf<uint64_t> d_inc, d_pend;
+  DBuf<int32_t> d_inc_n, d_pend_sel, d_pend_off, d_pend_n;
+  int32_t inc_cap = 32, pend_cap = 64;
+  // epoch control
+  DBuf<int64_t> d_ctl;
+  int64_t* h_ctl = nullptr;
+  DBuf<int32_t> d_abort;
   // spikes
   int32_t sp_cap = 1;
   DBuf<int32_t> d_sp_count;
@@ -147,37 +146,45 @@ struct Engine {
   DBuf<double> d_sp_t;
   DBuf<uint32_t> d_ep_gid;
   DBuf<int64_t> d_ep_step;
-  DBuf<double> d_log_t;
+  DBuf<double> d_log_t;       // batch log
   DBuf<uint32_t> d_log_gid;
+  DBuf<unsigned char> d_cub_tmp;
   // probes
   DBuf<McgProbe> d_probes;
   DBuf<int32_t> d_probe_off, d_probe_idx;
   DBuf<double> d_trace;
   DBuf<int64_t> d_trace_base;
+  std::vector<int64_t> probe_base_host;
+  int64_t probe_total = 0;
   std::vector<std::vector<std::pair<double, double>>> traces;
   // status
   DBuf<unsigned long long> d_ctr;
   DBuf<int32_t> d_err;
   unsigned long long* h_ctr = nullptr;
   int32_t* h_err = nullptr;
+  int32_t* h_abort = nullptr;
   // host spike mirror
   std::vector<double> spk_t;
   std::vector<uint32_t> spk_gid;
-  int64_t log_count = 0;   // device log length at the last sync
-  int64_t host_synced = 0; // mirrored prefix
+  // graph of one batch
+  cudaGraphExec_t gexec = nullptr;
+  bool graph_timed = false;
+  double* graph_trace = nullptr;
+  std::vector<cudaEvent_t> ev_epoch;
   // stats
   mcg_stats stats{};
   bool timing = false;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr, eva = nullptr, evb = nullptr;
-  bool ev_pending = false;
+  cudaEvent_t eva = nullptr, evb = nullptr;
 
   McgDev dev{};
 
   ~Engine() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    for (cudaEvent_t e : ev_epoch) cudaEventDestroy(e);
     if (h_ctr) cudaFreeHost(h_ctr);
     if (h_err) cudaFreeHost(h_err);
-    if (ev0) cudaEventDestroy(ev0);
-    if (ev1) cudaEventDestroy(ev1);
+    if (h_abort) cudaFreeHost(h_abort);
+    if (h_ctl) cudaFreeHost(h_ctl);
     if (eva) cudaEventDestroy(eva);
     if (evb) cudaEventDestroy(evb);
     if (st) cudaStreamDestroy(st);
@@ -192,23 +199,28 @@ struct Engine {
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     CK(cudaMallocHost(&h_ctr, C_N * sizeof(unsigned long long)));
     CK(cudaMallocHost(&h_err, sizeof(int32_t)));
-    CK(cudaEventCreate(&ev0));
-    CK(cudaEventCreate(&ev1));
+    CK(cudaMallocHost(&h_abort, sizeof(int32_t)));
+    CK(cudaMallocHost(&h_ctl, 4 * sizeof(int64_t)));
     CK(cudaEventCreate(&eva));
     CK(cudaEventCreate(&evb));
+    ev_epoch.resize(2 * kBatch);
+    for (auto& e : ev_epoch) CK(cudaEventCreate(&e));
     const int nl = n_local();
-    // epoch bounds
-    free_epoch = std::clamp<int64_t>((int64_t(1) << 22) / std::max(nl, 1), 16, 4096);
-    max_epoch = m.min_delay_steps > 0 ? m.min_delay_steps : free_epoch;
-    sp_cap = static_cast<int32_t>(max_epoch);
-    // key layout: dst | step | rank
+    // epoch length: min delay (cells independent within it, engine.cpp:913-915)
+    const int64_t free_epoch = std::clamp<int64_t>((int64_t(1) << 22) / std::max(nl, 1), 16, 4096);
+    L = m.min_delay_steps > 0 ? m.min_delay_steps : free_epoch;
+    // spikes per cell per epoch: at most one per (ref_steps + 1) steps (LIF)
+    // or every other step (HH hysteresis)
+    sp_cap = 1;
+    for (const McgKind& K : m.kinds) {
+      int64_t b = 0;
+      if (K.dyn == MCG_DYN_LIF || K.dyn == MCG_DYN_LIF_EXACT) b = (L + K.ref_steps) / (K.ref_steps + 1);
+      else if (K.dyn == MCG_DYN_HH) b = (L + 1) / 2;
+      sp_cap = static_cast<int32_t>(std::max<int64_t>(sp_cap, std::min<int64_t>(b, L)));
+    }
     const int64_t ne = static_cast<int64_t>(m.e_dst.size());
     rank_bits = bits_for(static_cast<uint64_t>(std::max<int64_t>(ne, 1)));
-    dst_bits = bits_for(static_cast<uint64_t>(std::max(nl, 1)));
-    int64_t max_step_rel = m.max_delay_steps + 2 * max_epoch + 2;
-    step_bits = bits_for(static_cast<uint64_t>(max_step_rel));
-    if (rank_bits + step_bits + dst_bits > 64)
-      throw Error(MCG_ERR_ENGINE, "event key exceeds 64 bits (too many edges/cells/delay steps)");
+    if (rank_bits > 30) throw Error(MCG_ERR_ENGINE, "too many local edges for the event key");
 
     d_kinds.upload(m.kinds, st);
     d_specs.upload(m.specs, st);
@@ -224,6 +236,10 @@ struct Engine {
     d_k_sp_cap_dt.upload(m.k_sp_cap_dt, st);
     d_k_sp_gs.upload(m.k_sp_gs, st);
     d_k_sp_coupling.upload(m.k_sp_coupling, st);
+    d_k_vf.upload(m.k_vf, st);
+    d_k_vd.upload(m.k_vd, st);
+    d_k_sp_f.upload(m.k_sp_f, st);
+    d_k_sp_d.upload(m.k_sp_d, st);
     d_cell_kind.upload(m.cell_kind, st);
     d_comp_off.upload(m.comp_off, st);
     d_sp_off.upload(m.sp_off, st);
@@ -243,17 +259,11 @@ struct Engine {
     d_s_rhs_cur.alloc(nc);
     d_s_diag.alloc(nc);
     d_s_rhs.alloc(nc);
-    sp_max = 0;
-    smem_n = 0;
     for (const McgKind& K : m.kinds) {
       sp_max = std::max(sp_max, K.n_species);
       if (K.n <= kSmemMaxComps) smem_n = std::max(smem_n, K.n);
     }
     d_s_r2.alloc(nc * (1 + sp_max));
-    d_k_vf.upload(m.k_vf, st);
-    d_k_vd.upload(m.k_vd, st);
-    d_k_sp_f.upload(m.k_sp_f, st);
-    d_k_sp_d.upload(m.k_sp_d, st);
     smem_stride = (9 + 2 * sp_max) * smem_n;
     smem_bytes = static_cast<size_t>(smem_stride) * sizeof(double) * (kBlock / 32);
     CK(cudaFuncSetAttribute(k_epoch, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -287,67 +297,65 @@ struct Engine {
     d_src_edge_off.upload(m.src_edge_off, st);
     d_src_edges.upload(m.src_edges, st);
 
-    // source tasks
+    // source tasks: one per Poisson window, one per regular/scripted source
     std::vector<McgSrcTask> tasks;
     std::vector<int64_t> scripted;
-    fire_cap = 0;
     for (size_t s = 0; s < m.sources.size(); ++s) {
       const Source& S = m.sources[s];
+      McgSrcTask T{};
+      T.source = static_cast<int32_t>(s);
+      T.type = S.type;
       if (S.type == MCG_SRC_POISSON) {
         for (size_t w = 0; w < S.prob.size(); ++w) {
-          McgSrcTask T{};
-          T.source = static_cast<int32_t>(s);
-          T.type = MCG_SRC_POISSON;
           T.window = static_cast<int32_t>(w);
           T.a = S.a[w];
           T.b = S.b[w];
           T.prob = S.prob[w];
           tasks.push_back(T);
-          fire_cap += max_epoch;
         }
       } else if (S.type == MCG_SRC_REGULAR) {
-        McgSrcTask T{};
-        T.source = static_cast<int32_t>(s);
-        T.type = MCG_SRC_REGULAR;
         T.r_t0 = S.r_t0;
         T.r_period = S.r_period;
         T.r_count = S.r_count;
         tasks.push_back(T);
-        fire_cap += max_epoch + 4;
       } else {
-        McgSrcTask T{};
-        T.source = static_cast<int32_t>(s);
-        T.type = MCG_SRC_SCRIPTED;
         T.a = static_cast<int64_t>(scripted.size());
         for (int64_t x : S.steps) scripted.push_back(x);
         T.b = static_cast<int64_t>(scripted.size());
         tasks.push_back(T);
-        fire_cap += static_cast<int64_t>(S.steps.size());
       }
     }
     n_tasks = static_cast<int32_t>(tasks.size());
     d_tasks.upload(tasks, st);
     d_scripted.upload(scripted, st);
-    fire_cap = std::max<int64_t>(fire_cap, 1);
-    d_fire_src.alloc(fire_cap);
-    d_fire_step.alloc(fire_cap);
 
-    // events and spikes
-    d_keys_work.alloc(1024);
-    d_keys_sorted.alloc(1024);
-    d_ev_begin.alloc(nl + 1);
-    d_ev_cursor.alloc(std::max(nl, 1));
-    d_left.alloc(std::max(nl, 1));
-    d_left_scan.alloc(std::max(nl, 1));
+    // inboxes, sized from the mean in-degree; grown on overflow
+    {
+      const double per_cell = double(ne) / std::max(nl, 1);
+      while (inc_cap < 4 * per_cell && inc_cap < (1 << 20)) inc_cap <<= 1;
+      pend_cap = 2 * inc_cap;
+    }
+    alloc_inboxes();
+    d_ctl.alloc(4);
+    d_abort.alloc(1);
+    d_abort.zero(st);
+
+    const size_t slots = static_cast<size_t>(std::max(nl, 1)) * sp_cap;
     d_sp_count.alloc(std::max(nl, 1));
+    d_sp_count.zero(st);
     d_sp_scan.alloc(std::max(nl, 1));
-    d_sp_step.alloc(static_cast<size_t>(std::max(nl, 1)) * sp_cap);
-    d_sp_t.alloc(static_cast<size_t>(std::max(nl, 1)) * sp_cap);
-    d_ep_gid.alloc(static_cast<size_t>(std::max(nl, 1)) * sp_cap);
-    d_ep_step.alloc(static_cast<size_t>(std::max(nl, 1)) * sp_cap);
-    d_log_t.alloc(4096);
-    d_log_gid.alloc(4096);
-    ensure_cub(1024);
+    d_sp_step.alloc(slots);
+    d_sp_t.alloc(slots);
+    d_ep_gid.alloc(slots);
+    d_ep_step.alloc(slots);
+    d_log_t.alloc(slots * kBatch);
+    d_log_gid.alloc(slots * kBatch);
+    {
+      size_t need = 0;
+      CK(cub::DeviceScan::ExclusiveSum(nullptr, need, d_sp_count.p, d_sp_scan.p,
+                                       std::max(nl, 1), st));
+      d_cub_tmp.alloc(std::max<size_t>(need, 16));
+    }
 
     // probes: per-cell CSR over local probes
     std::vector<int32_t> poff(nl + 1, 0), pidx;
@@ -368,10 +376,9 @@ struct Engine {
     traces.assign(m.probes.size(), {});
 
     d_ctr.alloc(C_N);
+    d_ctr.zero(st);
     d_err.alloc(1);
-    CK(cudaMemsetAsync(d_ctr.p, 0, C_N * sizeof(unsigned long long), st));
-    CK(cudaMemsetAsync(d_err.p, 0, sizeof(int32_t), st));
-    CK(cudaMemsetAsync(d_sp_count.p, 0, std::max(nl, 1) * sizeof(int32_t), st));
+    d_err.zero(st);
     CK(cudaStreamSynchronize(st));
 
     stats.total_comps = m.total_comps;
@@ -382,17 +389,38 @@ struct Engine {
     refresh_dev();
   }
 
-  void ensure_cub(int64_t n) {
-    size_t need = 0, need2 = 0;
-    CK(cub::DeviceRadixSort::SortKeys(nullptr, need, d_keys_work.p, d_keys_sorted.p,
-                                      static_cast<int>(n), 0, 64, st));
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, need2, d_sp_count.p, d_sp_scan.p,
-                                     std::max(n_local(), 1), st));
-    size_t need3 = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, need3, d_left.p, d_left_scan.p,
-                                     std::max(n_local(), 1), st));
-    need = std::max(need, std::max(need2, need3));
-    if (need > d_cub_tmp.n) d_cub_tmp.alloc(need * 2);
+  void alloc_inboxes() {
+    const size_t nl = static_cast<size_t>(std::max(n_local(), 1));
+    d_inc.alloc(nl * inc_cap);
+    d_pend.alloc(nl * 2 * pend_cap);
+    d_inc_n.alloc(nl);
+    d_inc_n.zero(st);
+    d_pend_sel.alloc(nl);
+    d_pend_sel.zero(st);
+    d_pend_off.alloc(nl);
+    d_pend_off.zero(st);
+    d_pend_n.alloc(nl);
+    d_pend_n.zero(st);
+  }
+
+  // double both inbox capacities, keeping the pending keys
+  void grow_inboxes() {
+    const int nl = n_local();
+    const int32_t old_pend = pend_cap;
+    DBuf<uint64_t> np;
+    inc_cap *= 2;
+    pend_cap *= 2;
+    np.alloc(static_cast<size_t>(std::max(nl, 1)) * 2 * pend_cap);
+    if (nl > 0)
+      k_pend_regrow<<<(nl * 32 + 127) / 128, 128, 0, st>>>(d_pend.p, old_pend, np.p, pend_cap,
+                                                           d_pend_sel.p, d_pend_off.p,
+                                                           d_pend_n.p, nl);
+    CK(cudaStreamSynchronize(st));
+    std::swap(d_pend.p, np.p);
+    std::swap(d_pend.n, np.n);
+    d_inc.alloc(static_cast<size_t>(std::max(nl, 1)) * inc_cap);
+    d_inc_n.zero(st);
+    invalidate_graph();
   }
 
   void refresh_dev() {
@@ -458,12 +486,17 @@ struct Engine {
     D.i_stc_z = d_i_stc_z.p;
     D.i_stc_c = d_i_stc_c.p;
     D.i_sps_abs = d_i_sps_abs.p;
-    D.keys = d_keys_sorted.p;
-    D.ev_begin = d_ev_begin.p;
-    D.ev_cursor = d_ev_cursor.p;
+    D.inc = d_inc.p;
+    D.inc_n = d_inc_n.p;
+    D.inc_cap = inc_cap;
+    D.pend = d_pend.p;
+    D.pend_sel = d_pend_sel.p;
+    D.pend_off = d_pend_off.p;
+    D.pend_n = d_pend_n.p;
+    D.pend_cap = pend_cap;
     D.rank_bits = rank_bits;
-    D.step_bits = step_bits;
-    D.key_base = key_base;
+    D.ctl = d_ctl.p;
+    D.abort = d_abort.p;
     D.e_dst = d_e_dst.p;
     D.e_group = d_e_group.p;
     D.e_inst = d_e_inst.p;
@@ -482,36 +515,72 @@ struct Engine {
     D.delivered = d_ctr.p + C_DELIVERED;
   }
 
-  McgSrcDev src_dev() {
-    McgSrcDev S{};
-    S.tasks = d_tasks.p;
-    S.n_tasks = n_tasks;
-    S.scripted_steps = d_scripted.p;
-    S.src_edge_off = d_src_edge_off.p;
-    S.src_edges = d_src_edges.p;
-    S.fire_src = d_fire_src.p;
-    S.fire_step = d_fire_step.p;
-    S.fire_cap = fire_cap;
-    S.ctr = d_ctr.p;
-    S.err = d_err.p;
-    return S;
-  }
-
-  McgEvDev ev_dev() {
-    McgEvDev E{};
-    E.keys = d_keys_work.p;
-    E.wcur = d_ctr.p + C_WCUR;
-    E.rank_bits = rank_bits;
-    E.step_bits = step_bits;
-    E.base = key_base;
+  McgEv ev_dev() {
+    McgEv E{};
+    E.tasks = d_tasks.p;
+    E.n_tasks = n_tasks;
+    E.scripted_steps = d_scripted.p;
+    E.src_edge_off = d_src_edge_off.p;
+    E.src_edges = d_src_edges.p;
     E.e_dst = d_e_dst.p;
     E.e_delay = d_e_delay.p;
     E.out_begin = d_out_begin.p;
     E.out_end = d_out_end.p;
+    E.inc = d_inc.p;
+    E.inc_n = d_inc_n.p;
+    E.inc_cap = inc_cap;
+    E.pend_off = d_pend_off.p;
+    E.pend_n = d_pend_n.p;
+    E.pend_cap = pend_cap;
+    E.rank_bits = rank_bits;
+    E.ctl = d_ctl.p;
+    E.abort = d_abort.p;
+    E.ep_gid = d_ep_gid.p;
+    E.ep_step = d_ep_step.p;
+    E.ep_n = d_ctr.p + C_EP_SPK;
+    E.seed = m.seed;
+    E.dt = m.dt;
     return E;
   }
 
-  void launched(int k = 1) { stats.kernel_launches += k; }
+  void invalidate_graph() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    gexec = nullptr;
+  }
+
+  // the kernels of epoch j of a batch (captured into the graph)
+  void enqueue_epoch(int32_t j) {
+    const int nl = n_local();
+    const McgEv E = ev_dev();
+    const int64_t work = std::max<int64_t>(int64_t(n_tasks) * L, int64_t(nl) * sp_cap * 32);
+    const unsigned ib = static_cast<unsigned>(std::clamp<int64_t>((work + 255) / 256, 1, 148 * 8));
+    k_inbox<<<ib, 256, 0, st>>>(E, j, L);
+    if (nl == 0) return;
+    // external event nodes: readable after the graph ran (plain records inside
+    // a capture only become internal dependencies)
+    if (timing) CK(cudaEventRecordWithFlags(ev_epoch[2 * j], st, cudaEventRecordExternal));
+    k_epoch<<<(nl * 32 + kBlock - 1) / kBlock, kBlock, smem_bytes, st>>>(dev, j);
+    if (timing) CK(cudaEventRecordWithFlags(ev_epoch[2 * j + 1], st, cudaEventRecordExternal));
+    size_t tb = d_cub_tmp.n;
+    CK(cub::DeviceScan::ExclusiveSum(d_cub_tmp.p, tb, d_sp_count.p, d_sp_scan.p, nl, st));
+    k_spike_write<<<(nl + 127) / 128, 128, 0, st>>>(dev, j, d_sp_scan.p, d_ep_gid.p, d_ep_step.p,
+                                                    d_log_t.p, d_log_gid.p, d_ctr.p + C_LOG);
+    k_spike_total<<<1, 1, 0, st>>>(dev, j, d_sp_scan.p, d_ctr.p + C_EP_SPK, d_ctr.p + C_LOG);
+  }
+  static constexpr int kKernelsPerEpoch = 6;
+
+  void capture_graph() {
+    invalidate_graph();
+    refresh_dev();
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    for (int32_t j = 0; j < kBatch; ++j) enqueue_epoch(j);
+    CK(cudaStreamEndCapture(st, &g));
+    CK(cudaGraphInstantiate(&gexec, g, 0));
+    CK(cudaGraphDestroy(g));
+    graph_timed = timing;
+    graph_trace = d_trace.p;
+  }
 
   void check_err() {
     if (*h_err == 0) return;
@@ -521,124 +590,69 @@ struct Engine {
     if (e & MCG_ERR_FLAG_SINGULAR) throw Error(MCG_ERR_NUMERIC, "tree solve: singular system");
     if (e & MCG_ERR_FLAG_FIFO) throw Error(MCG_ERR_ENGINE, "internal event queue overflow");
     if (e & MCG_ERR_FLAG_ACTIVE) throw Error(MCG_ERR_ENGINE, "active synapse list overflow");
-    if (e & MCG_ERR_FLAG_SPIKES) throw Error(MCG_ERR_ENGINE, "spike/firing buffer overflow");
+    if (e & MCG_ERR_FLAG_SPIKES) throw Error(MCG_ERR_ENGINE, "spike buffer overflow");
   }
 
-  // counters -> host (the one synchronization point per epoch)
-  void sync_counters() {
+  void sync_counters_raw() {
     CK(cudaMemcpyAsync(h_ctr, d_ctr.p, C_N * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(h_err, d_err.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_abort, d_abort.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (ev_pending) {
-      float ms = 0;
-      CK(cudaEventElapsedTime(&ms, ev0, ev1));
-      stats.epoch_kernel_ms += ms;
-      ev_pending = false;
-    }
     stats.events_delivered = static_cast<int64_t>(h_ctr[C_DELIVERED]);
-    log_count = static_cast<int64_t>(h_ctr[C_LOG]);
-    check_err();
   }
 
-  void run_epoch(int64_t s0, int64_t s1) {
-    const int nl = n_local();
-    const int64_t len = s1 - s0;
-    // ---- A: count this epoch's source firings and the previous epoch's fan-out
-    CK(cudaMemsetAsync(d_ctr.p + C_FIRE, 0, 3 * sizeof(unsigned long long), st));
-    if (n_tasks > 0) {
-      const int64_t nt = int64_t(n_tasks) * len;
-      k_source_fire<<<static_cast<unsigned>((nt + 255) / 256), 256, 0, st>>>(src_dev(), m.seed,
-                                                                          m.dt, s0, s1);
-      launched();
-    }
-    const int64_t max_ep = static_cast<int64_t>(nl) * sp_cap;
-    if (max_ep > 0) {
-      k_spike_outdeg<<<static_cast<unsigned>((max_ep + 255) / 256), 256, 0, st>>>(
-          d_ep_gid.p, d_ctr.p + C_EP_SPK, d_out_begin.p, d_out_end.p, d_ctr.p + C_SPK_EV);
-      launched();
-    }
-    sync_counters();
-    const int64_t n_left = static_cast<int64_t>(h_ctr[C_LEFT]);
-    const int64_t n_fire = static_cast<int64_t>(h_ctr[C_FIRE]);
-    const int64_t n_new = static_cast<int64_t>(h_ctr[C_SRC_EV] + h_ctr[C_SPK_EV]);
-    const int64_t n_tot = n_left + n_new;
-    const int64_t n_ep = static_cast<int64_t>(h_ctr[C_EP_SPK]);
-    if (n_fire > fire_cap) throw Error(MCG_ERR_ENGINE, "source firing buffer overflow");
-    if (static_cast<size_t>(n_tot) > d_keys_work.n) {
-      const size_t cap = static_cast<size_t>(n_tot) * 2;
-      d_keys_work.grow(cap, static_cast<size_t>(n_left), st);
-      d_keys_sorted.alloc(cap);
-      ensure_cub(static_cast<int64_t>(cap));
-    }
-    const int64_t log_need = log_count + max_ep;
-    if (static_cast<size_t>(log_need) > d_log_t.n) {
-      const size_t cap = static_cast<size_t>(log_need) * 2;
-      d_log_t.grow(cap, static_cast<size_t>(log_count), st);
-      d_log_gid.grow(cap, static_cast<size_t>(log_count), st);
-    }
-    // ---- B: write keys, sort, offsets
-    key_base = s0;
-    h_ctr[C_WCUR] = static_cast<unsigned long long>(n_left);
-    CK(cudaMemcpyAsync(d_ctr.p + C_WCUR, &h_ctr[C_WCUR], sizeof(unsigned long long),
-                       cudaMemcpyHostToDevice, st));
-    McgEvDev E = ev_dev();
-    if (n_fire > 0) {
-      const int64_t thr = n_fire * 32;
-      k_write_source_events<<<static_cast<unsigned>((thr + 127) / 128), 128, 0, st>>>(E, src_dev(),
-                                                                                  n_fire);
-      launched();
-    }
-    if (n_ep > 0 && h_ctr[C_SPK_EV] > 0) {
-      const int64_t thr = n_ep * 32;
-      k_write_spike_events<<<static_cast<unsigned>((thr + 127) / 128), 128, 0, st>>>(
-          E, d_ep_gid.p, d_ep_step.p, d_ctr.p + C_EP_SPK);
-      launched();
-    }
-    const int end_bit = rank_bits + step_bits + dst_bits;
-    if (n_tot > 0) {
-      size_t tb = d_cub_tmp.n;
-      CK(cub::DeviceRadixSort::SortKeys(d_cub_tmp.p, tb, d_keys_work.p, d_keys_sorted.p,
-                                        static_cast<int>(n_tot), 0, end_bit, st));
-      launched(4);
-    }
-    k_offsets<<<(nl + 1 + 255) / 256, 256, 0, st>>>(d_keys_sorted.p, n_tot, nl,
-                                                     rank_bits + step_bits, d_ev_begin.p,
-                                                     d_ev_cursor.p);
-    launched();
-    // ---- C: the epoch
-    refresh_dev();
-    dev.key_base = key_base;
-    if (nl > 0) {
-      if (timing) CK(cudaEventRecord(ev0, st));
-      k_epoch<<<(nl * 32 + kBlock - 1) / kBlock, kBlock, smem_bytes, st>>>(dev, s0, s1);
-      if (timing) {
-        CK(cudaEventRecord(ev1, st));
-        ev_pending = true;
+  // copy the batch spike log to the host mirror and reset it
+  void drain_log() {
+    const int64_t n = static_cast<int64_t>(h_ctr[C_LOG]);
+    if (n <= 0) return;
+    const size_t o = spk_t.size();
+    spk_t.resize(o + n);
+    spk_gid.resize(o + n);
+    CK(cudaMemcpyAsync(spk_t.data() + o, d_log_t.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(spk_gid.data() + o, d_log_gid.p, n * sizeof(uint32_t),
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaMemsetAsync(d_ctr.p + C_LOG, 0, sizeof(unsigned long long), st));
+    CK(cudaStreamSynchronize(st));
+    h_ctr[C_LOG] = 0;
+  }
+
+  // one graph launch: up to kBatch epochs from `step` towards `target`
+  void run_batch(int64_t target, int64_t call_first) {
+    h_ctl[0] = step;
+    h_ctl[1] = target;
+    h_ctl[2] = L;
+    h_ctl[3] = call_first;
+    CK(cudaMemcpyAsync(d_ctl.p, h_ctl, 4 * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    if (!gexec || graph_timed != timing || graph_trace != d_trace.p) capture_graph();
+    CK(cudaGraphLaunch(gexec, st));
+    sync_counters_raw();
+    const int64_t planned = std::min<int64_t>(kBatch, (target - step + L - 1) / L);
+    const int32_t ab = *h_abort;
+    const int64_t done = ab ? ab - 1 : planned;
+    if (timing && done > 0) {
+      for (int64_t j = 0; j < done; ++j) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, ev_epoch[2 * j], ev_epoch[2 * j + 1]));
+        stats.epoch_kernel_ms += ms;
       }
-      launched();
-      stats.epoch_kernel_launches += 1;
-      // ---- D: ordered spike compaction, leftover carry
-      size_t tb = d_cub_tmp.n;
-      CK(cub::DeviceScan::ExclusiveSum(d_cub_tmp.p, tb, d_sp_count.p, d_sp_scan.p, nl, st));
-      k_spike_write<<<(nl + 127) / 128, 128, 0, st>>>(dev, d_sp_scan.p, d_ep_gid.p, d_ep_step.p,
-                                                      d_log_t.p, d_log_gid.p,
-                                                      d_ctr.p + C_EP_SPK, d_ctr.p + C_LOG);
-      k_spike_total<<<1, 1, 0, st>>>(d_sp_count.p, d_sp_scan.p, nl, d_ctr.p + C_EP_SPK,
-                                     d_ctr.p + C_LOG);
-      k_left_count<<<(nl + 255) / 256, 256, 0, st>>>(d_ev_begin.p, d_ev_cursor.p, nl, d_left.p);
-      tb = d_cub_tmp.n;
-      CK(cub::DeviceScan::ExclusiveSum(d_cub_tmp.p, tb, d_left.p, d_left_scan.p, nl, st));
-      k_leftover<<<(nl * 32 + 127) / 128, 128, 0, st>>>(
-          d_keys_sorted.p, d_ev_begin.p, d_ev_cursor.p, d_left_scan.p, nl, d_keys_work.p,
-          static_cast<uint64_t>(len) << rank_bits);
-      k_left_total<<<1, 1, 0, st>>>(d_left.p, d_left_scan.p, nl, d_ctr.p + C_LEFT);
-      launched(7);
     }
-    stats.epochs += 1;
-    stats.steps += len;
+    stats.epochs += done;
+    stats.epoch_kernel_launches += done;
+    stats.kernel_launches += done * kKernelsPerEpoch;
+    stats.steps += std::min<int64_t>(step + done * L, target) - step;
+    drain_log();
+    step = std::min<int64_t>(step + done * L, target);
+    check_err();
+    if (ab) {
+      // an inbox overflowed while expanding epoch `done`: grow and resume there
+      *h_abort = 0;
+      d_abort.zero(st);
+      grow_inboxes();
+      refresh_dev();
+    }
   }
 
-  // probe sample counts for steps [a, b)
+  // probe sample slots for steps [a, b) (or n_forced forced samples)
   void probes_begin(int64_t a, int64_t b, bool forced, int64_t n_forced) {
     std::vector<int64_t> base(m.probes.size(), 0);
     int64_t tot = 0;
@@ -647,8 +661,9 @@ struct Engine {
       base[p] = tot;
       if (P.local < 0) continue;
       int64_t cnt;
-      if (forced) cnt = n_forced;
-      else {
+      if (forced) {
+        cnt = n_forced;
+      } else {
         const int64_t m0 = (a + P.every) / P.every, m1 = b / P.every;
         cnt = m1 >= m0 ? m1 - m0 + 1 : 0;
       }
@@ -658,13 +673,11 @@ struct Engine {
     if (!m.probes.empty())
       CK(cudaMemcpyAsync(d_trace_base.p, base.data(), base.size() * sizeof(int64_t),
                          cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
     probe_base_host = base;
     probe_total = tot;
     dev.trace_buf = d_trace.p;
-    dev.call_first = a;
   }
-  std::vector<int64_t> probe_base_host;
-  int64_t probe_total = 0;
 
   void probes_end(int64_t a, int64_t b, bool forced, int64_t n_forced, int64_t per) {
     if (probe_total == 0) return;
@@ -694,25 +707,17 @@ struct Engine {
   void advance_to(double t_ms) {
     const int64_t target = ceil_steps(t_ms, m.dt);
     if (step >= target) return;
-    probes_begin(step, target, false, 0);
-    refresh_dev();
     const int64_t a = step;
+    probes_begin(a, target, false, 0);
+    refresh_dev();
     CK(cudaEventRecord(eva, st));
-    while (step < target) {
-      const int64_t epoch = m.min_delay_steps > 0 ? m.min_delay_steps : free_epoch;
-      const int64_t s1 = std::min(target, step + epoch);
-      dev.call_first = a;
-      run_epoch(step, s1);
-      step = s1;
-    }
+    while (step < target) run_batch(target, a);
     CK(cudaEventRecord(evb, st));
-    sync_counters();
-    {
-      float ms = 0;
-      CK(cudaEventElapsedTime(&ms, eva, evb));
-      stats.advance_ms += ms;
-      stats.advance_calls += 1;
-    }
+    CK(cudaEventSynchronize(evb));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, eva, evb));
+    stats.advance_ms += ms;
+    stats.advance_calls += 1;
     probes_end(a, target, false, 0, 1);
   }
 
@@ -724,32 +729,23 @@ struct Engine {
     const int64_t target = ceil_steps(t_ms, dt);
     if ((target - step) % per != 0)
       throw Error(MCG_ERR_ENGINE, "fast-forward: span must be a multiple of coarse dt");
-    // pending: undelivered keys, unexpanded spikes with fan-out, queued calcium
-    CK(cudaMemsetAsync(d_ctr.p + C_SPK_EV, 0, sizeof(unsigned long long), st));
     const int nl = n_local();
-    const int64_t max_ep = static_cast<int64_t>(nl) * sp_cap;
-    if (max_ep > 0) {
-      k_spike_outdeg<<<static_cast<unsigned>((max_ep + 255) / 256), 256, 0, st>>>(
-          d_ep_gid.p, d_ctr.p + C_EP_SPK, d_out_begin.p, d_out_end.p, d_ctr.p + C_SPK_EV);
-      launched();
-    }
-    CK(cudaMemsetAsync(d_err.p, 0, sizeof(int32_t), st));
     const int nf = static_cast<int>(m.fifos.size());
-    if (nf > 0) {
-      k_ff_pending<<<(nf + 255) / 256, 256, 0, st>>>(dev, nf, d_err.p);
-      launched();
-    }
-    sync_counters_raw();
-    const bool fifo_pending = *h_err != 0;
-    *h_err = 0;
-    CK(cudaMemsetAsync(d_err.p, 0, sizeof(int32_t), st));
-    if (h_ctr[C_LEFT] > 0 || h_ctr[C_SPK_EV] > 0 || fifo_pending)
-      throw Error(MCG_ERR_ENGINE, "fast-forward: pending undelivered spikes");
-    const int64_t ncg = static_cast<int64_t>(m.cgs.size());
     refresh_dev();
+    DBuf<int32_t> flag;
+    flag.alloc(1);
+    flag.zero(st);
+    const int64_t span = std::max<int64_t>({int64_t(nl), int64_t(nf), int64_t(nl) * sp_cap, 1});
+    k_pending<<<static_cast<unsigned>((span + 255) / 256), 256, 0, st>>>(
+        dev, d_ep_gid.p, d_ctr.p + C_EP_SPK, d_out_begin.p, d_out_end.p, nf, flag.p);
+    int32_t pending = 0;
+    CK(cudaMemcpyAsync(&pending, flag.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (pending) throw Error(MCG_ERR_ENGINE, "fast-forward: pending undelivered spikes");
+    const int64_t ncg = static_cast<int64_t>(m.cgs.size());
     if (ncg > 0) {
       k_ff_reset<<<static_cast<unsigned>((ncg + 127) / 128), 128, 0, st>>>(dev, ncg);
-      launched();
+      stats.kernel_launches += 1;
     }
     const int64_t n_coarse = (target - step) / per;
     if (n_coarse <= 0) return;
@@ -785,44 +781,20 @@ struct Engine {
       dff.kinds = d_kinds_ff.p;
       k_ff<<<(nl * 32 + kBlock - 1) / kBlock, kBlock, smem_bytes, st>>>(
           dff, d_fh.p, d_cap_ff.p, d_f_ff.p, d_d_ff.p, dtc, n_coarse);
-      launched();
+      stats.kernel_launches += 1;
     }
     const int64_t a = step;
     step = target;
-    sync_counters();
+    sync_counters_raw();
+    check_err();
     probes_end(a, target, true, n_coarse, per);
   }
 
-  void sync_counters_raw() {
-    CK(cudaMemcpyAsync(h_ctr, d_ctr.p, C_N * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(h_err, d_err.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-  }
-
-  void sync_spikes() {
-    sync_counters_raw();
-    log_count = static_cast<int64_t>(h_ctr[C_LOG]);
-    if (host_synced >= log_count) return;
-    const int64_t n = log_count - host_synced;
-    const size_t o = spk_t.size();
-    spk_t.resize(o + n);
-    spk_gid.resize(o + n);
-    CK(cudaMemcpyAsync(spk_t.data() + o, d_log_t.p + host_synced, n * sizeof(double),
-                       cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(spk_gid.data() + o, d_log_gid.p + host_synced, n * sizeof(uint32_t),
-                       cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    host_synced = log_count;
-  }
+  void sync_spikes() {}  // the host mirror is filled after every batch
 
   void clear_spikes() {
-    sync_spikes();
     spk_t.clear();
     spk_gid.clear();
-    CK(cudaMemsetAsync(d_ctr.p + C_LOG, 0, sizeof(unsigned long long), st));
-    CK(cudaStreamSynchronize(st));
-    log_count = 0;
-    host_synced = 0;
   }
 
   int local_of(uint32_t gid) const {

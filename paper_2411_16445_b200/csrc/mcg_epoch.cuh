@@ -9,7 +9,31 @@
 // systems; HH gating is parallel over compartments; synapse mechanisms are
 // parallel over instances with the reference's folds kept in order.
 #pragma once
-#include "mcg_kernels.cuh"
+#include "mcg_events.cuh"
+#include "mcg_mech.cuh"
+
+// ascending bitonic sort of a[0..n) by one warp, padding to the next power
+// of two (<= capacity, itself a power of two) with ~0
+__device__ __forceinline__ void mcg_warp_sort(uint64_t* a, int n, int lane) {
+  int m = 1;
+  while (m < n) m <<= 1;
+  for (int i = n + lane; i < m; i += 32) a[i] = ~0ull;
+  __syncwarp();
+  for (int k = 2; k <= m; k <<= 1)
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      for (int i = lane; i < m; i += 32) {
+        const int ixj = i ^ jj;
+        if (ixj > i) {
+          const uint64_t x = a[i], y = a[ixj];
+          if (((i & k) == 0) ? (x > y) : (x < y)) {
+            a[i] = y;
+            a[ixj] = x;
+          }
+        }
+      }
+      __syncwarp();
+    }
+}
 
 struct McgCellMem {
   double *V, *SP, *HM, *HH, *HN;          // mutable compartment state
@@ -178,12 +202,14 @@ __device__ __forceinline__ bool mcg_species_rest(const McgDev& D, const McgKind&
   return ok;
 }
 
-__global__ void __launch_bounds__(128) k_epoch(McgDev D, int64_t s0, int64_t s1) {
+__global__ void __launch_bounds__(128) k_epoch(McgDev D, int32_t j) {
   extern __shared__ double mcg_smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (c >= D.n_cells) return;
+  if (c >= D.n_cells || *D.abort) return;
+  int64_t s0, s1;
+  if (!mcg_epoch_bounds(D.ctl, j, s0, s1)) return;
   const McgKind& K = D.kinds[D.cell_kind[c]];
   const int n = K.n;
   const int64_t cg0 = D.cg_off[c];
@@ -194,14 +220,37 @@ __global__ void __launch_bounds__(128) k_epoch(McgDev D, int64_t s0, int64_t s1)
   double* V = M.V;
   const int32_t* par = D.k_parent + K.arr;
   const uint64_t rank_mask = (1ull << D.rank_bits) - 1;
-  const uint64_t step_mask = (1ull << D.step_bits) - 1;
   const double* prp_base = (K.prp_idx >= 0) ? M.SP + int64_t(K.prp_idx) * n : nullptr;
   double* sps_base = (K.sps_idx >= 0) ? M.SP + int64_t(K.sps_idx) * n : nullptr;
   const double* vol_k = D.k_volume + K.arr;
   const bool stc_seq = sps_base != nullptr && (const double*)sps_base == prp_base;
   const bool noise = is_lif && K.has_bg && K.sig_bg != 0.0;
-  int64_t cur = D.ev_cursor[c];
-  const int64_t end = D.ev_begin[c + 1];
+
+  // ---- inbox: sort this epoch's incoming keys and merge them into the
+  // pending list (the reference's per-epoch inbox sort, engine.cpp:917-925)
+  int sel = D.pend_sel[c];
+  const uint64_t* pend = D.pend + (int64_t(c) * 2 + sel) * D.pend_cap;
+  int cur = D.pend_off[c], end = D.pend_n[c];
+  {
+    const int nin = D.inc_n[c];
+    if (nin > 0) {
+      uint64_t* in = D.inc + int64_t(c) * D.inc_cap;
+      if (nin > 1) mcg_warp_sort(in, nin, lane);
+      __syncwarp();
+      uint64_t* out = D.pend + (int64_t(c) * 2 + (1 - sel)) * D.pend_cap;
+      if (lane == 0) {
+        int a = cur, b = 0, o = 0;
+        while (a < end && b < nin) out[o++] = (pend[a] <= in[b]) ? pend[a++] : in[b++];
+        while (a < end) out[o++] = pend[a++];
+        while (b < nin) out[o++] = in[b++];
+      }
+      end = (end - cur) + nin;
+      cur = 0;
+      sel = 1 - sel;
+      pend = out;
+      __syncwarp();
+    }
+  }
   int64_t refr = D.refr_until[c];
   double det_prev = D.det_prev[c];
   int armed = D.armed[c];
@@ -226,8 +275,8 @@ __global__ void __launch_bounds__(128) k_epoch(McgDev D, int64_t s0, int64_t s1)
     // ---- 1. deliver due events: inbox, then internal (engine.cpp:549-560)
     if (lane == 0) {
       while (cur < end) {
-        const uint64_t key = D.keys[cur];
-        const int64_t st = D.key_base + int64_t((key >> D.rank_bits) & step_mask);
+        const uint64_t key = pend[cur];
+        const int64_t st = int64_t(key >> D.rank_bits);
         if (st > s) break;
         const int64_t r = int64_t(key & rank_mask);
         mcg_apply_event(D, K, c, cg0, V, D.e_group[r], D.e_inst[r], D.e_weight[r], 0, refractory,
@@ -456,7 +505,7 @@ __global__ void __launch_bounds__(128) k_epoch(McgDev D, int64_t s0, int64_t s1)
         const int p = D.probe_idx[q];
         const McgProbe& P = D.probes[p];
         if ((s + 1) % P.every != 0) continue;
-        const int64_t m0 = (D.call_first + P.every) / P.every;
+        const int64_t m0 = (D.ctl[3] + P.every) / P.every;  // ctl[3]: first step of the call
         D.trace_buf[D.trace_base[p] + ((s + 1) / P.every - m0)] =
             mcg_probe_value(D, K, c, P, V, M.SP);
       }
@@ -465,7 +514,10 @@ __global__ void __launch_bounds__(128) k_epoch(McgDev D, int64_t s0, int64_t s1)
   }
   mcg_stage(D, K, c, M, false, lane);
   if (lane == 0) {
-    D.ev_cursor[c] = cur;
+    D.pend_sel[c] = sel;
+    D.pend_off[c] = cur;
+    D.pend_n[c] = end;
+    D.inc_n[c] = 0;
     D.sp_count[c] = nsp < D.sp_cap ? nsp : D.sp_cap;
     D.refr_until[c] = refr;
     D.det_prev[c] = det_prev;
