@@ -19,7 +19,7 @@ LIB = os.path.join(HERE, "libmcg.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = ["mcg_engine.cu", "mcg_build.cpp"]
-HEADERS = ["mcg_build.h", "mcg_device.cuh", "mcg_events.cuh", "mcg_mech.cuh", "mcg_epoch.cuh",
+HEADERS = ["mcg_build.h", "mcg_device.cuh", "mcg_events.cuh", "mcg_mech.cuh", "mcg_epoch.cuh", "mcg_batch.cuh",
            "mcg_libm.h",
            "mcg_model.h",
            "mcg_rng.h", "glibc_tables.h"]

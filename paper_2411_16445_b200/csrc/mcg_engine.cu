@@ -17,13 +17,15 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
 #include <vector>
 
+#include "mcg_batch.cuh"
 #include "mcg_build.h"
-#include "mcg_epoch.cuh"
 
 namespace mcg {
 
@@ -80,10 +82,13 @@ __global__ void k_pending(McgDev D, const uint32_t* ep_gid, const unsigned long 
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < D.n_cells && (D.pend_n[i] > D.pend_off[i] || D.inc_n[i] > 0)) atomicOr(flag, 1);
   if (i < n_fifos && D.fifos[i].head < D.fifos[i].tail) atomicOr(flag, 1);
-  if (i < static_cast<int64_t>(*ep_n)) {
-    const uint32_t g = ep_gid[i];
+  // spikes of the last epoch are expanded at the next epoch's entry
+  if (i < D.n_cells && D.sp_count[i] > 0) {
+    const uint32_t g = D.gid0 + uint32_t(i);
     if (out_end[g] > out_begin[g]) atomicOr(flag, 1);
   }
+  (void)ep_gid;
+  (void)ep_n;
 }
 
 }  // namespace
@@ -166,11 +171,33 @@ struct Engine {
   // host spike mirror
   std::vector<double> spk_t;
   std::vector<uint32_t> spk_gid;
-  // graph of one batch
+  // graph of one batch (warp-per-cell path)
   cudaGraphExec_t gexec = nullptr;
   bool graph_timed = false;
   double* graph_trace = nullptr;
   std::vector<cudaEvent_t> ev_epoch;
+  // persistent batch kernel (cell batches per CTA)
+  static constexpr int kBatchThreads = 512;
+  int32_t bc_cells = 1, bc_batches = 1, bc_grid = 1, bc_stc_max = 1, bc_nstc_max = 1;
+  int32_t bc_kind_doubles = 0;
+  size_t bc_smem = 0;
+  DBuf<int4> d_chunks;
+  DBuf<unsigned long long> d_chunk_n;
+  DBuf<unsigned long long> d_stamp;
+  cudaEvent_t evk0 = nullptr, evk1 = nullptr;
+  // MCG_PHASE_TIMING=1: per-phase cycle totals of the batch kernel, printed
+  // to stderr after every advance_to (development instrumentation)
+  bool phase_timing = std::getenv("MCG_PHASE_TIMING") != nullptr;
+  DBuf<unsigned long long> d_phase;
+
+  void print_phases() {
+    if (!phase_timing || !d_phase.p) return;
+    unsigned long long ph[12];
+    CK(cudaMemcpy(ph, d_phase.p, sizeof(ph), cudaMemcpyDeviceToHost));
+    std::fprintf(stderr, "phase cycles (sum over CTA batches):");
+    for (int i = 0; i < 12; ++i) std::fprintf(stderr, " %d:%.3g", i, double(ph[i]));
+    std::fprintf(stderr, "  steps=%lld batches=%d\n", (long long)stats.steps, bc_batches);
+  }
   // stats
   mcg_stats stats{};
   bool timing = false;
@@ -187,7 +214,64 @@ struct Engine {
     if (h_ctl) cudaFreeHost(h_ctl);
     if (eva) cudaEventDestroy(eva);
     if (evb) cudaEventDestroy(evb);
+    if (evk0) cudaEventDestroy(evk0);
+    if (evk1) cudaEventDestroy(evk1);
     if (st) cudaStreamDestroy(st);
+  }
+
+  // geometry of the persistent batch kernel: ~n_cells/148 cells per CTA,
+  // capped by shared memory; grid = co-resident CTAs
+  void setup_batch_kernel() {
+    const int nl = n_local();
+    int dev_sms = 148;
+    CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device));
+    bc_stc_max = 1;
+    bc_nstc_max = 1;
+    for (int c = 0; c < nl; ++c) {
+      const McgKind& K = m.kinds[m.cell_kind[c]];
+      int tot = 0, ng = 0;
+      for (int gi = 0; gi < K.n_groups; ++gi) {
+        const McgCellGroup& G = m.cgs[m.cg_off[c] + gi];
+        if (m.specs[G.spec].kind != MCG_SYN_STC_CHARGE) continue;
+        tot += G.size;
+        ++ng;
+      }
+      bc_stc_max = std::max(bc_stc_max, tot);
+      bc_nstc_max = std::max(bc_nstc_max, ng);
+    }
+    // compartment block, noise draws, fold deltas, scalars, STC segments,
+    // changed-flag bitmask (see the carve-up in k_batch)
+    const size_t per_cell = size_t(smem_stride) * 8 + 32 * 8 + size_t(bc_stc_max) * 8 +
+                            sizeof(McgCellSm) + size_t(bc_nstc_max) * sizeof(McgSegSm) +
+                            (size_t(bc_stc_max) / 32 + 2) * 4;
+    // staged kind constants (mcg_batch.cuh McgKindSm): one block per distinct
+    // kind of a batch, (8 + 5 S) n doubles + the parent array
+    size_t kb_max = 0;
+    for (const McgKind& K : m.kinds)
+      if (K.n <= smem_n)
+        kb_max = std::max<size_t>(kb_max, size_t(8 + 5 * K.n_species) * K.n + (K.n + 1) / 2);
+    const size_t budget = 200 * 1024;
+    const int c_max = static_cast<int>(std::max<size_t>(1, budget / (per_cell + kb_max * 8)));
+    bc_cells = std::clamp((nl + dev_sms - 1) / std::max(dev_sms, 1), 1, c_max);
+    bc_batches = std::max(1, (nl + bc_cells - 1) / bc_cells);
+    bc_kind_doubles = static_cast<int32_t>(
+        std::min<size_t>(bc_cells, m.kinds.size()) * kb_max);
+    bc_smem = size_t(bc_cells) * per_cell + size_t(bc_kind_doubles) * 8 + 64;
+    CK(cudaFuncSetAttribute(k_batch, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(bc_smem)));
+    // leave the rest of the unified L1/shared array to L1 (STC state streams through it)
+    const int carve = std::min(100, static_cast<int>((bc_smem * 100 + 228 * 1024 - 1) / (228 * 1024)) + 5);
+    CK(cudaFuncSetAttribute(k_batch, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_batch, kBatchThreads, bc_smem));
+    if (occ < 1) throw Error(MCG_ERR_CUDA, "batch kernel does not fit on an SM");
+    bc_grid = std::min(bc_batches, occ * dev_sms);
+    d_chunks.alloc(size_t(kBatch) * bc_batches + 1);
+    d_chunk_n.alloc(1);
+    d_chunk_n.zero(st);
+    d_stamp.alloc(2 * kBatch + 2);
+    if (!evk0) CK(cudaEventCreate(&evk0));
+    if (!evk1) CK(cudaEventCreate(&evk1));
   }
 
   int32_t n_local() const { return static_cast<int32_t>(m.cell_kind.size()); }
@@ -386,6 +470,7 @@ struct Engine {
     stats.stc_synapses = m.stc_syn;
     stats.hh_comps = m.hh_comps;
     stats.species_comps = m.species_comps;
+    setup_batch_kernel();
     refresh_dev();
   }
 
@@ -616,31 +701,89 @@ struct Engine {
     h_ctr[C_LOG] = 0;
   }
 
-  // one graph launch: up to kBatch epochs from `step` towards `target`
+  // spike log of one launch: chunks (epoch, batch, offset, count) -> the
+  // reference's order (epoch, then gid, then step; engine.cpp:877-888)
+  void drain_chunks() {
+    unsigned long long nch = 0;
+    CK(cudaMemcpyAsync(&nch, d_chunk_n.p, sizeof(nch), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const int64_t n = static_cast<int64_t>(h_ctr[C_LOG]);
+    if (nch == 0 || n == 0) {
+      CK(cudaMemsetAsync(d_chunk_n.p, 0, sizeof(unsigned long long), st));
+      CK(cudaMemsetAsync(d_ctr.p + C_LOG, 0, sizeof(unsigned long long), st));
+      h_ctr[C_LOG] = 0;
+      return;
+    }
+    std::vector<int4> ch(nch);
+    std::vector<double> lt(n);
+    std::vector<uint32_t> lg(n);
+    CK(cudaMemcpyAsync(ch.data(), d_chunks.p, nch * sizeof(int4), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(lt.data(), d_log_t.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(lg.data(), d_log_gid.p, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemsetAsync(d_chunk_n.p, 0, sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(d_ctr.p + C_LOG, 0, sizeof(unsigned long long), st));
+    CK(cudaStreamSynchronize(st));
+    h_ctr[C_LOG] = 0;
+    std::sort(ch.begin(), ch.end(), [](const int4& a, const int4& b) {
+      return a.x != b.x ? a.x < b.x : a.y < b.y;
+    });
+    for (const int4& q : ch)
+      for (int i = 0; i < q.w; ++i) {
+        spk_t.push_back(lt[q.z + i]);
+        spk_gid.push_back(lg[q.z + i]);
+      }
+  }
+
+  // one persistent launch: up to kBatch epochs from `step` towards `target`
   void run_batch(int64_t target, int64_t call_first) {
     h_ctl[0] = step;
     h_ctl[1] = target;
     h_ctl[2] = L;
     h_ctl[3] = call_first;
     CK(cudaMemcpyAsync(d_ctl.p, h_ctl, 4 * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    if (!gexec || graph_timed != timing || graph_trace != d_trace.p) capture_graph();
-    CK(cudaGraphLaunch(gexec, st));
-    sync_counters_raw();
     const int64_t planned = std::min<int64_t>(kBatch, (target - step + L - 1) / L);
+    refresh_dev();
+    McgBatchArgs A{};
+    A.E = ev_dev();
+    A.n_epochs = static_cast<int32_t>(planned);
+    A.cells_per_cta = bc_cells;
+    A.n_batches = bc_batches;
+    A.comp_stride = smem_stride;
+    A.stc_max = bc_stc_max;
+    A.n_stc_max = bc_nstc_max;
+    A.kind_doubles = bc_kind_doubles;
+    if (phase_timing) {
+      if (!d_phase.p) {
+        d_phase.alloc(12);
+        d_phase.zero(st);
+      }
+      A.phase = d_phase.p;
+    }
+    A.log_t = d_log_t.p;
+    A.log_gid = d_log_gid.p;
+    A.log_n = d_ctr.p + C_LOG;
+    A.chunks = d_chunks.p;
+    A.chunk_n = d_chunk_n.p;
+    McgDev Dv = dev;
+    int64_t max_len = L;
+    void* args[] = {&Dv, &A, &max_len};
+    CK(cudaEventRecord(evk0, st));
+    CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_batch), bc_grid, kBatchThreads, args,
+                                   bc_smem, st));
+    CK(cudaEventRecord(evk1, st));
+    sync_counters_raw();
     const int32_t ab = *h_abort;
     const int64_t done = ab ? ab - 1 : planned;
-    if (timing && done > 0) {
-      for (int64_t j = 0; j < done; ++j) {
-        float ms = 0;
-        CK(cudaEventElapsedTime(&ms, ev_epoch[2 * j], ev_epoch[2 * j + 1]));
-        stats.epoch_kernel_ms += ms;
-      }
+    {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, evk0, evk1));
+      stats.epoch_kernel_ms += ms;
     }
     stats.epochs += done;
-    stats.epoch_kernel_launches += done;
-    stats.kernel_launches += done * kKernelsPerEpoch;
+    stats.epoch_kernel_launches += 1;
+    stats.kernel_launches += 1;
     stats.steps += std::min<int64_t>(step + done * L, target) - step;
-    drain_log();
+    drain_chunks();
     step = std::min<int64_t>(step + done * L, target);
     check_err();
     if (ab) {
@@ -718,6 +861,7 @@ struct Engine {
     CK(cudaEventElapsedTime(&ms, eva, evb));
     stats.advance_ms += ms;
     stats.advance_calls += 1;
+    print_phases();
     probes_end(a, target, false, 0, 1);
   }
 
