@@ -5,17 +5,20 @@
 //     phase 1  expansion: source events of the epoch and the previous epoch's
 //              spikes into the per-cell incoming buffers (mcg_events.cuh)
 //     grid.sync
-//     phase 2  every CTA steps its cell batches through the epoch
+//     phase 2  every CTA steps its cell batch through the epoch
 //     grid.sync
 //
-// Phase 2 maps threads to whatever each part of step_cell (engine.cpp:541-783)
-// can use, with the cells' compartment state and all per-cell metadata staged
-// in shared memory (no dependent global loads on the per-step critical path):
+// Each CTA owns a batch of ~n_cells/148 cells.  When every batch has its own
+// CTA ("resident" mode, the normal case) the batch's compartment state, kind
+// constants and per-cell metadata are staged into shared memory once per
+// launch and stay there for all epochs of the launch; otherwise each CTA
+// stages and writes back a batch per epoch.  Phase 2 maps threads to whatever
+// each part of step_cell (engine.cpp:541-783) can use:
 //   owner thread per cell   event delivery, SPS fold, background current,
 //                           spike detection (the reference's ordered folds)
 //   warp per cell           active-list kernel decay, post-spike hook, inbox merge
 //   all threads             STC synapse updates of every cell of the batch,
-//                           HH gating of every compartment of the batch
+//                           HH gating, right-hand sides of the Hines systems
 //   thread per system       the Hines sweeps: V and each species of every
 //                           cell, all in one instruction stream
 // Spikes are logged per CTA batch as chunks (epoch, batch, offset, count); the
@@ -25,16 +28,20 @@
 
 #include "mcg_epoch.cuh"
 
+#define MCG_NPHASE 16
+
 struct McgBatchArgs {
   McgEv E;
   int32_t n_epochs;        // epochs in this launch
   int32_t cells_per_cta;   // C
   int32_t n_batches;       // ceil(n_cells / C)
   int32_t comp_stride;     // doubles of shared memory per cell for compartment state
-  int32_t stc_max;         // max STC instances per cell
+  int32_t stc_max;         // max STC instances per batch (shared-memory table size)
   int32_t n_stc_max;       // max STC groups per cell
   int32_t kind_doubles;    // shared memory for staged kind constants
-  unsigned long long* phase;  // optional per-phase cycle totals (12)
+  int32_t n_specs_sm;      // spec table staged in shared memory (0: read from global)
+  int32_t stc_sm;          // STC instance state kept in shared memory (resident batches)
+  unsigned long long* phase;  // optional per-phase cycle totals (MCG_NPHASE)
   double* log_t;           // spike log of the launch
   uint32_t* log_gid;
   unsigned long long* log_n;
@@ -104,17 +111,18 @@ __device__ void mcg_expand(const McgEv& E, const McgDev& D, int32_t j, int64_t s
   }
 }
 
-// per-cell state kept in shared memory for the duration of an epoch
+// per-cell state kept in shared memory while the batch is staged
 struct McgCellSm {
-  int32_t kind, n, sel, cur, end;
+  int32_t n, sel, cur, end;
   int32_t refractory, has_gsyn, has_current, fired, noise;
   int32_t nsp, armed, stc_off, stc_n, n_stc_seg, hh_off, hh_n, has_act;
   int32_t p0, p1;           // probe range
-  int32_t kb, pad2;         // offset of the cell's staged kind constants (-1: global)
+  int32_t kb;               // offset of the cell's staged kind constants (-1: global)
+  int32_t lif;
+  int32_t pad;
   int64_t refr;
   int64_t fifo_next;        // earliest queued delayed-calcium step (INT64_MAX if none)
-  uint32_t iseq;
-  uint32_t pad;
+  uint64_t nk;              // next pending inbox key (~0 if none)
   unsigned long long ndel;
   double det_prev, prod;
 };
@@ -123,22 +131,24 @@ struct McgCellSm {
 struct McgSegSm {
   int64_t inst;
   int32_t gi, size, spec, comp;
+  int32_t start, pad;       // first instance's index within the cell's STC range
+  double vol, rvol;         // volume of the placement's compartment, mcg_recip of it
 };
 
 // per-kind constants the sweeps read every step, staged in shared memory once
-// per epoch (one copy per distinct kind of the batch).  Layout per kind of n
+// (one copy per distinct kind of the batch).  Layout per kind of n
 // compartments and S species (doubles):
-//   cap_dt, g_leak, g_leak_rhs, axial, vf, vd, g_na, g_k            8 n
-//   per species: sp_cap_dt, sp_gs, sp_coup, sp_f, sp_d               5 n S
-// followed by the parent array (n int32, padded to doubles).
+//   cap_dt, g_leak, g_leak_rhs, axial, vf, vd, vr, g_na, g_k        9 n
+//   per species: sp_cap_dt, sp_gs, sp_coup, sp_f, sp_d, sp_r         6 n S
+// followed by the parent array (n int32, padded to doubles) and a spare word.
 struct McgKindSm {
-  const double *cap, *gl, *glr, *ax, *vf, *vd, *gna, *gk;
-  const double *sp_cap, *sp_gs, *sp_coup, *sp_f, *sp_d;  // [sp * n + i]
+  const double *cap, *gl, *glr, *ax, *vf, *vd, *vr, *gna, *gk;
+  const double *sp_cap, *sp_gs, *sp_coup, *sp_f, *sp_d, *sp_r;  // [sp * n + i]
   const int32_t* par;
 };
 
-__device__ __forceinline__ int mcg_kind_block_doubles(int n, int S) {
-  return (8 + 5 * S) * n + (n + 1) / 2;
+__host__ __device__ __forceinline__ int mcg_kind_block_doubles(int n, int S) {
+  return (9 + 6 * S) * n + (n + 1) / 2 + 1;  // + one spare word (mcg_sweep_const_sm)
 }
 
 __device__ __forceinline__ McgKindSm mcg_kind_view(const double* p, int n, int S) {
@@ -149,29 +159,32 @@ __device__ __forceinline__ McgKindSm mcg_kind_view(const double* p, int n, int S
   v.ax = p + 3 * n;
   v.vf = p + 4 * n;
   v.vd = p + 5 * n;
-  v.gna = p + 6 * n;
-  v.gk = p + 7 * n;
-  v.sp_cap = p + 8 * n;
-  v.sp_gs = p + (8 + S) * n;
-  v.sp_coup = p + (8 + 2 * S) * n;
-  v.sp_f = p + (8 + 3 * S) * n;
-  v.sp_d = p + (8 + 4 * S) * n;
-  v.par = reinterpret_cast<const int32_t*>(p + (8 + 5 * S) * n);
+  v.vr = p + 6 * n;
+  v.gna = p + 7 * n;
+  v.gk = p + 8 * n;
+  v.sp_cap = p + 9 * n;
+  v.sp_gs = p + (9 + S) * n;
+  v.sp_coup = p + (9 + 2 * S) * n;
+  v.sp_f = p + (9 + 3 * S) * n;
+  v.sp_d = p + (9 + 4 * S) * n;
+  v.sp_r = p + (9 + 5 * S) * n;
+  v.par = reinterpret_cast<const int32_t*>(p + (9 + 6 * S) * n);
   return v;
 }
 
 // copy kind K's constants into p (all threads of the CTA)
 __device__ __forceinline__ void mcg_kind_stage(const McgDev& D, const McgKind& K, double* p) {
   const int n = K.n, S = K.n_species, T = blockDim.x;
-  const double* src[8] = {D.k_cap_dt, D.k_g_leak, D.k_g_leak_rhs, D.k_axial,
-                          D.k_vf,     D.k_vd,     D.k_g_na,       D.k_g_k};
-  for (int i = threadIdx.x; i < 8 * n; i += T) p[i] = src[i / n][K.arr + i % n];
-  const double* ssrc[5] = {D.k_sp_cap_dt, D.k_sp_gs, D.k_sp_coupling, D.k_sp_f, D.k_sp_d};
-  for (int i = threadIdx.x; i < 5 * S * n; i += T) {
+  const double* src[9] = {D.k_cap_dt, D.k_g_leak, D.k_g_leak_rhs, D.k_axial, D.k_vf,
+                          D.k_vd,     D.k_vr,     D.k_g_na,       D.k_g_k};
+  for (int i = threadIdx.x; i < 9 * n; i += T) p[i] = src[i / n][K.arr + i % n];
+  const double* ssrc[6] = {D.k_sp_cap_dt, D.k_sp_gs, D.k_sp_coupling,
+                           D.k_sp_f,      D.k_sp_d,  D.k_sp_r};
+  for (int i = threadIdx.x; i < 6 * S * n; i += T) {
     const int a = i / (S * n), r = i % (S * n);
-    p[8 * n + i] = ssrc[a][K.sp_arr + r];
+    p[9 * n + i] = ssrc[a][K.sp_arr + r];
   }
-  int32_t* par = reinterpret_cast<int32_t*>(p + (8 + 5 * S) * n);
+  int32_t* par = reinterpret_cast<int32_t*>(p + (9 + 6 * S) * n);
   for (int i = threadIdx.x; i < n; i += T) par[i] = D.k_parent[K.arr + i];
 }
 
@@ -185,6 +198,7 @@ __device__ __forceinline__ McgKindSm mcg_kind_consts(const McgDev& D, const McgK
   v.ax = D.k_axial + K.arr;
   v.vf = D.k_vf + K.arr;
   v.vd = D.k_vd + K.arr;
+  v.vr = D.k_vr + K.arr;
   v.gna = D.k_g_na + K.arr;
   v.gk = D.k_g_k + K.arr;
   v.sp_cap = D.k_sp_cap_dt + K.sp_arr;
@@ -192,27 +206,209 @@ __device__ __forceinline__ McgKindSm mcg_kind_consts(const McgDev& D, const McgK
   v.sp_coup = D.k_sp_coupling + K.sp_arr;
   v.sp_f = D.k_sp_f + K.sp_arr;
   v.sp_d = D.k_sp_d + K.sp_arr;
+  v.sp_r = D.k_sp_r + K.sp_arr;
   v.par = D.k_parent + K.arr;
   return v;
 }
 
-// one species system from staged constants (engine.cpp:726-750)
+// the dynamic shared memory of k_batch; the shared-memory-resident paths index
+// it with 32-bit offsets so they compile to LDS/STS (a generic pointer that may
+// point to either space costs a 64-bit generic load per access)
+extern __shared__ double mcg_smem[];
+
+// offsets (in doubles; par in int32 units) of one staged kind block
+struct McgKindOff {
+  int cap, gl, glr, ax, vf, vd, vr, gna, gk;
+  int sp_cap, sp_gs, sp_coup, sp_f, sp_d, sp_r;  // + sp * n
+  int par;
+};
+
+__device__ __forceinline__ McgKindOff mcg_kind_off(int o, int n, int S) {
+  McgKindOff v;
+  v.cap = o;
+  v.gl = o + n;
+  v.glr = o + 2 * n;
+  v.ax = o + 3 * n;
+  v.vf = o + 4 * n;
+  v.vd = o + 5 * n;
+  v.vr = o + 6 * n;
+  v.gna = o + 7 * n;
+  v.gk = o + 8 * n;
+  v.sp_cap = o + 9 * n;
+  v.sp_gs = o + (9 + S) * n;
+  v.sp_coup = o + (9 + 2 * S) * n;
+  v.sp_f = o + (9 + 3 * S) * n;
+  v.sp_d = o + (9 + 4 * S) * n;
+  v.sp_r = o + (9 + 5 * S) * n;
+  v.par = 2 * (o + (9 + 6 * S) * n);
+  return v;
+}
+
+// Constant-diagonal Hines solve (tree_solver.cpp:55-73 with the elimination
+// factors f and eliminated diagonal d precomputed, y = mcg_recip(d)); r2 holds
+// cap*x + rhs on entry, x receives the solution.  Operation order is the
+// reference's: r2[par[i]] += f[i]*r2[i] for i = n-1..1, then
+// x[i] = (r2[i] + coup[i]*x[par[i]]) / d[i] for i = 0..n-1.  Along unbranched
+// runs (par[i] == i-1) the running value stays in a register, so each link of
+// the dependency chain is a multiply-add pair (elimination) or a multiply-add
+// plus mcg_div (substitution); everything else is prefetched one node ahead.
+__device__ __forceinline__ void mcg_sweep_const(int n, const int32_t* par, const double* coup,
+                                                const double* f, const double* d,
+                                                const double* y, double* x, double* r2) {
+  if (n == 1) {
+    x[0] = mcg_div(r2[0], d[0], y[0]);
+    return;
+  }
+  // elimination: cur = final r2 of node i; base = r2 of node i-1 before child i
+  double cur = r2[n - 1];
+  double base = r2[n - 2];
+  int p = par[n - 1];
+  double fi = f[n - 1];
+  for (int i = n - 1; i >= 1; --i) {
+    int pn = 0;
+    double fn = 0.0, bn = 0.0;
+    const bool more = i >= 2;
+    if (more) {
+      pn = par[i - 1];
+      fn = f[i - 1];
+    }
+    const double t = fi * cur;
+    if (p == i - 1) {
+      if (more) bn = r2[i - 2];  // no store of this iteration touches node i-2
+      cur = base + t;            // child i is node i-1's last (smallest) child
+      r2[i - 1] = cur;
+    } else {
+      r2[p] = r2[p] + t;         // branch point p < i-1: partial sum in memory
+      if (more) bn = r2[i - 2];  // after the store (p may be i-2)
+      cur = base;                // node i-1 is complete (its children are > i)
+    }
+    p = pn;
+    fi = fn;
+    base = bn;
+  }
+  // back-substitution
+  double vprev = mcg_div(r2[0], d[0], y[0]);
+  x[0] = vprev;
+  int p1 = par[1];
+  double r1 = r2[1], c1 = coup[1], d1 = d[1], y1 = y[1];
+  for (int i = 1; i < n; ++i) {
+    int pn = 0;
+    double rn = 0.0, cn = 0.0, dn = 1.0, yn = 0.0;
+    if (i + 1 < n) {
+      pn = par[i + 1];
+      rn = r2[i + 1];
+      cn = coup[i + 1];
+      dn = d[i + 1];
+      yn = y[i + 1];
+    }
+    const double vp = (p1 == i - 1) ? vprev : x[p1];
+    vprev = mcg_div(r1 + c1 * vp, d1, y1);
+    x[i] = vprev;
+    p1 = pn;
+    r1 = rn;
+    c1 = cn;
+    d1 = dn;
+    y1 = yn;
+  }
+}
+
+// right-hand side of a constant system on shared memory, four compartments'
+// operands loaded ahead of their stores:
+//   r2[i] = cap[i]*x[i] + (v ? (glr[i] + 0.0 + (rc >= 0 ? S[rc+i] : 0.0))
+//                            : (i == pc ? prod : 0.0))
+__device__ __forceinline__ void mcg_rhs_sm(int n, int cap, int x, int r2, bool v, int glr, int rc,
+                                           int pc, double prod) {
+  double* S = mcg_smem;
+  const bool hc = rc >= 0;
+  if (!v) glr = cap;  // any valid offset: the V-only operands are unused
+  if (!hc) rc = cap;
+  int i = 0;
+  for (; i + 4 <= n; i += 4) {
+    double c4[4], x4[4], g4[4], r4[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      c4[u] = S[cap + i + u];
+      x4[u] = S[x + i + u];
+      g4[u] = S[glr + i + u];
+      r4[u] = S[rc + i + u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double rhs = v ? (g4[u] + 0.0 + (hc ? r4[u] : 0.0)) : (i + u == pc ? prod : 0.0);
+      S[r2 + i + u] = c4[u] * x4[u] + rhs;
+    }
+  }
+  for (; i < n; ++i) {
+    const double rhs = v ? (S[glr + i] + 0.0 + (hc ? S[rc + i] : 0.0)) : (i == pc ? prod : 0.0);
+    S[r2 + i] = S[cap + i] * S[x + i] + rhs;
+  }
+}
+
+// mcg_sweep_const on shared memory: every operand an offset into mcg_smem.
+// Operands of the next node are loaded unconditionally; at the ends of the
+// sweeps that reads one element outside an array (r2[-1] or one past the
+// end), which stays inside the carve-up (diag precedes r2; every kind block
+// has one spare word, see mcg_kind_block_doubles) and is never used.
+__device__ __forceinline__ void mcg_sweep_const_sm(int n, int par, int coup, int f, int d, int y,
+                                                   int x, int r2) {
+  double* S = mcg_smem;
+  const int32_t* PI = reinterpret_cast<const int32_t*>(mcg_smem);
+  if (n == 1) {
+    S[x] = mcg_div(S[r2], S[d], S[y]);
+    return;
+  }
+  // elimination: cur = final r2 of node i; base = r2 of node i-1 before child i
+  double cur = S[r2 + n - 1];
+  double base = S[r2 + n - 2];
+  int p = PI[par + n - 1];
+  double fi = S[f + n - 1];
+#pragma unroll 1
+  for (int i = n - 1; i >= 1; --i) {
+    const int pn = PI[par + i - 1];
+    const double fn = S[f + i - 1];
+    const double t = fi * cur;
+    const bool chain = p == i - 1;     // child i is node i-1's last (smallest) child
+    if (!chain) S[r2 + p] += t;        // branch point p < i-1: partial sum in memory
+    const double bn = S[r2 + i - 2];   // after that store (p may be i-2)
+    cur = chain ? base + t : base;     // else node i-1 is complete (children > i)
+    S[r2 + i - 1] = cur;
+    p = pn;
+    fi = fn;
+    base = bn;
+  }
+  // back-substitution
+  double vprev = mcg_div(S[r2], S[d], S[y]);
+  S[x] = vprev;
+  int p1 = PI[par + 1];
+  double r1 = S[r2 + 1], c1 = S[coup + 1], d1 = S[d + 1], y1 = S[y + 1];
+#pragma unroll 1
+  for (int i = 1; i < n; ++i) {
+    const int pn = PI[par + i + 1];
+    const double rn = S[r2 + i + 1], cn = S[coup + i + 1], dn = S[d + i + 1], yn = S[y + i + 1];
+    const double vp = (p1 == i - 1) ? vprev : S[x + p1];
+    vprev = mcg_div(r1 + c1 * vp, d1, y1);
+    S[x + i] = vprev;
+    p1 = pn;
+    r1 = rn;
+    c1 = cn;
+    d1 = dn;
+    y1 = yn;
+  }
+}
+
+// one species system from staged constants (engine.cpp:726-750), for the
+// cases the constant stream does not cover
 __device__ __forceinline__ bool mcg_species_sys(int n, bool is_prp, int prp_comp, double prod,
                                                 const double* cap, const double* gs,
-                                                const double* coup, const double* f,
-                                                const double* d, const int32_t* par, double* conc,
-                                                double* r2, double* diag, double* rhs_scr) {
+                                                const double* coup, const int32_t* par,
+                                                double* conc, double* r2, double* diag,
+                                                double* rhs_scr) {
   if (n == 1) {
     const double r = cap[0] * conc[0] + (is_prp ? prod : 0.0);
     conc[0] = r / (cap[0] + gs[0]);
     return true;
   }
   const int pc = (is_prp && prod != 0.0) ? prp_comp : -1;
-  if (f != nullptr) {
-    for (int i = 0; i < n; ++i) r2[i] = cap[i] * conc[i] + (i == pc ? prod : 0.0);
-    mcg_solve_const(n, par, coup, f, d, conc, r2);
-    return true;
-  }
   for (int i = 0; i < n; ++i) rhs_scr[i] = (i == pc) ? prod : 0.0;
   return mcg_solve_tree(n, par, cap, gs, coup, rhs_scr, conc, diag, r2);
 }
@@ -231,35 +427,120 @@ __device__ __forceinline__ int64_t mcg_fifo_next(const McgDev& D, const McgKind&
   return nx;
 }
 
-// one cell batch [c0, c0 + nc) through epoch [s0, s1)
-__device__ void mcg_cell_batch(const McgDev& D, const McgBatchArgs& A, int32_t b, int32_t j,
-                               int64_t s0, int64_t s1, double* smem, McgCellSm* cs,
-                               double* nbuf, double* dbuf, uint32_t* fmask, McgSegSm* seg,
-                               double* ksm) {
-  const int tid = threadIdx.x;
-  const int T = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5, nwarps = T >> 5;
-  const int c0 = b * A.cells_per_cta;
-  const int nc = min(A.cells_per_cta, D.n_cells - c0);
-  const int S1 = 1 + D.sp_max;  // systems per cell
-  const int m = D.smem_n;
-  // optional per-phase cycle accounting (A.phase != nullptr)
-  unsigned long long ph_last = clock64(), ph[12] = {0};
-#define MCG_PH(i)                                     \
-  do {                                                \
-    if (A.phase && tid == 0) {                        \
-      const unsigned long long t_ = clock64();        \
-      ph[i] += t_ - ph_last;                          \
-      ph_last = t_;                                   \
-    }                                                 \
+// shared-memory carve-up of one CTA (see k_batch)
+struct McgBatchSm {
+  double* comp;     // C x comp_stride: V | SP | HM HH HN | gsyn gsyn_rhs rhs_cur diag | r2
+  double* nbuf;     // C x 32 background-noise draws
+  double* dbuf;     // stc_max SPS fold deltas
+  double* stc;      // stc_sm: 4 x stc_max STC state h | z | c | |h-h0| (SoA)
+  double* ksm;      // staged kind constants
+  McgKind* kc;      // C kind records
+  McgCellSm* cs;    // C cell records
+  McgSegSm* seg;    // C x n_stc_max STC groups
+  McgSpec* spec;    // staged spec table (n_specs_sm entries)
+  uint32_t* floc;   // stc_max: (cell << 16) | group of each STC instance slot
+  uint32_t* fmask;  // stc_max / 32 changed-flag words
+  int ksm_o;        // offset of ksm in mcg_smem (doubles)
+};
+
+// the carve-up, derived from mcg_smem in every function that uses it (so the
+// compiler sees shared-memory pointers, not generic ones)
+__device__ __forceinline__ McgBatchSm mcg_batch_sm(const McgBatchArgs& A) {
+  const int C = A.cells_per_cta;
+  McgBatchSm B;
+  B.comp = mcg_smem;
+  B.nbuf = B.comp + C * A.comp_stride;
+  B.dbuf = B.nbuf + C * 32;
+  B.stc = B.dbuf + A.stc_max;
+  B.ksm_o = C * A.comp_stride + C * 32 + A.stc_max + (A.stc_sm ? 4 * A.stc_max : 0);
+  B.ksm = mcg_smem + B.ksm_o;
+  B.kc = reinterpret_cast<McgKind*>(B.ksm + A.kind_doubles);
+  B.cs = reinterpret_cast<McgCellSm*>(B.kc + C);
+  B.seg = reinterpret_cast<McgSegSm*>(B.cs + C);
+  B.spec = reinterpret_cast<McgSpec*>(B.seg + C * A.n_stc_max);
+  B.floc = reinterpret_cast<uint32_t*>(B.spec + A.n_specs_sm);
+  B.fmask = B.floc + A.stc_max;
+  return B;
+}
+
+// optional per-phase cycle accounting (A.phase != nullptr), thread 0 of each
+// CTA; the accumulators live in static shared memory (no registers held)
+__shared__ unsigned long long mcg_ph_acc[MCG_NPHASE + 1];  // [MCG_NPHASE]: last stamp
+#define MCG_PH(i)                                                  \
+  do {                                                             \
+    if (A.phase && threadIdx.x == 0) {                             \
+      const unsigned long long t_ = clock64();                     \
+      mcg_ph_acc[i] += t_ - mcg_ph_acc[MCG_NPHASE];                \
+      mcg_ph_acc[MCG_NPHASE] = t_;                                 \
+    }                                                              \
   } while (0)
 
-  // ---- epoch entry: per-cell scalars and metadata
+__device__ __forceinline__ double* mcg_comp_block(const McgBatchArgs& A, const McgBatchSm& B,
+                                                  int k) {
+  return B.comp + k * A.comp_stride;
+}
+
+// where the STC state of cell k's group gi lives (shared-memory slot or global)
+__device__ __forceinline__ McgStcSm mcg_stc_ref(const McgBatchArgs& A, const McgBatchSm& B, int k,
+                                                int gi) {
+  McgStcSm R{B.stc, A.stc_max, -1};
+  if (!A.stc_sm) return R;
+  const McgCellSm& X = B.cs[k];
+  for (int q = 0; q < X.n_stc_seg; ++q) {
+    const McgSegSm& g = B.seg[k * A.n_stc_max + q];
+    if (g.gi == gi) R.slot0 = X.stc_off + g.start;
+  }
+  return R;
+}
+
+// post_event (engine.cpp:515-539) of cell k, one warp; STC calcium in the
+// shared-memory copy when the batch keeps it there
+__device__ __forceinline__ void mcg_post_event_b(const McgDev& D, const McgBatchArgs& A,
+                                                 const McgBatchSm& B, const McgKind& K, int k,
+                                                 int64_t cg0, int64_t s, int lane) {
+  if (!A.stc_sm) {
+    mcg_post_event(D, K, cg0, s, lane);
+    return;
+  }
+  for (int gi = 0; gi < K.n_groups; ++gi) {
+    const McgCellGroup G = D.cgs[cg0 + gi];
+    const McgSpec& S = D.specs[G.spec];
+    if (S.kind == MCG_SYN_STC_CHARGE) {
+      const McgStcSm R = mcg_stc_ref(A, B, k, gi);
+      for (int i = lane; i < G.size; i += 32) R.base[2 * R.stride + R.slot0 + i] += S.cpost_s;
+    } else if (S.kind == MCG_SYN_STDP_COND) {
+      for (int i = lane; i < G.size; i += 32) {
+        const int64_t j = G.inst + i;
+        double pre = D.i_stdp_pre[j], post = D.i_stdp_post[j];
+        const double gap = double(s + 1 - D.i_stdp_last[j]) * D.dt;
+        if (gap > 0) mcg_stdp_decay(pre, post, S, gap);
+        D.i_stdp_last[j] = s + 1;
+        post += S.a_post;  // stdp_on_post
+        D.i_stdp_w[j] += pre;
+        D.i_stdp_pre[j] = pre;
+        D.i_stdp_post[j] = post;
+      }
+    } else if (S.kind == MCG_SYN_HOMEO_CURRENT) {
+      for (int i = lane; i < G.size; i += 32) {
+        const int64_t j = G.inst + i;
+        D.i_homeo_w[j] = fmax(D.i_homeo_w[j] + S.dw_minus, 0.0);
+      }
+    }
+  }
+}
+
+// ---- staging: metadata, kind constants, compartment state of batch b
+__device__ void mcg_batch_enter(const McgDev& D, const McgBatchArgs& A, int32_t b) {
+  const McgBatchSm B = mcg_batch_sm(A);
+  const int tid = threadIdx.x, T = blockDim.x;
+  const int c0 = b * A.cells_per_cta;
+  const int nc = min(A.cells_per_cta, D.n_cells - c0);
+  const int m = D.smem_n;
   if (tid < nc) {
     const int c = c0 + tid;
-    McgCellSm& X = cs[tid];
-    const McgKind& K = D.kinds[D.cell_kind[c]];
-    X.kind = D.cell_kind[c];
+    McgCellSm& X = B.cs[tid];
+    B.kc[tid] = D.kinds[D.cell_kind[c]];
+    const McgKind& K = B.kc[tid];
     X.n = K.n;
     X.sel = D.pend_sel[c];
     X.cur = D.pend_off[c];
@@ -271,8 +552,8 @@ __device__ void mcg_cell_batch(const McgDev& D, const McgBatchArgs& A, int32_t b
     X.ndel = 0;
     X.p0 = D.probe_off[c];
     X.p1 = D.probe_off[c + 1];
-    const bool is_lif = K.dyn == MCG_DYN_LIF || K.dyn == MCG_DYN_LIF_EXACT;
-    X.noise = (is_lif && K.has_bg && K.sig_bg != 0.0) ? 1 : 0;
+    X.lif = (K.dyn == MCG_DYN_LIF || K.dyn == MCG_DYN_LIF_EXACT) ? 1 : 0;
+    X.noise = (X.lif && K.has_bg && K.sig_bg != 0.0) ? 1 : 0;
     const int64_t cg0 = D.cg_off[c];
     int ns = 0, tot = 0, act = 0;
     for (int gi = 0; gi < K.n_groups; ++gi) {
@@ -282,12 +563,15 @@ __device__ void mcg_cell_batch(const McgDev& D, const McgBatchArgs& A, int32_t b
           S.kind == MCG_SYN_STATIC_CURRENT || S.kind == MCG_SYN_HOMEO_CURRENT)
         act = 1;
       if (S.kind != MCG_SYN_STC_CHARGE || ns >= A.n_stc_max) continue;
-      McgSegSm& g = seg[tid * A.n_stc_max + ns];
+      McgSegSm& g = B.seg[tid * A.n_stc_max + ns];
       g.inst = G.inst;
       g.gi = gi;
       g.size = G.size;
       g.spec = G.spec;
       g.comp = S.comp;
+      g.start = tot;
+      g.vol = D.k_volume[K.arr + S.comp];
+      g.rvol = D.k_rvol[K.arr + S.comp];
       tot += G.size;
       ++ns;
     }
@@ -296,46 +580,68 @@ __device__ void mcg_cell_batch(const McgDev& D, const McgBatchArgs& A, int32_t b
     X.stc_n = tot;
     X.hh_n = (K.dyn == MCG_DYN_HH) ? K.n : 0;
     X.fifo_next = (K.n_stc_groups > 0) ? mcg_fifo_next(D, K, cg0) : INT64_MAX;
-    X.iseq = D.internal_seq[c];
   }
   __syncthreads();
   if (tid == 0) {
     int acc = 0, hacc = 0, kacc = 0;
     for (int k = 0; k < nc; ++k) {
-      cs[k].stc_off = acc;
-      acc += cs[k].stc_n;
-      cs[k].hh_off = hacc;
-      hacc += cs[k].hh_n;
+      B.cs[k].stc_off = acc;
+      acc += B.cs[k].stc_n;
+      B.cs[k].hh_off = hacc;
+      hacc += B.cs[k].hh_n;
       // one staged copy per distinct kind of the batch
-      cs[k].kb = -1;
-      if (cs[k].n <= m) {
+      B.cs[k].kb = -1;
+      if (B.cs[k].n <= m) {
         for (int q = 0; q < k; ++q)
-          if (cs[q].kind == cs[k].kind && cs[q].kb >= 0) {
-            cs[k].kb = cs[q].kb;
+          if (B.kc[q].arr == B.kc[k].arr && B.cs[q].kb >= 0) {
+            B.cs[k].kb = B.cs[q].kb;
             break;
           }
-        if (cs[k].kb < 0) {
-          const McgKind& K = D.kinds[cs[k].kind];
-          cs[k].kb = kacc;
-          kacc += mcg_kind_block_doubles(K.n, K.n_species);
+        if (B.cs[k].kb < 0) {
+          B.cs[k].kb = kacc;
+          kacc += mcg_kind_block_doubles(B.kc[k].n, B.kc[k].n_species);
         }
       }
     }
   }
   __syncthreads();
   for (int k = 0; k < nc; ++k) {
-    if (cs[k].kb < 0) continue;
+    if (B.cs[k].kb < 0) continue;
     bool first = true;
     for (int q = 0; q < k; ++q)
-      if (cs[q].kb == cs[k].kb) first = false;
-    if (first) mcg_kind_stage(D, D.kinds[cs[k].kind], ksm + cs[k].kb);
+      if (B.cs[q].kb == B.cs[k].kb) first = false;
+    if (first) mcg_kind_stage(D, B.kc[k], B.ksm + B.cs[k].kb);
   }
-  // stage compartment state (cells that fit; the rest use global memory)
+  // STC instance locator: slot f -> (cell, group)
+  for (int k = 0; k < nc; ++k) {
+    const McgCellSm& X = B.cs[k];
+    for (int q = 0; q < X.n_stc_seg; ++q) {
+      const McgSegSm& g = B.seg[k * A.n_stc_max + q];
+      for (int i = tid; i < g.size; i += T)
+        B.floc[X.stc_off + g.start + i] = (uint32_t(k) << 16) | uint32_t(q);
+    }
+  }
+  __syncthreads();
+  if (A.stc_sm) {
+    const int stc_total = B.cs[nc - 1].stc_off + B.cs[nc - 1].stc_n;
+    const int S4 = A.stc_max;
+    for (int f = tid; f < stc_total; f += T) {
+      const uint32_t loc = B.floc[f];
+      const int k = int(loc >> 16);
+      const McgSegSm& g = B.seg[k * A.n_stc_max + int(loc & 0xffffu)];
+      const int64_t j = g.inst + (f - B.cs[k].stc_off - g.start);
+      B.stc[f] = D.i_stc_h[j];
+      B.stc[S4 + f] = D.i_stc_z[j];
+      B.stc[2 * S4 + f] = D.i_stc_c[j];
+      B.stc[3 * S4 + f] = D.i_sps_abs[j];
+    }
+  }
+  // compartment state (cells that fit; the rest use global memory)
   for (int k = 0; k < nc; ++k) {
     const int c = c0 + k;
-    const McgKind& K = D.kinds[D.cell_kind[c]];
+    const McgKind& K = B.kc[k];
     if (K.n > m) continue;
-    double* base = smem + int64_t(k) * A.comp_stride;
+    double* base = mcg_comp_block(A, B, k);
     const int n = K.n;
     const int64_t co = D.comp_off[c];
     for (int i = tid; i < n; i += T) base[i] = D.v[co + i];
@@ -349,44 +655,131 @@ __device__ void mcg_cell_batch(const McgDev& D, const McgBatchArgs& A, int32_t b
       }
   }
   __syncthreads();
+}
+
+// ---- write-back of batch b (state that lives in shared memory while staged)
+__device__ void mcg_batch_exit(const McgDev& D, const McgBatchArgs& A, int32_t b) {
+  const McgBatchSm B = mcg_batch_sm(A);
+  const int tid = threadIdx.x, T = blockDim.x;
+  const int c0 = b * A.cells_per_cta;
+  const int nc = min(A.cells_per_cta, D.n_cells - c0);
+  const int m = D.smem_n;
+  for (int k = 0; k < nc; ++k) {
+    const int c = c0 + k;
+    const McgKind& K = B.kc[k];
+    if (K.n > m) continue;
+    const double* base = mcg_comp_block(A, B, k);
+    const int n = K.n;
+    const int64_t co = D.comp_off[c];
+    for (int i = tid; i < n; i += T) D.v[co + i] = base[i];
+    double* gs = D.species + D.sp_off[c];
+    for (int i = tid; i < K.n_species * n; i += T) gs[i] = base[m + i];
+    if (K.dyn == MCG_DYN_HH)
+      for (int i = tid; i < n; i += T) {
+        D.hh_m[co + i] = base[(1 + D.sp_max) * m + i];
+        D.hh_h[co + i] = base[(2 + D.sp_max) * m + i];
+        D.hh_n[co + i] = base[(3 + D.sp_max) * m + i];
+      }
+  }
+  if (A.stc_sm) {
+    const int stc_total = B.cs[nc - 1].stc_off + B.cs[nc - 1].stc_n;
+    const int S4 = A.stc_max;
+    for (int f = tid; f < stc_total; f += T) {
+      const uint32_t loc = B.floc[f];
+      const int k = int(loc >> 16);
+      const McgSegSm& g = B.seg[k * A.n_stc_max + int(loc & 0xffffu)];
+      const int64_t j = g.inst + (f - B.cs[k].stc_off - g.start);
+      D.i_stc_h[j] = B.stc[f];
+      D.i_stc_z[j] = B.stc[S4 + f];
+      D.i_stc_c[j] = B.stc[2 * S4 + f];
+      D.i_sps_abs[j] = B.stc[3 * S4 + f];
+    }
+  }
+  if (tid < nc) {
+    const int c = c0 + tid;
+    McgCellSm& X = B.cs[tid];
+    if (X.ndel) atomicAdd(D.delivered, X.ndel);
+    X.ndel = 0;
+    D.refr_until[c] = X.refr;
+    D.det_prev[c] = X.det_prev;
+    D.armed[c] = X.armed;
+  }
+  __syncthreads();
+}
+
+// ---- one epoch [s0, s1) of the staged batch b
+__device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t b, int32_t j,
+                                int64_t s0, int64_t s1) {
+  const McgBatchSm B = mcg_batch_sm(A);
+  const int tid = threadIdx.x;
+  const int T = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = T >> 5;
+  const int c0 = b * A.cells_per_cta;
+  const int nc = min(A.cells_per_cta, D.n_cells - c0);
+  const int S1 = 1 + D.sp_max;  // systems per cell
+  const int m = D.smem_n;
+  McgCellSm* cs = B.cs;
+  const McgKind* kc = B.kc;
+  const McgSpec* specs = A.n_specs_sm > 0 ? B.spec : D.specs;
+
   // inbox merge, warp per cell (the reference's per-epoch inbox sort)
   for (int k = warp; k < nc; k += nwarps) {
     const int c = c0 + k;
     const int nin = D.inc_n[c];
-    if (nin == 0) continue;
     McgCellSm& X = cs[k];
-    uint64_t* in = D.inc + int64_t(c) * D.inc_cap;
-    if (nin > 1) mcg_warp_sort(in, nin, lane);
-    __syncwarp();
-    const uint64_t* pold = D.pend + (int64_t(c) * 2 + X.sel) * D.pend_cap;
-    uint64_t* out = D.pend + (int64_t(c) * 2 + (1 - X.sel)) * D.pend_cap;
-    if (lane == 0) {
-      int a = X.cur, bb = 0, o = 0;
-      const int e = X.end;
-      while (a < e && bb < nin) out[o++] = (pold[a] <= in[bb]) ? pold[a++] : in[bb++];
-      while (a < e) out[o++] = pold[a++];
-      while (bb < nin) out[o++] = in[bb++];
-      X.end = o;
-      X.cur = 0;
-      X.sel = 1 - X.sel;
+    if (nin > 0) {
+      uint64_t* in = D.inc + int64_t(c) * D.inc_cap;
+      if (nin > 1) mcg_warp_sort(in, nin, lane);
+      __syncwarp();
+      const uint64_t* pold = D.pend + (int64_t(c) * 2 + X.sel) * D.pend_cap;
+      uint64_t* out = D.pend + (int64_t(c) * 2 + (1 - X.sel)) * D.pend_cap;
+      if (lane == 0) {
+        int a = X.cur, bb = 0, o = 0;
+        const int e = X.end;
+        while (a < e && bb < nin) out[o++] = (pold[a] <= in[bb]) ? pold[a++] : in[bb++];
+        while (a < e) out[o++] = pold[a++];
+        while (bb < nin) out[o++] = in[bb++];
+        X.end = o;
+        X.cur = 0;
+        X.sel = 1 - X.sel;
+      }
+      __syncwarp();
     }
-    __syncwarp();
+    if (lane == 0) {
+      X.nk = (X.cur < X.end) ? D.pend[(int64_t(c) * 2 + X.sel) * D.pend_cap + X.cur] : ~0ull;
+      X.nsp = 0;
+    }
   }
   __syncthreads();
-  MCG_PH(9);
+  MCG_PH(10);
   const int stc_total = cs[nc - 1].stc_off + cs[nc - 1].stc_n;
   const int hh_total = cs[nc - 1].hh_off + cs[nc - 1].hh_n;
+  const int stc_rounds = (stc_total + T - 1) / T;
 
   const uint64_t rank_mask = (1ull << D.rank_bits) - 1;
   for (int64_t s = s0; s < s1; ++s) {
     const int64_t so = s - s0;
-    // background-noise draws for the next 32 steps of every noisy cell
+    // background-noise draws for the next 32 steps of every noisy cell, one
+    // Box-Muller pair per thread (normal_for, rng.cpp:67-78: step n uses pair
+    // n >> 1 of threefry block n >> 2, element n & 1)
     if ((so & 31) == 0) {
-      for (int q = tid; q < nc * 32; q += T) {
-        const int k = q >> 5, l = q & 31;
-        if (!cs[k].noise || s + l >= s1) continue;
+      const int64_t w1 = min(s + 32, s1);
+      for (int q = tid; q < nc * 17; q += T) {
+        const int k = q / 17, pp = q - k * 17;
+        if (!cs[k].noise) continue;
+        const uint64_t pr = (uint64_t(s) >> 1) + uint64_t(pp);
+        const int64_t n0 = int64_t(pr * 2);
+        if (n0 + 1 < s || n0 >= w1) continue;
         const mcg_key key = mcg_make_key(D.seed, D.gid0 + uint32_t(c0 + k), 1, 0);
-        nbuf[q] = mcg_normal_for(&key, static_cast<uint64_t>(s + l));
+        uint64_t x[4];
+        mcg_threefry(&key, pr >> 1, x);
+        const unsigned h = unsigned(pr & 1u);
+        const double u1 = ((double)(x[2 * h] >> 11) + 1.0) * MCG_2POW_M53;
+        const double u2 = (double)(x[2 * h + 1] >> 11) * MCG_2POW_M53;
+        double z0, z1;
+        mcg_normal_pair(u1, u2, &z0, &z1);
+        if (n0 >= s) B.nbuf[k * 32 + int(n0 - s)] = z0;
+        if (n0 + 1 < w1) B.nbuf[k * 32 + int(n0 + 1 - s)] = z1;
       }
       __syncthreads();
       MCG_PH(0);
@@ -395,60 +788,56 @@ __device__ void mcg_cell_batch(const McgDev& D, const McgBatchArgs& A, int32_t b
     if (tid < nc) {
       const int c = c0 + tid;
       McgCellSm& X = cs[tid];
-      const McgKind& K = D.kinds[X.kind];
-      const bool is_lif = K.dyn == MCG_DYN_LIF || K.dyn == MCG_DYN_LIF_EXACT;
-      const bool refractory = is_lif && s < X.refr;
+      const McgKind& K = kc[tid];
+      const bool refractory = X.lif && s < X.refr;
       X.refractory = refractory;
-      double* V = (K.n <= m) ? smem + int64_t(tid) * A.comp_stride : D.v + D.comp_off[c];
+      double* V = (K.n <= m) ? mcg_comp_block(A, B, tid) : D.v + D.comp_off[c];
       const int64_t cg0 = D.cg_off[c];
-      int cur = X.cur;
-      if (cur < X.end) {
+      uint64_t key = X.nk;
+      if (int64_t(key >> D.rank_bits) <= s) {
         const uint64_t* pend = D.pend + (int64_t(c) * 2 + X.sel) * D.pend_cap;
-        while (cur < X.end) {
-          const uint64_t key = pend[cur];
-          if (int64_t(key >> D.rank_bits) > s) break;
+        int cur = X.cur;
+        while (int64_t(key >> D.rank_bits) <= s) {
           const int64_t r = int64_t(key & rank_mask);
-          mcg_apply_event(D, K, c, cg0, V, D.e_group[r], D.e_inst[r], D.e_weight[r], 0,
-                          refractory, s);
+          const int32_t grp = D.e_group[r];
+          mcg_apply_event(D, K, c, cg0, V, grp, D.e_inst[r], D.e_weight[r], 0, refractory, s,
+                          mcg_stc_ref(A, B, tid, grp));
           ++cur;
           ++X.ndel;
+          key = (cur < X.end) ? pend[cur] : ~0ull;
         }
         X.cur = cur;
+        X.nk = key;
+        // STC events queue delayed calcium (apply_event, engine.cpp:497-503)
+        if (K.n_stc_groups > 0) X.fifo_next = mcg_fifo_next(D, K, cg0);
       }
-      if (K.n_stc_groups > 0) {
-        const uint32_t iseq = D.internal_seq[c];
-        if (iseq != X.iseq) {  // calcium was queued this step
-          X.iseq = iseq;
-          X.fifo_next = mcg_fifo_next(D, K, cg0);
-        }
-        if (X.fifo_next <= s) {
-          for (;;) {
-            int best = -1;
-            uint64_t bseq = ~0ull;
-            for (int gi = 0; gi < K.n_groups; ++gi) {
-              const McgCellGroup& G = D.cgs[cg0 + gi];
-              if (G.fifo < 0) continue;
-              const McgFifo& F = D.fifos[G.fifo];
-              if (F.head < F.tail) {
-                const int64_t slot = F.base + (F.head % F.cap);
-                if (D.fifo_step[slot] <= s) {
-                  const uint64_t seq = D.fifo_si[slot] >> 32;
-                  if (seq < bseq) {
-                    bseq = seq;
-                    best = gi;
-                  }
+      if (X.fifo_next <= s) {
+        for (;;) {
+          int best = -1;
+          uint64_t bseq = ~0ull;
+          for (int gi = 0; gi < K.n_groups; ++gi) {
+            const McgCellGroup& G = D.cgs[cg0 + gi];
+            if (G.fifo < 0) continue;
+            const McgFifo& F = D.fifos[G.fifo];
+            if (F.head < F.tail) {
+              const int64_t slot = F.base + (F.head % F.cap);
+              if (D.fifo_step[slot] <= s) {
+                const uint64_t seq = D.fifo_si[slot] >> 32;
+                if (seq < bseq) {
+                  bseq = seq;
+                  best = gi;
                 }
               }
             }
-            if (best < 0) break;
-            McgFifo& F = D.fifos[D.cgs[cg0 + best].fifo];
-            const uint64_t si = D.fifo_si[F.base + (F.head % F.cap)];
-            ++F.head;
-            mcg_apply_event(D, K, c, cg0, V, best, uint32_t(si & 0xffffffffu), 0.0, 1,
-                            refractory, s);
           }
-          X.fifo_next = mcg_fifo_next(D, K, cg0);
+          if (best < 0) break;
+          McgFifo& F = D.fifos[D.cgs[cg0 + best].fifo];
+          const uint64_t si = D.fifo_si[F.base + (F.head % F.cap)];
+          ++F.head;
+          mcg_apply_event(D, K, c, cg0, V, best, uint32_t(si & 0xffffffffu), 0.0, 1,
+                          refractory, s, mcg_stc_ref(A, B, tid, best));
         }
+        X.fifo_next = mcg_fifo_next(D, K, cg0);
       }
       X.has_gsyn = 0;
       X.has_current = 0;
@@ -463,12 +852,12 @@ __device__ void mcg_cell_batch(const McgDev& D, const McgBatchArgs& A, int32_t b
     for (int k = warp; k < nc; k += nwarps) {
       if (!cs[k].has_act) continue;
       const int c = c0 + k;
-      const McgKind& K = D.kinds[cs[k].kind];
-      const McgCellMem M = mcg_cell_mem(D, K, c, K.n <= m ? smem + int64_t(k) * A.comp_stride : nullptr);
+      const McgKind& K = kc[k];
+      const McgCellMem M = mcg_cell_mem(D, K, c, K.n <= m ? mcg_comp_block(A, B, k) : nullptr);
       bool hg = false, hc = false;
       for (int gi = 0; gi < K.n_groups; ++gi) {
         McgCellGroup* G = &D.cgs[D.cg_off[c] + gi];
-        const McgSpec& S = D.specs[G->spec];
+        const McgSpec& S = specs[G->spec];
         if (G->active_n == 0) continue;
         if (S.kind == MCG_SYN_STATIC_COND || S.kind == MCG_SYN_STDP_COND) {
           if (!hg) {
@@ -490,33 +879,86 @@ __device__ void mcg_cell_batch(const McgDev& D, const McgBatchArgs& A, int32_t b
       }
     }
     // ---- C. STC synapses of every cell of the batch, one flat index space
-    // (engine.cpp:617-646); changed flags as warp ballots for the fold
-    for (int f0 = tid - lane; f0 < stc_total; f0 += T) {
-      const int f = f0 + lane;
-      bool changed = false;
-      if (f < stc_total) {
-        int lo = 0, hi = nc - 1;  // last cell with stc_off <= f
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (cs[mid].stc_off <= f) lo = mid;
-          else hi = mid - 1;
+    // (engine.cpp:617-646), four instances per thread in flight; changed
+    // flags as warp ballots for the fold
+    if (A.stc_sm) {  // state in shared memory: one instance per thread and round
+      const int S4 = A.stc_max;
+      for (int f0 = tid - lane; f0 < stc_total; f0 += T) {
+        const int f = f0 + lane;
+        bool changed = false;
+        if (f < stc_total) {
+          const uint32_t loc = B.floc[f];
+          const int k = int(loc >> 16);
+          const McgSegSm& g = B.seg[k * A.n_stc_max + int(loc & 0xffffu)];
+          const McgKind& K = kc[k];
+          const int c = c0 + k;
+          const bool late = K.prp_idx >= 0;
+          double prp = 0.0;
+          if (late) {
+            const double* SPb =
+                (K.n <= m) ? mcg_comp_block(A, B, k) + m : D.species + D.sp_off[c];
+            prp = SPb[K.prp_idx * K.n + g.comp];
+          }
+          McgStcVal v{B.stc[f], B.stc[S4 + f], B.stc[2 * S4 + f], B.stc[3 * S4 + f]};
+          double delta = 0.0;
+          changed = mcg_stc_step(specs[g.spec], D.dt, D.seed, D.gid0 + uint32_t(c), g.gi,
+                                 f - cs[k].stc_off - g.start, s, late, prp, g.vol, g.rvol, v,
+                                 delta);
+          B.dbuf[f] = delta;
+          B.stc[f] = v.h;
+          B.stc[S4 + f] = v.z;
+          B.stc[2 * S4 + f] = v.c;
+          B.stc[3 * S4 + f] = v.a;
         }
-        const int k = lo, c = c0 + k;
-        int li = f - cs[k].stc_off, q = 0;
-        const McgSegSm* sg = seg + k * A.n_stc_max;
-        while (li >= sg[q].size) li -= sg[q++].size;
-        const McgKind& K = D.kinds[cs[k].kind];
-        const double* SPb = (K.n <= m) ? smem + int64_t(k) * A.comp_stride + m
-                                       : D.species + D.sp_off[c];
-        const double* prp_base = (K.prp_idx >= 0) ? SPb + int64_t(K.prp_idx) * K.n : nullptr;
-        const McgStcOut o = mcg_stc_instance(D, D.specs[sg[q].spec], sg[q].inst + li,
-                                             D.gid0 + uint32_t(c), sg[q].gi, li, s, prp_base,
-                                             D.k_volume + K.arr);
-        dbuf[f] = o.delta;
-        changed = o.changed;
+        const unsigned bal = __ballot_sync(MCG_FULL, changed);
+        if (lane == 0) B.fmask[f0 >> 5] = bal;
       }
-      const unsigned bal = __ballot_sync(MCG_FULL, changed);
-      if (lane == 0) fmask[f0 >> 5] = bal;
+    } else
+    for (int r0 = 0; r0 < stc_rounds; r0 += 4) {
+      McgStcVal v[4];
+      int64_t jj[4];
+      uint32_t loc[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int f = (r0 + u) * T + tid;
+        jj[u] = -1;
+        if (r0 + u < stc_rounds && f < stc_total) {
+          loc[u] = B.floc[f];
+          const int k = int(loc[u] >> 16), q = int(loc[u] & 0xffffu);
+          const McgSegSm& g = B.seg[k * A.n_stc_max + q];
+          jj[u] = g.inst + (f - cs[k].stc_off - g.start);
+          v[u].h = D.i_stc_h[jj[u]];
+          v[u].z = D.i_stc_z[jj[u]];
+          v[u].c = D.i_stc_c[jj[u]];
+          v[u].a = D.i_sps_abs[jj[u]];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (r0 + u >= stc_rounds) break;
+        const int f = (r0 + u) * T + tid;
+        bool changed = false;
+        if (jj[u] >= 0) {
+          const int k = int(loc[u] >> 16), q = int(loc[u] & 0xffffu);
+          const McgSegSm& g = B.seg[k * A.n_stc_max + q];
+          const McgKind& K = kc[k];
+          const int c = c0 + k;
+          const double* SPb = (K.n <= m) ? mcg_comp_block(A, B, k) + m : D.species + D.sp_off[c];
+          const bool late = K.prp_idx >= 0;
+          const double prp = late ? SPb[int64_t(K.prp_idx) * K.n + g.comp] : 0.0;
+          double delta = 0.0;
+          const int li = f - cs[k].stc_off - g.start;
+          changed = mcg_stc_step(specs[g.spec], D.dt, D.seed, D.gid0 + uint32_t(c), g.gi, li, s,
+                                 late, prp, g.vol, g.rvol, v[u], delta);
+          B.dbuf[f] = delta;
+          D.i_stc_h[jj[u]] = v[u].h;
+          D.i_stc_z[jj[u]] = v[u].z;
+          D.i_stc_c[jj[u]] = v[u].c;
+          if (changed) D.i_sps_abs[jj[u]] = v[u].a;
+        }
+        const unsigned bal = __ballot_sync(MCG_FULL, changed);
+        if (lane == 0) B.fmask[((r0 + u) * T + (tid - lane)) >> 5] = bal;
+      }
     }
     __syncthreads();
     MCG_PH(2);
@@ -525,27 +967,38 @@ __device__ void mcg_cell_batch(const McgDev& D, const McgBatchArgs& A, int32_t b
     if (tid < nc) {
       const int c = c0 + tid;
       McgCellSm& X = cs[tid];
-      const McgKind& K = D.kinds[X.kind];
+      const McgKind& K = kc[tid];
       const bool in_sm = K.n <= m;
-      double* base = in_sm ? smem + int64_t(tid) * A.comp_stride : nullptr;
+      double* base = in_sm ? mcg_comp_block(A, B, tid) : nullptr;
       double* SP = in_sm ? base + m : D.species + D.sp_off[c];
       if (K.sps_idx >= 0) {
         double* sps = SP + int64_t(K.sps_idx) * K.n;
         int f = X.stc_off;
         for (int q = 0; q < X.n_stc_seg; ++q) {
-          const McgSegSm& g = seg[tid * A.n_stc_max + q];
+          const McgSegSm& g = B.seg[tid * A.n_stc_max + q];
           const int fe = f + g.size;
           // every instance of a placement sits on the placement's compartment
           double acc = sps[g.comp];
           while (f < fe) {
             const int w = f >> 5;
-            uint32_t bits = fmask[w] >> (f & 31);
+            uint32_t bits = B.fmask[w] >> (f & 31);
             const int lim = min(32 - (f & 31), fe - f);
             if (lim < 32) bits &= (1u << lim) - 1u;
+            // the adds stay in instance order; the loads of up to 8 changed
+            // slots are issued ahead of them
             while (bits) {
-              const int l = __ffs(bits) - 1;
-              bits &= bits - 1;
-              acc += dbuf[f + l];
+              double dv[8];
+              int cnt = 0;
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if (bits) {
+                  dv[u] = B.dbuf[f + __ffs(bits) - 1];
+                  bits &= bits - 1;
+                  cnt = u + 1;
+                }
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if (u < cnt) acc += dv[u];
             }
             f += lim;
           }
@@ -555,12 +1008,11 @@ __device__ void mcg_cell_batch(const McgDev& D, const McgBatchArgs& A, int32_t b
       X.prod = 0.0;
       if (K.prp_enabled)
         X.prod = (SP[int64_t(K.sps_idx) * K.n + K.prp_comp] > K.prp_theta_star) ? K.prp_rate : 0.0;
-      const bool is_lif = K.dyn == MCG_DYN_LIF || K.dyn == MCG_DYN_LIF_EXACT;
       const double ts = double(s) * D.dt;
       const bool bg_gated = K.bg_t1 > K.bg_t0 && ts >= K.bg_t0 && ts < K.bg_t1;
-      if (is_lif && K.has_bg && !bg_gated) {
+      if (X.lif && K.has_bg && !bg_gated) {
         double ib = K.i_bg;
-        if (K.sig_bg != 0.0) ib += K.sig_bg * nbuf[tid * 32 + int(so & 31)];
+        if (K.sig_bg != 0.0) ib += K.sig_bg * B.nbuf[tid * 32 + int(so & 31)];
         double* rc = in_sm ? base + (6 + D.sp_max) * m : D.s_rhs_cur + D.comp_off[c];
         rc[K.noise_comp] += ib;
         X.has_current = 1;
@@ -579,10 +1031,10 @@ __device__ void mcg_cell_batch(const McgDev& D, const McgBatchArgs& A, int32_t b
           else hi = mid - 1;
         }
         const int k = lo, c = c0 + k;
-        const McgKind& K = D.kinds[cs[k].kind];
-        const McgCellMem M = mcg_cell_mem(D, K, c, K.n <= m ? smem + int64_t(k) * A.comp_stride : nullptr);
+        const McgKind& K = kc[k];
+        const McgCellMem M = mcg_cell_mem(D, K, c, K.n <= m ? mcg_comp_block(A, B, k) : nullptr);
         const int i = f - cs[k].hh_off;
-        const McgKindSm KS = mcg_kind_consts(D, K, ksm, cs[k].kb);
+        const McgKindSm KS = mcg_kind_consts(D, K, B.ksm, cs[k].kb);
         const bool hg = cs[k].has_gsyn, hc = cs[k].has_current;
         const double v = M.V[i];
         double gsum = KS.gl[i];
@@ -611,15 +1063,17 @@ __device__ void mcg_cell_batch(const McgDev& D, const McgBatchArgs& A, int32_t b
       MCG_PH(4);
     }
 
-    // ---- E2. membrane and species systems: thread per (cell, system)
+
+    // ---- E2b. membrane and species systems: thread per (cell, system)
     for (int t = tid; t < nc * S1; t += T) {
       const int k = t / S1, sys = t - k * S1;
       const int c = c0 + k;
       const McgCellSm& X = cs[k];
-      const McgKind& K = D.kinds[X.kind];
-      const McgCellMem M = mcg_cell_mem(D, K, c, K.n <= m ? smem + int64_t(k) * A.comp_stride : nullptr);
-      const McgKindSm KS = mcg_kind_consts(D, K, ksm, X.kb);
+      const McgKind& K = kc[k];
       const int n = K.n;
+      const bool in_sm = n <= m;
+      const McgCellMem M = mcg_cell_mem(D, K, c, in_sm ? mcg_comp_block(A, B, k) : nullptr);
+      const McgKindSm KS = mcg_kind_consts(D, K, B.ksm, X.kb);
       const bool refractory = X.refractory;
       const bool hg = X.has_gsyn, hc = X.has_current;
       const int q = sys - 1;
@@ -628,25 +1082,40 @@ __device__ void mcg_cell_batch(const McgDev& D, const McgBatchArgs& A, int32_t b
       const bool v_sys = sys == 0 && K.dyn == MCG_DYN_LIF && !refractory && !hg && K.v_const;
       const bool s_sys = sys > 0 && q < K.n_species && n > 1 && K.sp_const;
       bool ok = true;
-      if (v_sys || s_sys) {
+      if ((v_sys || s_sys) && in_sm) {
+        const McgKindOff KO = mcg_kind_off(B.ksm_o + X.kb, n, K.n_species);
+        const int bo = k * A.comp_stride, r2o = bo + (8 + D.sp_max) * m;
+        // one call for V and species (operands selected first), so lanes with
+        // different systems run the sweep in lockstep instead of serialized
+        const int qn = v_sys ? 0 : q * n;
+        const int x = v_sys ? bo : bo + m + qn, r2 = v_sys ? r2o : r2o + n + qn;
+        // right-hand side (engine.cpp:683 / 746-748):
+        //   V:       r2 = cap*v + (g_leak_rhs + 0.0 + (has_current ? rhs_cur : 0.0))
+        //   species: r2 = cap*c + (prod at the synthesis compartment, else 0.0)
+        const int pc = (!v_sys && q == K.prp_idx && X.prod != 0.0) ? K.prp_comp : -1;
+        mcg_rhs_sm(n, v_sys ? KO.cap : KO.sp_cap + qn, x, r2, v_sys, KO.glr,
+                   hc ? bo + (6 + D.sp_max) * m : -1, pc, X.prod);
+        mcg_sweep_const_sm(n, KO.par, (v_sys ? KO.ax : KO.sp_coup) + qn,
+                           (v_sys ? KO.vf : KO.sp_f) + qn, (v_sys ? KO.vd : KO.sp_d) + qn,
+                           (v_sys ? KO.vr : KO.sp_r) + qn, x, r2);
+      } else if (v_sys || s_sys) {
         double* x = v_sys ? M.V : M.SP + int64_t(q) * n;
         const int qq = v_sys ? 0 : q;
-        const double* cap = v_sys ? KS.cap : KS.sp_cap + qq * n;
         const double* coup = v_sys ? KS.ax : KS.sp_coup + qq * n;
         const double* f = v_sys ? KS.vf : KS.sp_f + qq * n;
         const double* d = v_sys ? KS.vd : KS.sp_d + qq * n;
-        const double* glr = v_sys ? KS.glr : cap;
-        const double* rc = v_sys ? M.rhs_cur : cap;
+        const double* y = v_sys ? KS.vr : KS.sp_r + qq * n;
         double* r2 = M.r2 + int64_t(v_sys ? 0 : 1 + q) * n;
-        const int pc = (!v_sys && q == K.prp_idx && X.prod != 0.0) ? K.prp_comp : -1;
-        const double prod = X.prod;
-        for (int i = 0; i < n; ++i) {
-          // V:       rhs = g_leak_rhs + 0.0 + (has_current ? rhs_current : 0.0) (engine.cpp:683)
-          // species: rhs = 0.0, or prod at the synthesis compartment          (engine.cpp:746-748)
-          const double rhs = v_sys ? (glr[i] + 0.0 + (hc ? rc[i] : 0.0)) : (i == pc ? prod : 0.0);
-          r2[i] = cap[i] * x[i] + rhs;
+        {
+          const double* cap = v_sys ? KS.cap : KS.sp_cap + qq * n;
+          const int pc = (!v_sys && q == K.prp_idx && X.prod != 0.0) ? K.prp_comp : -1;
+          for (int i = 0; i < n; ++i) {
+            const double rhs = v_sys ? (KS.glr[i] + 0.0 + (hc ? M.rhs_cur[i] : 0.0))
+                                     : (i == pc ? X.prod : 0.0);
+            r2[i] = cap[i] * x[i] + rhs;
+          }
         }
-        mcg_solve_const(n, KS.par, coup, f, d, x, r2);
+        mcg_sweep_const(n, KS.par, coup, f, d, y, x, r2);
       } else if (sys == 0) {
         if (K.dyn == MCG_DYN_LIF_EXACT) {
           if (!refractory) {
@@ -669,27 +1138,26 @@ __device__ void mcg_cell_batch(const McgDev& D, const McgBatchArgs& A, int32_t b
         if (n > 1 && !K.sp_const)
           for (int p = 0; p < K.n_species; ++p)
             ok &= mcg_species_sys(n, p == K.prp_idx, K.prp_comp, X.prod, KS.sp_cap + p * n,
-                                  KS.sp_gs + p * n, KS.sp_coup + p * n, nullptr, nullptr, KS.par,
+                                  KS.sp_gs + p * n, KS.sp_coup + p * n, KS.par,
                                   M.SP + int64_t(p) * n, M.r2 + int64_t(1 + p) * n, M.diag,
                                   D.s_rhs + D.comp_off[c]);
       } else if (q < K.n_species && n == 1) {
         mcg_species_sys(1, q == K.prp_idx, K.prp_comp, X.prod, KS.sp_cap + q, KS.sp_gs + q,
-                        KS.sp_coup + q, nullptr, nullptr, KS.par, M.SP + q, M.r2, M.diag,
-                        M.rhs_cur);
+                        KS.sp_coup + q, KS.par, M.SP + q, M.r2, M.diag, M.rhs_cur);
       }
       if (!ok) atomicOr(D.err, MCG_ERR_FLAG_SINGULAR);
     }
     __syncthreads();
-    MCG_PH(5);
+    MCG_PH(6);
 
     // ---- F. spike detection (engine.cpp:753-769)
     if (tid < nc) {
       const int c = c0 + tid;
       McgCellSm& X = cs[tid];
-      const McgKind& K = D.kinds[X.kind];
+      const McgKind& K = kc[tid];
       X.fired = 0;
       if (K.has_detector && !X.refractory) {
-        const double* V = (K.n <= m) ? smem + int64_t(tid) * A.comp_stride : D.v + D.comp_off[c];
+        const double* V = (K.n <= m) ? mcg_comp_block(A, B, tid) : D.v + D.comp_off[c];
         const double va = V[K.detector_comp];
         if (X.armed && X.det_prev < K.threshold && va >= K.threshold) {
           double f = (va > X.det_prev) ? (K.threshold - X.det_prev) / (va - X.det_prev) : 1.0;
@@ -706,31 +1174,30 @@ __device__ void mcg_cell_batch(const McgDev& D, const McgBatchArgs& A, int32_t b
       }
     }
     __syncthreads();
-    MCG_PH(6);
+    MCG_PH(7);
     // post-event hook and LIF reset of the cells that fired (warp per cell)
     for (int k = warp; k < nc; k += nwarps) {
       if (!cs[k].fired) continue;
       const int c = c0 + k;
-      const McgKind& K = D.kinds[cs[k].kind];
-      mcg_post_event(D, K, D.cg_off[c], s, lane);
-      if (K.dyn == MCG_DYN_LIF || K.dyn == MCG_DYN_LIF_EXACT) {
-        double* V = (K.n <= m) ? smem + int64_t(k) * A.comp_stride : D.v + D.comp_off[c];
+      const McgKind& K = kc[k];
+      mcg_post_event_b(D, A, B, K, k, D.cg_off[c], s, lane);
+      if (cs[k].lif) {
+        double* V = (K.n <= m) ? mcg_comp_block(A, B, k) : D.v + D.comp_off[c];
         for (int i = lane; i < K.n; i += 32) V[i] = K.v_reset;
       }
     }
     __syncthreads();
-    MCG_PH(7);
+    MCG_PH(8);
     // detector bookkeeping and probes (engine.cpp:770-793)
     if (tid < nc) {
       const int c = c0 + tid;
       McgCellSm& X = cs[tid];
-      const McgKind& K = D.kinds[X.kind];
+      const McgKind& K = kc[tid];
       const bool in_sm = K.n <= m;
-      const double* V = in_sm ? smem + int64_t(tid) * A.comp_stride : D.v + D.comp_off[c];
-      const bool is_lif = K.dyn == MCG_DYN_LIF || K.dyn == MCG_DYN_LIF_EXACT;
+      const double* V = in_sm ? mcg_comp_block(A, B, tid) : D.v + D.comp_off[c];
       if (K.has_detector && !X.refractory) {
         if (X.fired) {
-          if (is_lif) X.refr = s + 1 + K.ref_steps;
+          if (X.lif) X.refr = s + 1 + K.ref_steps;
           else X.armed = 0;
         } else if (!X.armed && V[K.detector_comp] < K.threshold) {
           X.armed = 1;
@@ -739,35 +1206,20 @@ __device__ void mcg_cell_batch(const McgDev& D, const McgBatchArgs& A, int32_t b
       }
       for (int q = X.p0; q < X.p1; ++q) {
         const int p = D.probe_idx[q];
-        const McgProbe& P = D.probes[p];
-        if ((s + 1) % P.every != 0) continue;
-        const int64_t m0 = (D.ctl[3] + P.every) / P.every;
+        const McgProbe& Pr = D.probes[p];
+        if ((s + 1) % Pr.every != 0) continue;
+        const int64_t m0 = (D.ctl[3] + Pr.every) / Pr.every;
         const double* SP = in_sm ? V + m : D.species + D.sp_off[c];
-        D.trace_buf[D.trace_base[p] + ((s + 1) / P.every - m0)] = mcg_probe_value(D, K, c, P, V, SP);
+        D.trace_buf[D.trace_base[p] + ((s + 1) / Pr.every - m0)] =
+            mcg_probe_value(D, K, c, Pr, V, SP, mcg_stc_ref(A, B, tid, Pr.group));
       }
     }
     __syncthreads();
-    MCG_PH(8);
+    MCG_PH(9);
   }
 
-  // ---- epoch exit: write back state, log the batch's spikes as one chunk
-  for (int k = 0; k < nc; ++k) {
-    const int c = c0 + k;
-    const McgKind& K = D.kinds[cs[k].kind];
-    if (K.n > m) continue;
-    const double* base = smem + int64_t(k) * A.comp_stride;
-    const int n = K.n;
-    const int64_t co = D.comp_off[c];
-    for (int i = tid; i < n; i += T) D.v[co + i] = base[i];
-    double* gs = D.species + D.sp_off[c];
-    for (int i = tid; i < K.n_species * n; i += T) gs[i] = base[m + i];
-    if (K.dyn == MCG_DYN_HH)
-      for (int i = tid; i < n; i += T) {
-        D.hh_m[co + i] = base[(1 + D.sp_max) * m + i];
-        D.hh_h[co + i] = base[(2 + D.sp_max) * m + i];
-        D.hh_n[co + i] = base[(3 + D.sp_max) * m + i];
-      }
-  }
+  // ---- epoch end: log the batch's spikes as one chunk, publish what the next
+  // expansion reads (spike slots, inbox cursors)
   __shared__ int s_log_off;
   if (tid == 0) {
     int tot = 0;
@@ -794,44 +1246,55 @@ __device__ void mcg_cell_batch(const McgDev& D, const McgBatchArgs& A, int32_t b
       }
     }
     D.sp_count[c] = k;
-    if (X.ndel) atomicAdd(D.delivered, X.ndel);
     D.pend_sel[c] = X.sel;
     D.pend_off[c] = X.cur;
     D.pend_n[c] = X.end;
     D.inc_n[c] = 0;
-    D.refr_until[c] = X.refr;
-    D.det_prev[c] = X.det_prev;
-    D.armed[c] = X.armed;
   }
   __syncthreads();
-  MCG_PH(10);
-  if (A.phase && tid == 0)
-    for (int i = 0; i < 12; ++i) atomicAdd(&A.phase[i], ph[i]);
-#undef MCG_PH
+  MCG_PH(11);
 }
 
 __global__ void __launch_bounds__(512, 1) k_batch(McgDev D, McgBatchArgs A, int64_t max_len) {
-  extern __shared__ double mcg_smem[];
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
-  const int C = A.cells_per_cta;
-  // shared-memory carve-up: compartment blocks, noise draws, STC fold
-  // deltas, per-cell scalars, STC segment table, changed-flag bitmask
-  double* comp = mcg_smem;
-  double* nbuf = comp + int64_t(C) * A.comp_stride;
-  double* dbuf = nbuf + C * 32;
-  double* ksm = dbuf + int64_t(C) * A.stc_max;
-  McgCellSm* cs = reinterpret_cast<McgCellSm*>(ksm + A.kind_doubles);
-  McgSegSm* seg = reinterpret_cast<McgSegSm*>(cs + C);
-  uint32_t* fmask = reinterpret_cast<uint32_t*>(seg + C * A.n_stc_max);
+  const McgBatchSm B = mcg_batch_sm(A);
+  if (A.phase && threadIdx.x == 0) {
+    for (int i = 0; i < MCG_NPHASE; ++i) mcg_ph_acc[i] = 0;
+    mcg_ph_acc[MCG_NPHASE] = clock64();
+  }
+  if (A.n_specs_sm > 0) {
+    for (int i = threadIdx.x; i < A.n_specs_sm; i += blockDim.x) B.spec[i] = D.specs[i];
+    __syncthreads();
+  }
+  // resident: every batch has its own CTA for the whole launch
+  const bool resident = A.n_batches <= int(gridDim.x);
+  const bool mine = int(blockIdx.x) < A.n_batches;
+  if (resident && mine) mcg_batch_enter(D, A, blockIdx.x);
+  MCG_PH(14);
   for (int32_t j = 0; j < A.n_epochs; ++j) {
     int64_t s0, s1;
     if (!mcg_epoch_bounds(D.ctl, j, s0, s1)) break;
     mcg_expand(A.E, D, j, s0, s1, max_len);
+    MCG_PH(12);
     grid.sync();
+    MCG_PH(13);
     if (*D.abort) break;
-    for (int32_t b = blockIdx.x; b < A.n_batches; b += gridDim.x)
-      mcg_cell_batch(D, A, b, j, s0, s1, comp, cs, nbuf, dbuf, fmask, seg, ksm);
+    if (resident) {
+      if (mine) mcg_batch_epoch(D, A, blockIdx.x, j, s0, s1);
+    } else {
+      for (int32_t b = blockIdx.x; b < A.n_batches; b += gridDim.x) {
+        mcg_batch_enter(D, A, b);
+        mcg_batch_epoch(D, A, b, j, s0, s1);
+        mcg_batch_exit(D, A, b);
+      }
+    }
     grid.sync();
+    MCG_PH(13);
   }
+  if (resident && mine) mcg_batch_exit(D, A, blockIdx.x);
+  MCG_PH(14);
+  if (A.phase && threadIdx.x == 0)
+    for (int i = 0; i < MCG_NPHASE; ++i) atomicAdd(&A.phase[i], mcg_ph_acc[i]);
 }
+#undef MCG_PH

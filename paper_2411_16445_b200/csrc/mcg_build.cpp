@@ -329,6 +329,8 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
       S.sigma = P.sigma_pl_mV;
       S.f_int = P.f_int;
       S.tau_z = P.tau_z_ms;
+      S.r_tau_h = mcg_recip(S.tau_h);
+      S.r_tau_z = mcg_recip(S.tau_z);
       S.theta_tag = P.theta_tag_mV;
       S.cf = std::exp(-dt / P.tau_c_ms);
       S.nz1 = P.sigma_pl_mV * std::sqrt(double(1) / P.tau_h_ms) * std::sqrt(dt);
@@ -370,6 +372,7 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
       m.k_g_k.push_back(k.g_k[i]);
       m.k_cf.push_back(k.cf[i]);
       m.k_volume.push_back(g.volume[i]);
+      m.k_rvol.push_back(mcg_recip(g.volume[i]));
     }
     // LIF-cable V system without active conductances: cap/dt, g_leak + 0.0
     // (engine.cpp:680-686 with has_gsyn == false)
@@ -379,13 +382,14 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
         capv[i] = k.cap_nF[i] / dt;
         gsv[i] = k.g_leak[i] + 0.0;
       }
-      K.v_const = (K.dyn == MCG_DYN_LIF && n > 1 &&
+      K.v_const = (K.dyn == MCG_DYN_LIF &&
                    eliminate_constant(n, g.parent.data(), capv.data(), gsv.data(),
                                       k.axial.data(), fv.data(), dv.data()))
                       ? 1 : 0;
       for (int i = 0; i < n; ++i) {
         m.k_vf.push_back(fv[i]);
         m.k_vd.push_back(dv[i]);
+        m.k_vr.push_back(mcg_recip(dv[i]));
       }
     }
     K.sp_arr = static_cast<int64_t>(m.k_sp_cap_dt.size());
@@ -409,6 +413,7 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
       for (int i = 0; i < n; ++i) {
         m.k_sp_f.push_back(fs[i]);
         m.k_sp_d.push_back(ds[i]);
+        m.k_sp_r.push_back(mcg_recip(ds[i]));
       }
     }
     m.k_sp_off[ki + 1] = static_cast<int64_t>(m.k_sp_decay_tau.size());

@@ -33,6 +33,13 @@ struct Grid {
 Grid discretize(const mcg_kind& k);
 int64_t ceil_steps(double t_ms, double dt_ms);
 
+// reciprocal operand of mcg_div (mcg_device.cuh): RN(1/d), or 0 outside the
+// range where the FMA-corrected quotient is proven correctly rounded
+inline double mcg_recip(double d) {
+  const double a = d < 0 ? -d : d;
+  return (a >= 0x1p-200 && a <= 0x1p200) ? 1.0 / d : 0.0;
+}
+
 struct Source {
   int32_t type;
   std::vector<double> t0, t1, prob;   // poisson windows (prob = rate*dt*1e-3)
@@ -58,6 +65,7 @@ struct HostModel {
   std::vector<double> k_sp_cap_dt, k_sp_gs, k_sp_coupling, k_sp_init;
   std::vector<double> k_vf, k_vd;        // precomputed V elimination (per comp)
   std::vector<double> k_sp_f, k_sp_d;    // precomputed species elimination
+  std::vector<double> k_vr, k_sp_r, k_rvol;  // mcg_recip of k_vd, k_sp_d, k_volume
   std::vector<double> k_sp_decay_tau;  // per kind species (for fast-forward)
   std::vector<int64_t> k_sp_off;       // per kind: offset into k_sp_decay_tau
   std::vector<McgSpec> specs;

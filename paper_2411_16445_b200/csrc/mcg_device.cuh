@@ -48,6 +48,7 @@ struct McgDev {
   double *s_gsyn, *s_gsyn_rhs, *s_rhs_cur, *s_diag, *s_rhs;
   double* s_r2;               // (1 + sp_max) x compartments
   const double *k_vf, *k_vd, *k_sp_f, *k_sp_d;
+  const double *k_vr, *k_sp_r, *k_rvol;  // mcg_recip of k_vd, k_sp_d, k_volume
   int32_t sp_max;             // max species per kind
   int32_t smem_n;             // cells with n <= smem_n are staged in shared memory
   int32_t smem_stride;        // doubles per warp in dynamic shared memory
@@ -97,6 +98,29 @@ struct McgDev {
   unsigned long long* delivered;
 };
 
+// x / d, bitwise IEEE division, from y = mcg_recip(d) = RN(1/d): with
+// q = RN(x*y) and the exact remainder r = x - q*d (one FMA), RN(q + r*y) is the
+// correctly rounded quotient (Markstein's theorem) as long as nothing under-
+// or overflows, which the operand ranges below guarantee.  x == +-0 gives
+// q = x*y, the IEEE signed zero of x/d.  Elsewhere (y == 0, tiny or huge x,
+// inf, nan) it is the plain division.  Replaces a ~110-cycle dependent DDIV
+// with three FP64 operations on the sweep critical paths.
+// out of line: the rare paths keep their register pressure off the callers
+__device__ __noinline__ double mcg_div_slow(double x, double d) { return __ddiv_rn(x, d); }
+
+__device__ __forceinline__ double mcg_div(double x, double d, double y) {
+  // the quotient is computed unconditionally (nothing on the dependent chain
+  // waits for the range test); only the rare fallback is a branch
+  const double q = __dmul_rn(x, y);
+  const double r = __fma_rn(-q, d, x);
+  double res = __fma_rn(r, y, q);
+  const double ax = fabs(x);
+  if (ax == 0.0) res = q;
+  if (__builtin_expect(y == 0.0 || ax > 0x1p700 || (ax < 0x1p-700 && ax != 0.0), 0))
+    res = mcg_div_slow(x, d);
+  return res;
+}
+
 __device__ __forceinline__ unsigned mcg_lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -110,10 +134,18 @@ __device__ __forceinline__ void mcg_stdp_decay(double& pre, double& post, const 
   post *= mcg_exp(-gap / S.tau_post);
 }
 
+// STC instance state of the addressed group: in global memory (slot0 < 0) or
+// in the batch kernel's shared-memory copy, SoA with `stride` doubles per
+// field (h, z, c, |h-h0|), instance i at slot0 + i
+struct McgStcSm {
+  double* base;
+  int32_t stride, slot0;
+};
+
 // ---- apply_events (engine.cpp:452-513); lane 0 only -----------------------
 __device__ void mcg_apply_event(const McgDev& D, const McgKind& K, int c, int64_t cg0,
                                 double* V, int32_t group, uint32_t inst, double w, int etype,
-                                bool refractory, int64_t s) {
+                                bool refractory, int64_t s, McgStcSm R = McgStcSm{nullptr, 0, -1}) {
   McgCellGroup& G = D.cgs[cg0 + group];
   const McgSpec& S = D.specs[G.spec];
   const int64_t j = G.inst + inst;
@@ -167,8 +199,11 @@ __device__ void mcg_apply_event(const McgDev& D, const McgKind& K, int c, int64_
       break;
     }
     case MCG_SYN_STC_CHARGE: {
+      const bool sm = R.slot0 >= 0;
+      const int32_t sl = R.slot0 + int32_t(inst);
       if (etype == 1) {
-        D.i_stc_c[j] += S.cpre_s;  // stc_on_pre_calcium
+        if (sm) R.base[2 * R.stride + sl] += S.cpre_s;  // stc_on_pre_calcium
+        else D.i_stc_c[j] += S.cpre_s;
       } else {
         // delayed calcium: internal event at s + delay, seq = internal_seq++
         McgFifo& F = D.fifos[G.fifo];
@@ -182,8 +217,9 @@ __device__ void mcg_apply_event(const McgDev& D, const McgKind& K, int c, int64_
         }
         ++D.internal_seq[c];
         if (!refractory) {
-          const int comp = D.i_comp[j];
-          const double tw = D.i_stc_h[j] + S.h0 * D.i_stc_z[j];
+          const int comp = S.comp;  // every instance sits on the placement's compartment
+          const double tw = sm ? R.base[sl] + S.h0 * R.base[R.stride + sl]
+                               : D.i_stc_h[j] + S.h0 * D.i_stc_z[j];
           V[comp] += tw * w * D.k_cf[K.arr + comp];
         }
       }
@@ -248,70 +284,76 @@ __device__ __forceinline__ double mcg_hh_bn(double v) {
   return 0.125 * mcg_exp(-(v + 65.0) / 80.0);
 }
 
-// STC early/late phase of one instance (mechanisms.hpp:213-242, engine.cpp:624-644)
-// `changed`: |h-h0| changed; `delta` is then the SPS increment at `comp`
-struct McgStcOut {
-  double delta;
-  int comp;
-  bool changed;
+// STC early/late phase of one instance (mechanisms.hpp:213-242,
+// engine.cpp:624-644) on values already in registers: h, z, calcium c and the
+// |h - h0| last folded into the SPS pool (a).  Returns true when |h - h0|
+// changed; `delta` is then the SPS increment at the placement's compartment.
+// late: the cell has a PRP pool (prp = its value at that compartment).
+struct McgStcVal {
+  double h, z, c, a;
 };
 
-__device__ __forceinline__ McgStcOut mcg_stc_instance(const McgDev& D, const McgSpec& S,
-                                                      int64_t j, uint32_t gid, int gi, int i,
-                                                      int64_t s, const double* prp_base,
-                                                      const double* vol_k) {
-  McgStcOut out{0.0, 0, false};
-  double h = D.i_stc_h[j];
-  double z = D.i_stc_z[j];
-  double cc = D.i_stc_c[j];
-  const bool up = cc > S.theta_p, dn = cc > S.theta_d;
+// plasticity noise draw of one STC instance (rare: calcium above a threshold)
+__device__ __noinline__ double mcg_stc_noise(uint64_t seed, uint32_t gid, int gi, int i,
+                                             int64_t s) {
+  const mcg_key key = mcg_make_key(seed, gid, (2ull << 32) | uint64_t(gi), uint64_t(i));
+  return mcg_normal_for(&key, static_cast<uint64_t>(s));
+}
+
+__device__ __forceinline__ bool mcg_stc_step(const McgSpec& S, double dt, uint64_t seed,
+                                             uint32_t gid, int gi, int i, int64_t s, bool late,
+                                             double prp, double vol, double rvol, McgStcVal& v,
+                                             double& delta) {
+  double h = v.h;
+  const bool up = v.c > S.theta_p, dn = v.c > S.theta_d;
   double nrm = 0.0;
-  if (S.sigma != 0.0 && (up || dn)) {
-    const mcg_key key = mcg_make_key(D.seed, gid, (2ull << 32) | uint64_t(gi), uint64_t(i));
-    nrm = mcg_normal_for(&key, static_cast<uint64_t>(s));
-  }
+  if (S.sigma != 0.0 && (up || dn)) nrm = mcg_stc_noise(seed, gid, gi, i, s);
   // stc_early_step
   const int crossings = int(up) + int(dn);
   double d = 0.1 * (S.h0 - h);
   if (up) d += S.gamma_p * (10.0 - h);
   if (dn) d -= S.gamma_d * h;
-  double dh = d / S.tau_h * D.dt;
+  double dh = mcg_div(d, S.tau_h, S.r_tau_h) * dt;
   if (crossings > 0 && S.sigma != 0.0) dh += (crossings == 1 ? S.nz1 : S.nz2) * nrm;
   h += dh;
-  const int comp = D.i_comp[j];
-  out.comp = comp;
   const double na = fabs(h - S.h0);
-  const double old = D.i_sps_abs[j];
-  if (na != old) {
-    out.delta = (na - old) / vol_k[comp];
-    D.i_sps_abs[j] = na;
-    out.changed = true;
+  bool changed = false;
+  if (na != v.a) {
+    delta = mcg_div(na - v.a, vol, rvol);
+    v.a = na;
+    changed = true;
   }
   // stc_late_step
-  if (prp_base) {
-    const double prp = prp_base[comp];
-    if (!(prp <= 0.0)) {
-      double dd = 0.0;
-      if (h - S.h0 > S.theta_tag) dd += (1.0 - z);
-      if (S.h0 - h > S.theta_tag) dd -= (z + 0.5);
-      z += prp * S.f_int * dd * D.dt / S.tau_z;
-    }
+  if (late && !(prp <= 0.0)) {
+    double dd = 0.0;
+    if (h - S.h0 > S.theta_tag) dd += (1.0 - v.z);
+    if (S.h0 - h > S.theta_tag) dd -= (v.z + 0.5);
+    v.z += mcg_div(prp * S.f_int * dd * dt, S.tau_z, S.r_tau_z);
   }
-  cc *= S.cf;
-  D.i_stc_h[j] = h;
-  D.i_stc_z[j] = z;
-  D.i_stc_c[j] = cc;
-  return out;
+  v.c *= S.cf;
+  v.h = h;
+  return changed;
 }
 
 // probe_value (engine.cpp:795-829)
 __device__ double mcg_probe_value(const McgDev& D, const McgKind& K, int c, const McgProbe& P,
-                                  const double* V, const double* SP) {
+                                  const double* V, const double* SP,
+                                  McgStcSm R = McgStcSm{nullptr, 0, -1}) {
   if (P.what == MCG_PROBE_VOLTAGE) return (K.dyn == MCG_DYN_NONE) ? 0.0 : V[P.comp];
   if (P.what == MCG_PROBE_SPECIES) return SP[int64_t(P.species) * K.n + P.comp];
   const McgCellGroup& G = D.cgs[D.cg_off[c] + P.group];
   const McgSpec& S = D.specs[G.spec];
   const int64_t j = G.inst + P.instance;
+  if (S.kind == MCG_SYN_STC_CHARGE && R.slot0 >= 0) {
+    const double* b = R.base + R.slot0 + P.instance;
+    switch (P.what) {
+      case MCG_PROBE_SYN_WEIGHT: return b[0] + S.h0 * b[R.stride];
+      case MCG_PROBE_SYN_H: return b[0];
+      case MCG_PROBE_SYN_Z: return b[R.stride];
+      case MCG_PROBE_SYN_C: return b[2 * R.stride];
+      default: break;
+    }
+  }
   switch (P.what) {
     case MCG_PROBE_SYN_WEIGHT:
       switch (S.kind) {

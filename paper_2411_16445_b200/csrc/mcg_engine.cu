@@ -1,18 +1,15 @@
 // mcg_engine.cu — host orchestration of the B200 engine and the C ABI
 // (include/mcg.h).
 //
-// Engine::advance_to (engine.cpp:909-945) runs as batches of min-delay epochs.
-// One batch is a CUDA graph of E epochs, each epoch
-//   k_inbox        source events of the epoch + spike exchange of the previous
-//                  epoch into per-cell incoming buffers        (mcg_events.cuh)
-//   k_epoch        every cell, every step of the epoch, one warp per cell;
-//                  inbox sort + merge at entry                  (mcg_epoch.cuh)
-//   scan + k_spike_write/total   ordered spike compaction     (mcg_events.cuh)
-// Epoch bounds live in device memory, so the graph is replayed unchanged; the
-// host synchronizes once per batch (spike log, overflow/abort flags).  All
-// state stays resident in HBM; cell state, spikes and traces are copied to
-// the host only when asked (the lazily-synced mirror of engine.hpp).
-#include <cub/cub.cuh>
+// Engine::advance_to (engine.cpp:909-945) runs as launches of the persistent
+// cooperative batch kernel k_batch (mcg_batch.cuh): up to kBatch min-delay
+// epochs per launch, each epoch = spike/source expansion into per-cell
+// inboxes, grid barrier, every CTA steps its cells through the epoch, grid
+// barrier.  Epoch bounds live in device memory; the host synchronizes once per
+// launch (spike log chunks, overflow/abort flags).  All state stays resident
+// in HBM; cell state, spikes and traces are copied to the host only when
+// asked (the lazily-synced mirror of engine.hpp).
+#include <cub/cub.cuh>  // mcg_er_connect's scan
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -76,9 +73,8 @@ enum { C_EP_SPK = 0, C_LOG = 1, C_DELIVERED = 2, C_N = 4 };
 
 // anything still undelivered: queued keys, unexpanded spikes with local
 // fan-out, or delayed calcium (the fast-forward guard, engine.cpp:958-960)
-__global__ void k_pending(McgDev D, const uint32_t* ep_gid, const unsigned long long* ep_n,
-                          const int64_t* out_begin, const int64_t* out_end, int32_t n_fifos,
-                          int32_t* flag) {
+__global__ void k_pending(McgDev D, const int64_t* out_begin, const int64_t* out_end,
+                          int32_t n_fifos, int32_t* flag) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < D.n_cells && (D.pend_n[i] > D.pend_off[i] || D.inc_n[i] > 0)) atomicOr(flag, 1);
   if (i < n_fifos && D.fifos[i].head < D.fifos[i].tail) atomicOr(flag, 1);
@@ -87,8 +83,6 @@ __global__ void k_pending(McgDev D, const uint32_t* ep_gid, const unsigned long 
     const uint32_t g = D.gid0 + uint32_t(i);
     if (out_end[g] > out_begin[g]) atomicOr(flag, 1);
   }
-  (void)ep_gid;
-  (void)ep_n;
 }
 
 }  // namespace
@@ -100,15 +94,15 @@ struct Engine {
   int64_t step = 0;
   int64_t L = 1;              // epoch length (min_delay_steps, or free_epoch without cell edges)
   static constexpr int kSmemMaxComps = 96;  // cells up to this size live in shared memory
-  static constexpr int kBlock = 128;        // 4 warps = 4 cells per block
-  static constexpr int kBatch = 32;         // epochs per graph launch
+  static constexpr int kBlock = 128;        // fast-forward: 4 warps = 4 cells per block
+  static constexpr int kBatch = 32;         // epochs per batch-kernel launch
 
   // device model
   DBuf<McgKind> d_kinds;
   DBuf<McgSpec> d_specs;
   DBuf<int32_t> d_k_parent;
   DBuf<double> d_k_cap_dt, d_k_g_leak, d_k_g_leak_rhs, d_k_axial, d_k_g_na, d_k_g_k, d_k_cf,
-      d_k_volume, d_k_sp_cap_dt, d_k_sp_gs, d_k_sp_coupling, d_k_vf, d_k_vd, d_k_sp_f, d_k_sp_d;
+      d_k_volume, d_k_sp_cap_dt, d_k_sp_gs, d_k_sp_coupling, d_k_vf, d_k_vd, d_k_sp_f, d_k_sp_d, d_k_vr, d_k_sp_r, d_k_rvol;
   DBuf<int32_t> d_cell_kind;
   DBuf<int64_t> d_comp_off, d_sp_off, d_cg_off;
   DBuf<double> d_v, d_hh_m, d_hh_h, d_hh_n, d_species, d_det_prev;
@@ -147,13 +141,10 @@ struct Engine {
   // spikes
   int32_t sp_cap = 1;
   DBuf<int32_t> d_sp_count;
-  DBuf<int64_t> d_sp_step, d_sp_scan;
+  DBuf<int64_t> d_sp_step;
   DBuf<double> d_sp_t;
-  DBuf<uint32_t> d_ep_gid;
-  DBuf<int64_t> d_ep_step;
   DBuf<double> d_log_t;       // batch log
   DBuf<uint32_t> d_log_gid;
-  DBuf<unsigned char> d_cub_tmp;
   // probes
   DBuf<McgProbe> d_probes;
   DBuf<int32_t> d_probe_off, d_probe_idx;
@@ -171,19 +162,13 @@ struct Engine {
   // host spike mirror
   std::vector<double> spk_t;
   std::vector<uint32_t> spk_gid;
-  // graph of one batch (warp-per-cell path)
-  cudaGraphExec_t gexec = nullptr;
-  bool graph_timed = false;
-  double* graph_trace = nullptr;
-  std::vector<cudaEvent_t> ev_epoch;
   // persistent batch kernel (cell batches per CTA)
   static constexpr int kBatchThreads = 512;
   int32_t bc_cells = 1, bc_batches = 1, bc_grid = 1, bc_stc_max = 1, bc_nstc_max = 1;
-  int32_t bc_kind_doubles = 0;
+  int32_t bc_kind_doubles = 0, bc_specs_sm = 0, bc_stc_sm = 0;
   size_t bc_smem = 0;
   DBuf<int4> d_chunks;
   DBuf<unsigned long long> d_chunk_n;
-  DBuf<unsigned long long> d_stamp;
   cudaEvent_t evk0 = nullptr, evk1 = nullptr;
   // MCG_PHASE_TIMING=1: per-phase cycle totals of the batch kernel, printed
   // to stderr after every advance_to (development instrumentation)
@@ -192,10 +177,10 @@ struct Engine {
 
   void print_phases() {
     if (!phase_timing || !d_phase.p) return;
-    unsigned long long ph[12];
+    unsigned long long ph[MCG_NPHASE];
     CK(cudaMemcpy(ph, d_phase.p, sizeof(ph), cudaMemcpyDeviceToHost));
-    std::fprintf(stderr, "phase cycles (sum over CTA batches):");
-    for (int i = 0; i < 12; ++i) std::fprintf(stderr, " %d:%.3g", i, double(ph[i]));
+    std::fprintf(stderr, "phase cycles (sum over CTAs):");
+    for (int i = 0; i < MCG_NPHASE; ++i) std::fprintf(stderr, " %d:%.3g", i, double(ph[i]));
     std::fprintf(stderr, "  steps=%lld batches=%d\n", (long long)stats.steps, bc_batches);
   }
   // stats
@@ -206,8 +191,6 @@ struct Engine {
   McgDev dev{};
 
   ~Engine() {
-    if (gexec) cudaGraphExecDestroy(gexec);
-    for (cudaEvent_t e : ev_epoch) cudaEventDestroy(e);
     if (h_ctr) cudaFreeHost(h_ctr);
     if (h_err) cudaFreeHost(h_err);
     if (h_abort) cudaFreeHost(h_abort);
@@ -225,7 +208,8 @@ struct Engine {
     const int nl = n_local();
     int dev_sms = 148;
     CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device));
-    bc_stc_max = 1;
+    std::vector<int> stc_n(nl, 0);
+    int cell_stc_max = 0;
     bc_nstc_max = 1;
     for (int c = 0; c < nl; ++c) {
       const McgKind& K = m.kinds[m.cell_kind[c]];
@@ -236,27 +220,48 @@ struct Engine {
         tot += G.size;
         ++ng;
       }
-      bc_stc_max = std::max(bc_stc_max, tot);
+      stc_n[c] = tot;
+      cell_stc_max = std::max(cell_stc_max, tot);
       bc_nstc_max = std::max(bc_nstc_max, ng);
     }
-    // compartment block, noise draws, fold deltas, scalars, STC segments,
-    // changed-flag bitmask (see the carve-up in k_batch)
-    const size_t per_cell = size_t(smem_stride) * 8 + 32 * 8 + size_t(bc_stc_max) * 8 +
-                            sizeof(McgCellSm) + size_t(bc_nstc_max) * sizeof(McgSegSm) +
-                            (size_t(bc_stc_max) / 32 + 2) * 4;
-    // staged kind constants (mcg_batch.cuh McgKindSm): one block per distinct
-    // kind of a batch, (8 + 5 S) n doubles + the parent array
+    if (bc_nstc_max > 0xffff) throw Error(MCG_ERR_ENGINE, "too many STC placements per kind");
+    // per cell: compartment block, noise draws, kind and cell records, STC
+    // segments, and (upper bound) its STC slots in the fold/locator tables
+    const size_t per_cell = size_t(smem_stride) * 8 + 32 * 8 + sizeof(McgKind) + sizeof(McgCellSm) +
+                            size_t(bc_nstc_max) * sizeof(McgSegSm) + size_t(cell_stc_max) * 12;
+    // staged kind constants (McgKindSm): one block per distinct kind of a batch
     size_t kb_max = 0;
     for (const McgKind& K : m.kinds)
-      if (K.n <= smem_n)
-        kb_max = std::max<size_t>(kb_max, size_t(8 + 5 * K.n_species) * K.n + (K.n + 1) / 2);
+      if (K.n <= smem_n) kb_max = std::max<size_t>(kb_max, mcg_kind_block_doubles(K.n, K.n_species));
+    // the spec table, when small, is staged once per launch
+    bc_specs_sm = m.specs.size() * sizeof(McgSpec) <= 16 * 1024 ? static_cast<int32_t>(m.specs.size()) : 0;
+    const size_t fixed = size_t(bc_specs_sm) * sizeof(McgSpec) + 2048;
     const size_t budget = 200 * 1024;
-    const int c_max = static_cast<int>(std::max<size_t>(1, budget / (per_cell + kb_max * 8)));
-    bc_cells = std::clamp((nl + dev_sms - 1) / std::max(dev_sms, 1), 1, c_max);
+    const int c_max = static_cast<int>(std::max<size_t>(1, (budget - fixed) / (per_cell + kb_max * 8)));
+    bc_cells = std::clamp((nl + dev_sms - 1) / std::max(dev_sms, 1), 1, std::min(c_max, 0xffff));
     bc_batches = std::max(1, (nl + bc_cells - 1) / bc_cells);
-    bc_kind_doubles = static_cast<int32_t>(
-        std::min<size_t>(bc_cells, m.kinds.size()) * kb_max);
-    bc_smem = size_t(bc_cells) * per_cell + size_t(bc_kind_doubles) * 8 + 64;
+    // STC slots of the fullest batch
+    bc_stc_max = 1;
+    for (int b = 0; b < bc_batches; ++b) {
+      int tot = 0;
+      for (int c = b * bc_cells; c < std::min(nl, (b + 1) * bc_cells); ++c) tot += stc_n[c];
+      bc_stc_max = std::max(bc_stc_max, tot);
+    }
+    bc_kind_doubles = static_cast<int32_t>(std::min<size_t>(bc_cells, m.kinds.size()) * kb_max);
+    // fold-flag words: one per 32 slots of every 512-thread round
+    const size_t fmask_words = size_t((bc_stc_max + kBatchThreads - 1) / kBatchThreads) * (kBatchThreads / 32) + 1;
+    bc_smem = size_t(bc_cells) * (size_t(smem_stride) * 8 + 32 * 8 + sizeof(McgKind) + sizeof(McgCellSm) +
+                                  size_t(bc_nstc_max) * sizeof(McgSegSm)) +
+              size_t(bc_stc_max) * (8 + 4) + size_t(bc_kind_doubles) * 8 +
+              size_t(bc_specs_sm) * sizeof(McgSpec) + fmask_words * 4 + 64;
+    // resident batches (one per CTA) keep their STC state in shared memory too
+    int smem_optin = 0;
+    CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    bc_stc_sm = (bc_batches <= dev_sms && stc_n.size() > 0 &&
+                 bc_smem + size_t(bc_stc_max) * 32 <= size_t(smem_optin) - 1024)
+                    ? 1 : 0;
+    if (std::getenv("MCG_NO_STC_SM")) bc_stc_sm = 0;
+    if (bc_stc_sm) bc_smem += size_t(bc_stc_max) * 32;
     CK(cudaFuncSetAttribute(k_batch, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(bc_smem)));
     // leave the rest of the unified L1/shared array to L1 (STC state streams through it)
@@ -266,10 +271,10 @@ struct Engine {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_batch, kBatchThreads, bc_smem));
     if (occ < 1) throw Error(MCG_ERR_CUDA, "batch kernel does not fit on an SM");
     bc_grid = std::min(bc_batches, occ * dev_sms);
+    if (bc_stc_sm && bc_grid < bc_batches) throw Error(MCG_ERR_CUDA, "batch kernel: not resident");
     d_chunks.alloc(size_t(kBatch) * bc_batches + 1);
     d_chunk_n.alloc(1);
     d_chunk_n.zero(st);
-    d_stamp.alloc(2 * kBatch + 2);
     if (!evk0) CK(cudaEventCreate(&evk0));
     if (!evk1) CK(cudaEventCreate(&evk1));
   }
@@ -287,8 +292,6 @@ struct Engine {
     CK(cudaMallocHost(&h_ctl, 4 * sizeof(int64_t)));
     CK(cudaEventCreate(&eva));
     CK(cudaEventCreate(&evb));
-    ev_epoch.resize(2 * kBatch);
-    for (auto& e : ev_epoch) CK(cudaEventCreate(&e));
     const int nl = n_local();
     // epoch length: min delay (cells independent within it, engine.cpp:913-915)
     const int64_t free_epoch = std::clamp<int64_t>((int64_t(1) << 22) / std::max(nl, 1), 16, 4096);
@@ -324,6 +327,9 @@ struct Engine {
     d_k_vd.upload(m.k_vd, st);
     d_k_sp_f.upload(m.k_sp_f, st);
     d_k_sp_d.upload(m.k_sp_d, st);
+    d_k_vr.upload(m.k_vr, st);
+    d_k_sp_r.upload(m.k_sp_r, st);
+    d_k_rvol.upload(m.k_rvol, st);
     d_cell_kind.upload(m.cell_kind, st);
     d_comp_off.upload(m.comp_off, st);
     d_sp_off.upload(m.sp_off, st);
@@ -350,8 +356,6 @@ struct Engine {
     d_s_r2.alloc(nc * (1 + sp_max));
     smem_stride = (9 + 2 * sp_max) * smem_n;
     smem_bytes = static_cast<size_t>(smem_stride) * sizeof(double) * (kBlock / 32);
-    CK(cudaFuncSetAttribute(k_epoch, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(smem_bytes)));
     CK(cudaFuncSetAttribute(k_ff, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(smem_bytes)));
     d_cgs.upload(m.cgs, st);
@@ -427,19 +431,10 @@ struct Engine {
     const size_t slots = static_cast<size_t>(std::max(nl, 1)) * sp_cap;
     d_sp_count.alloc(std::max(nl, 1));
     d_sp_count.zero(st);
-    d_sp_scan.alloc(std::max(nl, 1));
     d_sp_step.alloc(slots);
     d_sp_t.alloc(slots);
-    d_ep_gid.alloc(slots);
-    d_ep_step.alloc(slots);
     d_log_t.alloc(slots * kBatch);
     d_log_gid.alloc(slots * kBatch);
-    {
-      size_t need = 0;
-      CK(cub::DeviceScan::ExclusiveSum(nullptr, need, d_sp_count.p, d_sp_scan.p,
-                                       std::max(nl, 1), st));
-      d_cub_tmp.alloc(std::max<size_t>(need, 16));
-    }
 
     // probes: per-cell CSR over local probes
     std::vector<int32_t> poff(nl + 1, 0), pidx;
@@ -505,7 +500,6 @@ struct Engine {
     std::swap(d_pend.n, np.n);
     d_inc.alloc(static_cast<size_t>(std::max(nl, 1)) * inc_cap);
     d_inc_n.zero(st);
-    invalidate_graph();
   }
 
   void refresh_dev() {
@@ -551,6 +545,9 @@ struct Engine {
     D.k_vd = d_k_vd.p;
     D.k_sp_f = d_k_sp_f.p;
     D.k_sp_d = d_k_sp_d.p;
+    D.k_vr = d_k_vr.p;
+    D.k_sp_r = d_k_sp_r.p;
+    D.k_rvol = d_k_rvol.p;
     D.sp_max = sp_max;
     D.smem_n = smem_n;
     D.smem_stride = smem_stride;
@@ -620,51 +617,9 @@ struct Engine {
     E.rank_bits = rank_bits;
     E.ctl = d_ctl.p;
     E.abort = d_abort.p;
-    E.ep_gid = d_ep_gid.p;
-    E.ep_step = d_ep_step.p;
-    E.ep_n = d_ctr.p + C_EP_SPK;
     E.seed = m.seed;
     E.dt = m.dt;
     return E;
-  }
-
-  void invalidate_graph() {
-    if (gexec) cudaGraphExecDestroy(gexec);
-    gexec = nullptr;
-  }
-
-  // the kernels of epoch j of a batch (captured into the graph)
-  void enqueue_epoch(int32_t j) {
-    const int nl = n_local();
-    const McgEv E = ev_dev();
-    const int64_t work = std::max<int64_t>(int64_t(n_tasks) * L, int64_t(nl) * sp_cap * 32);
-    const unsigned ib = static_cast<unsigned>(std::clamp<int64_t>((work + 255) / 256, 1, 148 * 8));
-    k_inbox<<<ib, 256, 0, st>>>(E, j, L);
-    if (nl == 0) return;
-    // external event nodes: readable after the graph ran (plain records inside
-    // a capture only become internal dependencies)
-    if (timing) CK(cudaEventRecordWithFlags(ev_epoch[2 * j], st, cudaEventRecordExternal));
-    k_epoch<<<(nl * 32 + kBlock - 1) / kBlock, kBlock, smem_bytes, st>>>(dev, j);
-    if (timing) CK(cudaEventRecordWithFlags(ev_epoch[2 * j + 1], st, cudaEventRecordExternal));
-    size_t tb = d_cub_tmp.n;
-    CK(cub::DeviceScan::ExclusiveSum(d_cub_tmp.p, tb, d_sp_count.p, d_sp_scan.p, nl, st));
-    k_spike_write<<<(nl + 127) / 128, 128, 0, st>>>(dev, j, d_sp_scan.p, d_ep_gid.p, d_ep_step.p,
-                                                    d_log_t.p, d_log_gid.p, d_ctr.p + C_LOG);
-    k_spike_total<<<1, 1, 0, st>>>(dev, j, d_sp_scan.p, d_ctr.p + C_EP_SPK, d_ctr.p + C_LOG);
-  }
-  static constexpr int kKernelsPerEpoch = 6;
-
-  void capture_graph() {
-    invalidate_graph();
-    refresh_dev();
-    cudaGraph_t g = nullptr;
-    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    for (int32_t j = 0; j < kBatch; ++j) enqueue_epoch(j);
-    CK(cudaStreamEndCapture(st, &g));
-    CK(cudaGraphInstantiate(&gexec, g, 0));
-    CK(cudaGraphDestroy(g));
-    graph_timed = timing;
-    graph_trace = d_trace.p;
   }
 
   void check_err() {
@@ -684,21 +639,6 @@ struct Engine {
     CK(cudaMemcpyAsync(h_abort, d_abort.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     stats.events_delivered = static_cast<int64_t>(h_ctr[C_DELIVERED]);
-  }
-
-  // copy the batch spike log to the host mirror and reset it
-  void drain_log() {
-    const int64_t n = static_cast<int64_t>(h_ctr[C_LOG]);
-    if (n <= 0) return;
-    const size_t o = spk_t.size();
-    spk_t.resize(o + n);
-    spk_gid.resize(o + n);
-    CK(cudaMemcpyAsync(spk_t.data() + o, d_log_t.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(spk_gid.data() + o, d_log_gid.p, n * sizeof(uint32_t),
-                       cudaMemcpyDeviceToHost, st));
-    CK(cudaMemsetAsync(d_ctr.p + C_LOG, 0, sizeof(unsigned long long), st));
-    CK(cudaStreamSynchronize(st));
-    h_ctr[C_LOG] = 0;
   }
 
   // spike log of one launch: chunks (epoch, batch, offset, count) -> the
@@ -752,9 +692,11 @@ struct Engine {
     A.stc_max = bc_stc_max;
     A.n_stc_max = bc_nstc_max;
     A.kind_doubles = bc_kind_doubles;
+    A.n_specs_sm = bc_specs_sm;
+    A.stc_sm = bc_stc_sm;
     if (phase_timing) {
       if (!d_phase.p) {
-        d_phase.alloc(12);
+        d_phase.alloc(MCG_NPHASE);
         d_phase.zero(st);
       }
       A.phase = d_phase.p;
@@ -881,7 +823,7 @@ struct Engine {
     flag.zero(st);
     const int64_t span = std::max<int64_t>({int64_t(nl), int64_t(nf), int64_t(nl) * sp_cap, 1});
     k_pending<<<static_cast<unsigned>((span + 255) / 256), 256, 0, st>>>(
-        dev, d_ep_gid.p, d_ctr.p + C_EP_SPK, d_out_begin.p, d_out_end.p, nf, flag.p);
+        dev, d_out_begin.p, d_out_end.p, nf, flag.p);
     int32_t pending = 0;
     CK(cudaMemcpyAsync(&pending, flag.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

@@ -64,6 +64,7 @@ struct McgSpec {
   double nz1, nz2;        // sigma*sqrt(k/tau_h)*sqrt(dt), k=1,2 (mechanisms.hpp:226)
   double cpre_s, cpost_s; // c_pre*calcium_scale, c_post*calcium_scale
   int64_t ca_delay;       // stc_ca_delay_steps                  (engine.cpp:258-269)
+  double r_tau_h, r_tau_z;  // mcg_recip(tau_h), mcg_recip(tau_z)
 };
 
 // one (cell, group) pair: SynGroupRT's location in the instance SoA
