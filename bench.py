@@ -13,8 +13,10 @@ spontaneous phase and the onset of the 100 Hz learning stimulus at 10 s).
   e2e     same metric through the public API with host buffers: engine
           construction from the host recipe (H2D), advance over the W+K steps,
           spikes and final STC weights back to the host (D2H), wall-clocked
-  roofline  the epoch kernel (k_epoch): algorithmic bytes per launch
-          (SURVEY §8(d) B_step x fine steps per epoch) / mean launch duration
+  roofline  the persistent batch kernel (k_batch, one launch = up to 32
+          min-delay epochs): algorithmic bytes per launch (SURVEY §8(d) B_step
+          x fine steps per launch) / mean launch duration (CUDA events on the
+          engine's stream around each launch)
   cpu_baseline  the reference engine (oracle/_ref, compiled from
           /root/reference) on the same recipe, all host threads, bounded sample
 
@@ -113,11 +115,15 @@ def measured_peak_hbm():
         return 6650.0, "fallback"
 
 
-def traffic_per_launch():
-    p = os.path.join(ROOT, "profiles", "epoch_kernel_dram.json")
+def traffic_per_launch(steps_per_launch):
+    """DRAM bytes (read + write) of one k_batch launch from the committed ncu
+    capture (profiles/batch_kernel_dram.json), scaled to the mean launch's
+    fine steps so it is per launch like `achieved`."""
+    p = os.path.join(ROOT, "profiles", "batch_kernel_dram.json")
     try:
         with open(p) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            d = json.load(f)
+        return d["dram_bytes_per_launch"] * steps_per_launch / d["fine_steps_in_launch"]
     except Exception:
         return None
 
@@ -226,14 +232,14 @@ def run_gpu_arm(args):
     total = (s1["advance_ms"] - s0["advance_ms"]) * 1e-3
     wall_total = sum(wall_steps)
     value = args.steps * STEP_MS * 1e-3 / total
-    epochs = s1["epoch_kernel_launches"] - s0["epoch_kernel_launches"]
+    n_launch = s1["epoch_kernel_launches"] - s0["epoch_kernel_launches"]
     kern_ms = s1["epoch_kernel_ms"] - s0["epoch_kernel_ms"]
     fine_steps = s1["steps"] - s0["steps"]
     ev_per_step = (s1["events_delivered"] - s0["events_delivered"]) / max(fine_steps, 1)
     bstep = algorithmic_bytes_per_step(s1, ev_per_step)
-    steps_per_epoch = fine_steps / max(epochs, 1)
-    per_launch_bytes = bstep * steps_per_epoch
-    mean_launch_s = kern_ms * 1e-3 / max(epochs, 1)
+    steps_per_launch = fine_steps / max(n_launch, 1)
+    per_launch_bytes = bstep * steps_per_launch
+    mean_launch_s = kern_ms * 1e-3 / max(n_launch, 1)
     peak, peak_kind = measured_peak_hbm()
     achieved = per_launch_bytes / mean_launch_s / 1e9
     launches = s1["kernel_launches"] - s0["kernel_launches"]
@@ -272,16 +278,16 @@ def run_gpu_arm(args):
         "config": config_block(world, "256 MB buffer written between timed steps (flushes L2)"),
         "compartment_updates_per_s": 50000 * fine_steps / total,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic_per_launch(),
-                     "kernel": "k_epoch", "peak_kind": peak_kind,
+                     "frac": achieved / peak, "traffic": traffic_per_launch(steps_per_launch),
+                     "kernel": "k_batch", "peak_kind": peak_kind,
                      "bytes_per_launch": per_launch_bytes, "mean_launch_ms": mean_launch_s * 1e3,
-                     "steps_per_launch": steps_per_epoch},
+                     "steps_per_launch": steps_per_launch, "bytes_per_fine_step": bstep},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d / nsteps_e2e),
                 "d2h_bytes_per_step": int(d2h / nsteps_e2e)},
         "gpu_launches": int(launches),
         "clocks": clk,
-        "epoch_kernel_share": kern_ms * 1e-3 / total,
+        "batch_kernel_share": kern_ms * 1e-3 / total,
         "wall_ms_per_step": 1e3 * wall_total / args.steps,
     }
     print(json.dumps(line), flush=True)

@@ -1,0 +1,80 @@
+// drop_in_demo.cpp — the reference's own recipe builders through both
+// mcsim::Engine (the unmodified reference, oracle/_ref) and the drop-in
+// mcsim_gpu::Engine (integration/mcsim_gpu.hpp over libmcg.so); exits 0 iff
+// spike trains and sampled cell state are bitwise identical.
+//   drop_in_demo [consolidation|busyring] [t_ms]
+// Test infrastructure (tests/test_gpu_dropin.py); built by _build.py when the
+// reference headers are present.
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "mcsim/bench.hpp"
+#include "mcsim/network.hpp"
+#include "mcsim_gpu.hpp"
+
+template <class A, class B>
+static int compare(A& ref, B& gpu, const mcsim::Recipe& r, double t_ms) {
+  ref.advance_to(t_ms);
+  gpu.advance_to(t_ms);
+  const auto& s0 = ref.spikes();
+  const auto& s1 = gpu.spikes();
+  if (s0.size() != s1.size()) {
+    std::printf("FAIL spike count %zu vs %zu\n", s0.size(), s1.size());
+    return 1;
+  }
+  for (std::size_t i = 0; i < s0.size(); ++i)
+    if (s0[i].gid != s1[i].gid || std::memcmp(&s0[i].t_ms, &s1[i].t_ms, 8) != 0) {
+      std::printf("FAIL spike %zu: (%u, %.17g) vs (%u, %.17g)\n", i, s0[i].gid, s0[i].t_ms,
+                  s1[i].gid, s1[i].t_ms);
+      return 1;
+    }
+  const uint32_t n = static_cast<uint32_t>(r.cell_kind.size());
+  for (uint32_t gid = 0; gid < n; gid += (n > 16 ? n / 16 : 1)) {
+    const auto& a = ref.cell(gid);
+    const auto& b = gpu.cell(gid);
+    if (a.v_mV != b.v_mV || a.species != b.species) {
+      std::printf("FAIL cell %u membrane/species state\n", gid);
+      return 1;
+    }
+    for (std::size_t g = 0; g < a.groups.size(); ++g)
+      for (std::size_t i = 0; i < a.groups[g].stc.size(); ++i) {
+        const auto &x = a.groups[g].stc[i], &y = b.groups[g].stc[i];
+        if (std::memcmp(&x, &y, sizeof x) != 0) {
+          std::printf("FAIL cell %u group %zu STC instance %zu\n", gid, g, i);
+          return 1;
+        }
+      }
+  }
+  std::printf("OK %zu spikes identical, t = %.1f ms\n", s0.size(), t_ms);
+  return 0;
+}
+
+int main(int argc, char** argv) {
+  const std::string which = argc > 1 ? argv[1] : "consolidation";
+  const double t_ms = argc > 2 ? std::atof(argv[2]) : 2000.0;
+  try {
+    if (which == "busyring") {
+      mcsim::BusyringSpec spec = mcsim::default_busyring();
+      spec.n_cells = 256;
+      spec.ring_weight_uS = mcsim::calibrate_ring_weight(spec);
+      const mcsim::Recipe r = mcsim::build_busyring(spec);
+      const mcsim::EngineOptions opt{spec.dt_ms, spec.seed, 8};
+      mcsim::Engine ref(r, opt);
+      mcsim_gpu::Engine gpu(r, opt);
+      return compare(ref, gpu, r, t_ms);
+    }
+    mcsim::ConsolidationConfig cfg;
+    cfg.seed = 1;
+    cfg.multi_compartment = true;
+    const mcsim::ConsolidationBuild b = mcsim::build_consolidation_network(cfg, true);
+    const mcsim::EngineOptions opt{cfg.dt_ms, cfg.seed, 8};
+    mcsim::Engine ref(b.recipe, opt);
+    mcsim_gpu::Engine gpu(b.recipe, opt);
+    return compare(ref, gpu, b.recipe, t_ms);
+  } catch (const std::exception& e) {
+    std::printf("ERROR %s\n", e.what());
+    return 2;
+  }
+}

@@ -58,11 +58,35 @@ def build_oracle(verbose=False):
     return os.path.join(ROOT, "oracle", "_ref", "libmcsim_ref.so")
 
 
+def build_dropin(verbose=False):
+    """Build integration/_build/drop_in_demo (test infrastructure): the
+    reference's builders through mcsim::Engine and the drop-in mcsim_gpu::Engine.
+    Needs the reference headers (this container) and oracle/_ref."""
+    ref = os.environ.get("MCSIM_REF", "/root/reference/proj")
+    lib_ref = os.path.join(ROOT, "oracle", "_ref", "libmcsim_ref.so")
+    if not os.path.isdir(os.path.join(ref, "include")) or not os.path.exists(lib_ref):
+        return None
+    out_dir = os.path.join(ROOT, "integration", "_build")
+    os.makedirs(out_dir, exist_ok=True)
+    out = os.path.join(out_dir, "drop_in_demo")
+    cmd = ["g++", "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"),
+           "-I" + os.path.join(ROOT, "integration"), "-I" + os.path.join(ref, "include"),
+           os.path.join(ROOT, "integration", "drop_in_demo.cpp"),
+           "-L" + os.path.dirname(lib_ref), "-lmcsim_ref", "-L" + HERE, "-lmcg",
+           "-Wl,-rpath,$ORIGIN/../../oracle/_ref:$ORIGIN/../../paper_2411_16445_b200",
+           "-o", out]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    return out
+
+
 def main(argv):
     force = "--force" in argv
     print(build_engine(force=force, verbose=True))
     if "--no-oracle" not in argv:
         print(build_oracle(verbose=True))
+        print(build_dropin(verbose=True))
 
 
 if __name__ == "__main__":
