@@ -198,7 +198,7 @@ def run_gpu_arm(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if world > 1:
-        raise SystemExit("multi-GPU sharding is not wired into bench.py yet")
+        return run_gpu_arm_sharded(args, world, rank)
     torch.cuda.set_device(0)
     cfg = workload_config()
     b = N.build_consolidation_network(cfg, True)
@@ -291,6 +291,113 @@ def run_gpu_arm(args):
         "wall_ms_per_step": 1e3 * wall_total / args.steps,
     }
     print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_gpu_arm_sharded(args, world, rank):
+    """N > 1: cells of the same config-3 network partitioned over the ranks
+    (strong scaling), one min-delay epoch per launch, spikes exchanged by an
+    allgather after every epoch (paper_2411_16445_b200/shard.py).  Timed with
+    CUDA events around the whole step loop (exchange included), max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2411_16445_b200 import EngineOptions
+    from paper_2411_16445_b200 import network as N
+    from paper_2411_16445_b200 import shard
+
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    # MCG_EXCHANGE=gloo: host-staged exchange (lets several ranks share one GPU
+    # to exercise this path); default NCCL between the GPUs' device buffers
+    backend = os.environ.get("MCG_EXCHANGE", "nccl")
+    n_dev = torch.cuda.device_count()
+    device = local % max(n_dev, 1)
+    torch.cuda.set_device(device)
+    dist.init_process_group(backend, rank=rank, world_size=world)
+    b = N.build_consolidation_network(workload_config(), True, device=device)
+    flat = b.recipe.flatten()
+    opt = EngineOptions(DT_MS, SEED)
+
+    def make():
+        return shard.ShardedEngine(flat, opt, rank, world, device=device, backend=backend)
+
+    sh = make()
+    sh.engine.set_timing(True)
+    t = 0.0
+    for _ in range(args.warmup):
+        t += STEP_MS
+        sh.advance_to(t)
+    flush_l2()
+    s0 = sh.engine.stats()
+    clocks = ClockSampler(device) if rank == 0 else None
+    if clocks:
+        clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    ev0.record()
+    for _ in range(args.steps):
+        t += STEP_MS
+        sh.advance_to(t)
+    ev1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop() if clocks else None
+    s1 = sh.engine.stats()
+    el = torch.tensor([ev0.elapsed_time(ev1) * 1e-3], dtype=torch.float64,
+                      device="cuda" if backend == "nccl" else "cpu")
+    dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    total = float(el.item())
+    value = args.steps * STEP_MS * 1e-3 / total
+    fine_steps = s1["steps"] - s0["steps"]
+    n_launch = s1["epoch_kernel_launches"] - s0["epoch_kernel_launches"]
+    kern_ms = s1["epoch_kernel_ms"] - s0["epoch_kernel_ms"]
+    ev_per_step = (s1["events_delivered"] - s0["events_delivered"]) / max(fine_steps, 1)
+    bstep = algorithmic_bytes_per_step(s1, ev_per_step)  # this rank's share
+    steps_per_launch = fine_steps / max(n_launch, 1)
+    mean_launch_s = kern_ms * 1e-3 / max(n_launch, 1)
+    peak, peak_kind = measured_peak_hbm()
+    achieved = bstep * steps_per_launch / mean_launch_s / 1e9
+    # end to end through the public API: shard construction + W+K steps + spikes back
+    torch.cuda.synchronize()
+    dist.barrier()
+    a = time.perf_counter()
+    sh2 = make()
+    tt = 0.0
+    for _ in range(args.warmup + args.steps):
+        tt += STEP_MS
+        sh2.advance_to(tt)
+    st, sg = sh2.engine.spike_arrays()
+    e2e_wall = torch.tensor([time.perf_counter() - a], dtype=torch.float64,
+                            device="cuda" if backend == "nccl" else "cpu")
+    dist.all_reduce(e2e_wall, op=dist.ReduceOp.MAX)
+    nsteps_e2e = args.warmup + args.steps
+    e2e_val = nsteps_e2e * STEP_MS * 1e-3 / float(e2e_wall.item())
+    v = flat.view
+    h2d = v.n_connections * (1 + 4 + 4 + 4 + 1 + 8 + 8) + s1["total_synapses"] * 8 * 12 + s1["total_comps"] * 8 * 5
+    d2h = st.nbytes + sg.nbytes
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference's own recipe builder, seed 1)",
+            "config": config_block(world, "256 MB buffer written after warm-up (flushes L2)"),
+            "compartment_updates_per_s": 50000 * fine_steps / total,
+            "exchange": backend,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "kernel": "k_batch (rank 0)",
+                         "peak_kind": peak_kind, "bytes_per_launch": bstep * steps_per_launch,
+                         "mean_launch_ms": mean_launch_s * 1e3,
+                         "steps_per_launch": steps_per_launch},
+            "cpu_baseline": None,
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d / nsteps_e2e),
+                    "d2h_bytes_per_step": int(d2h / nsteps_e2e)},
+            "gpu_launches": int(s1["kernel_launches"] - s0["kernel_launches"]),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
     return 0
 
 

@@ -245,6 +245,32 @@ mcg_status mcg_read_state(mcg_engine* eng, int32_t field, uint32_t gid, int32_t 
 mcg_status mcg_write_state(mcg_engine* eng, int32_t field, uint32_t gid, int32_t index,
                            int64_t offset, int64_t count, const void* in);
 
+/* ---- sharded epoch loop (world > 1) ---------------------------------------
+ * The reference's epoch loop (engine.cpp:913-942) with cells partitioned over
+ * ranks (contiguous gid ranges balanced by compartments + synapses; each rank
+ * owns its cells and their incoming synapses).  Per epoch the caller runs
+ *   mcg_shard_run_epoch     expands the spikes in `recv` (all ranks' send
+ *                           blocks of the previous epoch) through this rank's
+ *                           incoming edges, steps one min-delay epoch towards
+ *                           t_ms, writes this rank's spikes into `send`
+ *   allgather(send -> recv) e.g. ncclAllGather / torch.distributed
+ * Blocks are int64[1 + 3*block_cap] = [count, (gid, step, t) x block_cap]
+ * (t: the interpolated spike time's IEEE bits; every rank can rebuild the
+ * global spike list, epoch by epoch, sorted by (gid, step)), the
+ * same block_cap on every rank (>= mcg_shard_spike_cap of every rank); `recv`
+ * holds `world` blocks in rank order and must be zero-initialised before the
+ * first epoch.  Both are device pointers; the engine synchronizes its stream
+ * before returning.  Replaces Impl::exchange (engine.cpp:875-889). */
+int64_t mcg_shard_spike_cap(const mcg_engine* eng);   /* max local spikes per epoch */
+uint32_t mcg_shard_gid_begin(const mcg_engine* eng);  /* local gid range [begin, end) */
+uint32_t mcg_shard_gid_end(const mcg_engine* eng);
+mcg_status mcg_shard_set_buffers(mcg_engine* eng, int64_t* send, int64_t* recv, int64_t block_cap,
+                                 int32_t world);
+mcg_status mcg_shard_run_epoch(mcg_engine* eng, double t_ms);
+/* the shard bounds mcg_create uses for (recipe, world): rank r owns gids
+ * [bounds[r], bounds[r+1]); bounds has world + 1 entries.  Host only (no GPU). */
+mcg_status mcg_partition(const mcg_recipe* recipe, int32_t world, uint32_t* bounds);
+
 /* ---- instrumentation (bench.py) -------------------------------------------- */
 
 typedef struct {

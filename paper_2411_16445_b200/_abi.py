@@ -125,7 +125,8 @@ EXPORTS = ("mcg_create", "mcg_destroy", "mcg_last_error", "mcg_abi_version", "mc
            "mcg_trace_len", "mcg_get_trace", "mcg_cell_ncomp", "mcg_cell_ngroups",
            "mcg_group_size", "mcg_cell_parent", "mcg_read_state", "mcg_write_state",
            "mcg_get_stats", "mcg_set_timing", "mcg_device_math",
-           "mcg_er_connect")
+           "mcg_er_connect", "mcg_shard_spike_cap", "mcg_shard_gid_begin", "mcg_shard_gid_end",
+           "mcg_shard_set_buffers", "mcg_shard_run_epoch", "mcg_partition")
 
 _lib = None
 
@@ -165,6 +166,12 @@ def _declare(L):
         "mcg_er_connect": (C.c_int32, [C.c_int32, C.c_uint64, C.c_uint32, C.c_double,
                                        C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p,
                                        P(C.c_int64)]),
+        "mcg_shard_spike_cap": (C.c_int64, [eng]),
+        "mcg_shard_gid_begin": (C.c_uint32, [eng]),
+        "mcg_shard_gid_end": (C.c_uint32, [eng]),
+        "mcg_shard_set_buffers": (C.c_int32, [eng, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32]),
+        "mcg_shard_run_epoch": (C.c_int32, [eng, C.c_double]),
+        "mcg_partition": (C.c_int32, [P(mcg_recipe), C.c_int32, C.c_void_p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

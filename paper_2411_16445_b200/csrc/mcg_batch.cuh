@@ -47,6 +47,8 @@ struct McgBatchArgs {
   unsigned long long* log_n;
   int4* chunks;            // (epoch, batch, offset, count)
   unsigned long long* chunk_n;
+  int64_t* x_send;         // sharded: this rank's spikes of the epoch [count, (gid, step, t) x cap]
+  int64_t x_cap;
 };
 
 // phase 1: sources of [s0, s1) + previous epoch's spikes (from the per-cell slots)
@@ -96,9 +98,23 @@ __device__ void mcg_expand(const McgEv& E, const McgDev& D, int32_t j, int64_t s
       }
     }
   }
-  // spikes of the previous epoch, one warp per spiking cell
+  // spikes of the previous epoch (engine.cpp:875-889: delivery at
+  // step + 1 + delay), one warp per spike / spiking cell, lanes over out-edges
   const int lane = threadIdx.x & 31;
   const int64_t nw = nthr >> 5;
+  if (E.x_recv != nullptr) {  // sharded: every rank's spikes, local out-edges only
+    for (int r = 0; r < E.x_world; ++r) {
+      const int64_t* blk = E.x_recv + r * E.x_block;
+      const int64_t n = blk[0];
+      for (int64_t w = tid >> 5; w < n; w += nw) {
+        const uint32_t gid = static_cast<uint32_t>(blk[1 + 3 * w]);
+        const int64_t st = blk[2 + 3 * w];
+        const int64_t e0 = E.out_begin[gid], e1 = E.out_end[gid];
+        for (int64_t q = e0 + lane; q < e1; q += 32) mcg_push(E, j, q, st + 1 + E.e_delay[q]);
+      }
+    }
+    return;
+  }
   for (int64_t c = tid >> 5; c < D.n_cells; c += nw) {
     const int k = D.sp_count[c];
     if (k == 0) continue;
@@ -1246,6 +1262,19 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
       }
     }
     D.sp_count[c] = k;
+    if (A.x_send != nullptr && k > 0) {  // sharded: publish for the caller's allgather
+      const int64_t pos = static_cast<int64_t>(
+          atomicAdd(reinterpret_cast<unsigned long long*>(A.x_send), static_cast<unsigned long long>(k)));
+      if (pos + k > A.x_cap) {
+        atomicOr(D.err, MCG_ERR_FLAG_SPIKES);
+      } else {
+        for (int i = 0; i < k; ++i) {
+          A.x_send[1 + 3 * (pos + i)] = int64_t(D.gid0) + c;
+          A.x_send[2 + 3 * (pos + i)] = D.sp_step[int64_t(c) * D.sp_cap + i];
+          A.x_send[3 + 3 * (pos + i)] = __double_as_longlong(D.sp_t[int64_t(c) * D.sp_cap + i]);
+        }
+      }
+    }
     D.pend_sel[c] = X.sel;
     D.pend_off[c] = X.cur;
     D.pend_n[c] = X.end;

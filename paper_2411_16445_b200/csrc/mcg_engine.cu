@@ -675,16 +675,34 @@ struct Engine {
   }
 
   // one persistent launch: up to kBatch epochs from `step` towards `target`
+  // sharded operation (world > 1): the caller's exchange buffers
+  int64_t* x_send = nullptr;
+  int64_t* x_recv = nullptr;
+  int64_t x_cap = 0;
+  int32_t x_world = 0;
+
+  int64_t shard_spike_cap() const { return int64_t(std::max(n_local(), 1)) * sp_cap; }
+
   void run_batch(int64_t target, int64_t call_first) {
     h_ctl[0] = step;
     h_ctl[1] = target;
     h_ctl[2] = L;
     h_ctl[3] = call_first;
     CK(cudaMemcpyAsync(d_ctl.p, h_ctl, 4 * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    const int64_t planned = std::min<int64_t>(kBatch, (target - step + L - 1) / L);
+    const bool sharded = x_send != nullptr;
+    // sharded: one epoch per launch, the exchange happens between launches
+    const int64_t planned = sharded ? 1 : std::min<int64_t>(kBatch, (target - step + L - 1) / L);
     refresh_dev();
     McgBatchArgs A{};
     A.E = ev_dev();
+    if (sharded) {
+      CK(cudaMemsetAsync(x_send, 0, sizeof(int64_t), st));
+      A.E.x_recv = x_recv;
+      A.E.x_world = x_world;
+      A.E.x_block = 1 + 3 * x_cap;
+      A.x_send = x_send;
+      A.x_cap = x_cap;
+    }
     A.n_epochs = static_cast<int32_t>(planned);
     A.cells_per_cta = bc_cells;
     A.n_batches = bc_batches;
@@ -789,7 +807,29 @@ struct Engine {
     }
   }
 
+  // one min-delay epoch towards t_ms (sharded epoch loop, engine.cpp:913-942):
+  // expands the imported spikes, steps the epoch, exports this rank's spikes
+  void run_epoch(double t_ms) {
+    if (x_send == nullptr) throw Error(MCG_ERR_ENGINE, "sharded engine: exchange buffers not set");
+    const int64_t target = ceil_steps(t_ms, m.dt);
+    if (step >= target) return;
+    const int64_t a = step, b = std::min<int64_t>(target, step + L);
+    probes_begin(a, b, false, 0);
+    refresh_dev();
+    CK(cudaEventRecord(eva, st));
+    while (step < b) run_batch(b, a);
+    CK(cudaEventRecord(evb, st));
+    CK(cudaEventSynchronize(evb));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, eva, evb));
+    stats.advance_ms += ms;
+    stats.advance_calls += 1;
+    probes_end(a, b, false, 0, 1);
+  }
+
   void advance_to(double t_ms) {
+    if (m.world > 1)
+      throw Error(MCG_ERR_ENGINE, "sharded engine: drive it with mcg_shard_run_epoch + an exchange");
     const int64_t target = ceil_steps(t_ms, m.dt);
     if (step >= target) return;
     const int64_t a = step;
@@ -1100,6 +1140,41 @@ mcg_status mcg_get_stats(mcg_engine* eng, mcg_stats* out) {
 }
 mcg_status mcg_set_timing(mcg_engine* eng, int32_t enabled) {
   return guarded([&] { eng->e.timing = enabled != 0; });
+}
+
+int64_t mcg_shard_spike_cap(const mcg_engine* eng) { return eng ? eng->e.shard_spike_cap() : 0; }
+
+uint32_t mcg_shard_gid_begin(const mcg_engine* eng) { return eng ? eng->e.m.gid_begin : 0; }
+
+uint32_t mcg_shard_gid_end(const mcg_engine* eng) { return eng ? eng->e.m.gid_end : 0; }
+
+mcg_status mcg_shard_set_buffers(mcg_engine* eng, int64_t* send, int64_t* recv, int64_t block_cap,
+                                 int32_t world) {
+  return guarded([&] {
+    if (!eng || !send || !recv || world < 1)
+      throw mcg::Error(MCG_ERR_ARGUMENT, "shard buffers: null pointer or world < 1");
+    mcg::Engine* E = &eng->e;
+    if (block_cap < E->shard_spike_cap())
+      throw mcg::Error(MCG_ERR_ARGUMENT, "shard buffers: block capacity below mcg_shard_spike_cap");
+    E->x_send = send;
+    E->x_recv = recv;
+    E->x_cap = block_cap;
+    E->x_world = world;
+  });
+}
+
+mcg_status mcg_partition(const mcg_recipe* recipe, int32_t world, uint32_t* bounds) {
+  return guarded([&] {
+    if (!recipe || !bounds || world < 1)
+      throw mcg::Error(MCG_ERR_ARGUMENT, "partition: null pointer or world < 1");
+    std::vector<uint32_t> b;
+    mcg::partition(*recipe, world, b);
+    std::copy(b.begin(), b.end(), bounds);
+  });
+}
+
+mcg_status mcg_shard_run_epoch(mcg_engine* eng, double t_ms) {
+  return guarded([&] { eng->e.run_epoch(t_ms); });
 }
 
 }  // extern "C"

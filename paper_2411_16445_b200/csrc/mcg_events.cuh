@@ -47,6 +47,12 @@ struct McgEv {
   int32_t* abort;
   uint64_t seed;
   double dt;
+  // sharded mode: the previous epoch's spikes of all ranks (the caller's
+  // allgather of every rank's send block), x_world blocks of x_block int64:
+  // [count, (gid, step, t bits) x cap]; nullptr on a single shard (local spikes)
+  const int64_t* x_recv;
+  int32_t x_world;
+  int64_t x_block;
 };
 
 // epoch j of the batch: [s0, s1); false if beyond the target

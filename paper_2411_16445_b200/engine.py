@@ -244,3 +244,18 @@ class Engine:
 
     def set_timing(self, enabled: bool):
         _check(A.lib().mcg_set_timing(self._h, 1 if enabled else 0))
+
+    # ---- sharded epoch loop (include/mcg.h; driven by shard.ShardedEngine) ----
+    def shard_spike_cap(self) -> int:
+        return int(A.lib().mcg_shard_spike_cap(self._h))
+
+    def gid_range(self) -> Tuple[int, int]:
+        L = A.lib()
+        return int(L.mcg_shard_gid_begin(self._h)), int(L.mcg_shard_gid_end(self._h))
+
+    def set_exchange_buffers(self, send_ptr: int, recv_ptr: int, block_cap: int, world: int):
+        _check(A.lib().mcg_shard_set_buffers(self._h, C.c_void_p(send_ptr), C.c_void_p(recv_ptr),
+                                             int(block_cap), int(world)))
+
+    def run_epoch(self, t_ms: float):
+        _check(A.lib().mcg_shard_run_epoch(self._h, float(t_ms)))
