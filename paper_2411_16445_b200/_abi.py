@@ -8,7 +8,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmcg.so")
+LIB_PATH = os.environ.get("MCG_LIB") or os.path.join(_HERE, "libmcg.so")
 
 # status codes
 MCG_OK = 0

@@ -27,8 +27,12 @@
 #include <cooperative_groups.h>
 
 #include "mcg_epoch.cuh"
+#include "mcg_sweep.cuh"
 
-#define MCG_NPHASE 16
+#define MCG_NPHASE 24
+#ifndef MCG_BATCH_THREADS
+#define MCG_BATCH_THREADS 512
+#endif
 
 struct McgBatchArgs {
   McgEv E;
@@ -41,6 +45,10 @@ struct McgBatchArgs {
   int32_t kind_doubles;    // shared memory for staged kind constants
   int32_t n_specs_sm;      // spec table staged in shared memory (0: read from global)
   int32_t stc_sm;          // STC instance state kept in shared memory (resident batches)
+  int32_t ch_stride;       // doubles per cell of chain-sweep scratch ((1 + sp_max) x P_max; 0: none)
+  int32_t ch_pmax;         // P_max = max over kinds of 2 ch_lp + 1
+  int32_t ev_cap;          // staged-delivery event buffer entries (0: off)
+  int32_t fmask_words;     // changed-flag words (fmask)
   unsigned long long* phase;  // optional per-phase cycle totals (MCG_NPHASE)
   double* log_t;           // spike log of the launch
   uint32_t* log_gid;
@@ -141,6 +149,26 @@ struct McgCellSm {
   uint64_t nk;              // next pending inbox key (~0 if none)
   unsigned long long ndel;
   double det_prev, prod;
+  // staged delivery (mcg_stage_events): the epoch's due events in shared memory
+  int32_t fast;             // cell eligible for staged delivery (static per launch)
+  int32_t staged;           // this epoch's events are staged
+  int32_t ev_cur, ev_end;   // network events [ev_cur, ev_end) of the event buffer
+  int32_t in_cur, in_end;   // delayed-calcium events [in_cur, in_end)
+  uint32_t iseq;            // internal_seq (engine.cpp:499), resident copy
+  int32_t pad2;
+  uint8_t gk[8];            // per group: synapse kind
+  int8_t gseg[8];           // per group: STC segment index (-1: none)
+};
+
+// one staged event (16 B): network events carry the weight (static charge:
+// weight x charge factor, the product apply_event forms) and the target
+// compartment; delayed-calcium events only their group and instance
+struct McgEvSm {
+  double w;
+  uint32_t inst;            // | 0x80000000 when the raw weight is nonzero
+  uint16_t comp;
+  uint8_t group;
+  uint8_t so;               // step - s0
 };
 
 // one STC group of a cell, in group order
@@ -149,6 +177,9 @@ struct McgSegSm {
   int32_t gi, size, spec, comp;
   int32_t start, pad;       // first instance's index within the cell's STC range
   double vol, rvol;         // volume of the placement's compartment, mcg_recip of it
+  double cf;                // charge factor of the placement's compartment
+  int64_t f_base, f_head, f_tail;  // delayed-calcium queue (McgFifo), resident copy
+  int32_t f_cap, fifo;
 };
 
 // per-kind constants the sweeps read every step, staged in shared memory once
@@ -163,8 +194,16 @@ struct McgKindSm {
   const int32_t* par;
 };
 
-__host__ __device__ __forceinline__ int mcg_kind_block_doubles(int n, int S) {
-  return (9 + 6 * S) * n + (n + 1) / 2 + 1;  // + one spare word (mcg_sweep_const_sm)
+// + one spare word (mcg_sweep_const_sm), then the chain section when the kind
+// has a chain schedule (lp > 0, P = 2 lp + 1 positions): the position -> node
+// list (int32) and, per system (V, then each species), f | coup | d | y in
+// position order (mcg_sweep.cuh)
+__host__ __device__ __forceinline__ int mcg_kind_block_doubles(int n, int S, int lp) {
+  const int P = 2 * lp + 1;
+  return (9 + 6 * S) * n + (n + 1) / 2 + 1 + (lp > 0 ? (P + 1) / 2 + 4 * (1 + S) * P : 0);
+}
+__host__ __device__ __forceinline__ int mcg_kind_chain_off(int n, int S) {  // doubles
+  return (9 + 6 * S) * n + (n + 1) / 2 + 1;
 }
 
 __device__ __forceinline__ McgKindSm mcg_kind_view(const double* p, int n, int S) {
@@ -202,6 +241,30 @@ __device__ __forceinline__ void mcg_kind_stage(const McgDev& D, const McgKind& K
   }
   int32_t* par = reinterpret_cast<int32_t*>(p + (9 + 6 * S) * n);
   for (int i = threadIdx.x; i < n; i += T) par[i] = D.k_parent[K.arr + i];
+  if (K.ch_lp > 0) {  // chain section (mcg_kind_block_doubles)
+    const int P = 2 * K.ch_lp + 1;
+    double* cb = p + mcg_kind_chain_off(n, S);
+    int32_t* idx = reinterpret_cast<int32_t*>(cb);
+    for (int i = threadIdx.x; i < P; i += T) idx[i] = D.k_ch_idx[K.ch_arr + i];
+    double* sysb = cb + (P + 1) / 2;
+    for (int i = threadIdx.x; i < (1 + S) * P; i += T) {
+      const int sy = i / P, pos = i - sy * P;
+      const int node = D.k_ch_idx[K.ch_arr + pos];
+      double f = -0.0, c = 0.0, d = 1.0, y = 1.0;  // padding: exact identities
+      if (node >= 0) {
+        const int64_t o = (sy == 0) ? K.arr + node : K.sp_arr + int64_t(sy - 1) * n + node;
+        f = (sy == 0) ? D.k_vf[o] : D.k_sp_f[o];
+        c = (sy == 0) ? D.k_axial[o] : D.k_sp_coupling[o];
+        d = (sy == 0) ? D.k_vd[o] : D.k_sp_d[o];
+        y = (sy == 0) ? D.k_vr[o] : D.k_sp_r[o];
+      }
+      double* q = sysb + sy * 4 * P;
+      q[pos] = f;
+      q[P + pos] = c;
+      q[2 * P + pos] = d;
+      q[3 * P + pos] = y;
+    }
+  }
 }
 
 __device__ __forceinline__ McgKindSm mcg_kind_consts(const McgDev& D, const McgKind& K,
@@ -443,6 +506,13 @@ __device__ __forceinline__ int64_t mcg_fifo_next(const McgDev& D, const McgKind&
   return nx;
 }
 
+// does system sys of a staged cell take the chain sweep this step
+__device__ __forceinline__ bool mcg_chain_ok(const McgKind& K, const McgCellSm& X, int sys, int m) {
+  if (K.ch_lp == 0 || K.n > m) return false;
+  if (sys == 0) return K.dyn == MCG_DYN_LIF && !X.refractory && !X.has_gsyn && K.v_const;
+  return sys - 1 < K.n_species && K.n > 1 && K.sp_const;
+}
+
 // shared-memory carve-up of one CTA (see k_batch)
 struct McgBatchSm {
   double* comp;     // C x comp_stride: V | SP | HM HH HN | gsyn gsyn_rhs rhs_cur diag | r2
@@ -456,7 +526,9 @@ struct McgBatchSm {
   McgSpec* spec;    // staged spec table (n_specs_sm entries)
   uint32_t* floc;   // stc_max: (cell << 16) | group of each STC instance slot
   uint32_t* fmask;  // stc_max / 32 changed-flag words
+  McgEvSm* evb;     // staged events (ev_cap entries)
   int ksm_o;        // offset of ksm in mcg_smem (doubles)
+  int chs_o;        // offset of the chain-sweep scratch (C x ch_stride doubles)
 };
 
 // the carve-up, derived from mcg_smem in every function that uses it (so the
@@ -468,7 +540,8 @@ __device__ __forceinline__ McgBatchSm mcg_batch_sm(const McgBatchArgs& A) {
   B.nbuf = B.comp + C * A.comp_stride;
   B.dbuf = B.nbuf + C * 32;
   B.stc = B.dbuf + A.stc_max;
-  B.ksm_o = C * A.comp_stride + C * 32 + A.stc_max + (A.stc_sm ? 4 * A.stc_max : 0);
+  B.chs_o = C * A.comp_stride + C * 32 + A.stc_max + (A.stc_sm ? 4 * A.stc_max : 0);
+  B.ksm_o = B.chs_o + C * A.ch_stride;
   B.ksm = mcg_smem + B.ksm_o;
   B.kc = reinterpret_cast<McgKind*>(B.ksm + A.kind_doubles);
   B.cs = reinterpret_cast<McgCellSm*>(B.kc + C);
@@ -476,6 +549,10 @@ __device__ __forceinline__ McgBatchSm mcg_batch_sm(const McgBatchArgs& A) {
   B.spec = reinterpret_cast<McgSpec*>(B.seg + C * A.n_stc_max);
   B.floc = reinterpret_cast<uint32_t*>(B.spec + A.n_specs_sm);
   B.fmask = B.floc + A.stc_max;
+  {
+    const uintptr_t e = reinterpret_cast<uintptr_t>(B.fmask + A.fmask_words);
+    B.evb = reinterpret_cast<McgEvSm*>((e + 15) & ~uintptr_t(15));
+  }
   return B;
 }
 
@@ -545,6 +622,182 @@ __device__ __forceinline__ void mcg_post_event_b(const McgDev& D, const McgBatch
   }
 }
 
+// staged delivery: queue metadata and internal_seq move between the global
+// arrays (authoritative while a cell is not staged) and the cell's shared
+// records (while it is)
+__device__ __forceinline__ void mcg_unstage(const McgDev& D, const McgBatchArgs& A,
+                                            const McgBatchSm& B, int k, int c) {
+  McgCellSm& X = B.cs[k];
+  for (int q = 0; q < X.n_stc_seg; ++q) {
+    const McgSegSm& g = B.seg[k * A.n_stc_max + q];
+    if (g.fifo < 0) continue;
+    D.fifos[g.fifo].head = g.f_head;
+    D.fifos[g.fifo].tail = g.f_tail;
+  }
+  D.internal_seq[c] = X.iseq;
+  X.staged = 0;
+}
+
+// The epoch's due events of cell k, staged by its warp at the epoch's start
+// (the reference's inbox and internal-heap pops of engine.cpp:549-560, with
+// every global lookup done here in parallel instead of on the delivery chain):
+// network events [cur, first step >= s1) of the sorted pending list with
+// their edge payload resolved, then the delayed-calcium entries due before s1
+// merged over the cell's STC groups in (step, seq) order (InternalOrder).
+// Returns false (cell delivered from global memory this epoch) if the event
+// buffer is full.
+__device__ bool mcg_stage_events(const McgDev& D, const McgBatchArgs& A, const McgBatchSm& B,
+                                 int k, int c, int64_t s0, int64_t s1, int lane, int* ev_top) {
+  McgCellSm& X = B.cs[k];
+  const McgKind& K = B.kc[k];
+  const uint64_t* pend = D.pend + (int64_t(c) * 2 + X.sel) * D.pend_cap;
+  const uint64_t lim = uint64_t(s1) << D.rank_bits;
+  int nd = 0;
+  for (int base = X.cur; base < X.end; base += 32) {
+    const int i = base + lane;
+    const unsigned bal = __ballot_sync(MCG_FULL, i < X.end && pend[i] < lim);
+    nd += __popc(bal);
+    if (bal != MCG_FULL) break;
+  }
+  if (!X.staged) {  // take the queue metadata over from global memory
+    __syncwarp();
+    if (lane == 0) {
+      for (int q = 0; q < X.n_stc_seg; ++q) {
+        McgSegSm& g = B.seg[k * A.n_stc_max + q];
+        if (g.fifo < 0) continue;
+        g.f_head = D.fifos[g.fifo].head;
+        g.f_tail = D.fifos[g.fifo].tail;
+      }
+      X.iseq = D.internal_seq[c];
+    }
+    __syncwarp();
+  }
+  // delayed-calcium entries due in the epoch, per STC segment
+  int ni = 0, nseg = 0;
+  for (int q = 0; q < X.n_stc_seg; ++q) {
+    const McgSegSm& g = B.seg[k * A.n_stc_max + q];
+    if (g.fifo < 0) continue;
+    int nq = 0;
+    for (int64_t base = g.f_head; base < g.f_tail; base += 32) {
+      const int64_t i = base + lane;
+      const bool due = i < g.f_tail && D.fifo_step[g.f_base + (i % g.f_cap)] < s1;
+      const unsigned bal = __ballot_sync(MCG_FULL, due);
+      nq += __popc(bal);
+      if (bal != MCG_FULL) break;
+    }
+    ni += nq;
+    nseg += nq > 0 ? 1 : 0;
+  }
+  int beg = 0;
+  if (lane == 0) beg = atomicAdd(ev_top, nd + ni);
+  beg = __shfl_sync(MCG_FULL, beg, 0);
+  if (beg + nd + ni > A.ev_cap) {
+    __syncwarp();
+    if (lane == 0) {
+      if (X.staged) mcg_unstage(D, A, B, k, c);
+      X.staged = 0;
+      X.fifo_next = mcg_fifo_next(D, K, D.cg_off[c]);
+      X.nk = (X.cur < X.end) ? pend[X.cur] : ~0ull;
+    }
+    __syncwarp();
+    return false;
+  }
+  const uint64_t rank_mask = (1ull << D.rank_bits) - 1;
+  const int64_t cg0 = D.cg_off[c];
+  for (int t = lane; t < nd; t += 32) {
+    const uint64_t key = pend[X.cur + t];
+    const int64_t r = int64_t(key & rank_mask);
+    const int grp = D.e_group[r];
+    const uint32_t inst = D.e_inst[r];
+    const double w = D.e_weight[r];
+    McgEvSm e;
+    e.group = static_cast<uint8_t>(grp);
+    e.so = static_cast<uint8_t>(int64_t(key >> D.rank_bits) - s0);
+    e.comp = 0;
+    e.w = w;
+    if (X.gk[grp] == MCG_SYN_STATIC_CHARGE) {  // apply_event: V[comp] += w * cf[comp]
+      const int comp = D.i_comp[D.cgs[cg0 + grp].inst + inst];
+      e.comp = static_cast<uint16_t>(comp);
+      e.w = w * D.k_cf[K.arr + comp];
+    }
+    e.inst = inst | (w != 0.0 ? 0x80000000u : 0u);
+    B.evb[beg + t] = e;
+  }
+  // delayed calcium: one segment's entries in queue order, or a merge by seq
+  int o = beg + nd;
+  for (int q = 0; q < X.n_stc_seg; ++q) {
+    McgSegSm& g = B.seg[k * A.n_stc_max + q];
+    if (g.fifo < 0) continue;
+    if (nseg <= 1) {
+      int nq = 0;
+      for (int64_t base = g.f_head; base < g.f_tail; base += 32) {
+        const int64_t i = base + lane;
+        const int64_t slot = g.f_base + (i % g.f_cap);
+        const bool due = i < g.f_tail && D.fifo_step[slot] < s1;
+        const unsigned bal = __ballot_sync(MCG_FULL, due);
+        if (due) {
+          McgEvSm e;
+          e.w = 0.0;
+          e.inst = uint32_t(D.fifo_si[slot] & 0xffffffffu);
+          e.comp = 0;
+          e.group = static_cast<uint8_t>(g.gi);
+          e.so = static_cast<uint8_t>(D.fifo_step[slot] - s0);
+          B.evb[o + nq + __popc(bal & mcg_lanemask_lt())] = e;
+        }
+        nq += __popc(bal);
+        if (bal != MCG_FULL) break;
+      }
+      o += nq;
+      __syncwarp();
+      if (lane == 0) g.f_head += nq;
+      __syncwarp();
+    }
+  }
+  if (nseg > 1 && lane == 0) {  // several groups due: pop in (step, seq) order
+    for (;;) {
+      int best = -1;
+      int64_t bst = 0;
+      uint64_t bseq = 0;
+      for (int q = 0; q < X.n_stc_seg; ++q) {
+        const McgSegSm& g = B.seg[k * A.n_stc_max + q];
+        if (g.fifo < 0 || g.f_head >= g.f_tail) continue;
+        const int64_t slot = g.f_base + (g.f_head % g.f_cap);
+        const int64_t st = D.fifo_step[slot];
+        if (st >= s1) continue;
+        const uint64_t seq = D.fifo_si[slot] >> 32;
+        if (best < 0 || st < bst || (st == bst && seq < bseq)) {
+          best = q;
+          bst = st;
+          bseq = seq;
+        }
+      }
+      if (best < 0) break;
+      McgSegSm& g = B.seg[k * A.n_stc_max + best];
+      const int64_t slot = g.f_base + (g.f_head % g.f_cap);
+      McgEvSm e;
+      e.w = 0.0;
+      e.inst = uint32_t(D.fifo_si[slot] & 0xffffffffu);
+      e.comp = 0;
+      e.group = static_cast<uint8_t>(g.gi);
+      e.so = static_cast<uint8_t>(bst - s0);
+      B.evb[o++] = e;
+      ++g.f_head;
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    X.ev_cur = beg;
+    X.ev_end = beg + nd;
+    X.in_cur = beg + nd;
+    X.in_end = beg + nd + ni;
+    X.cur += nd;
+    X.nk = (X.cur < X.end) ? pend[X.cur] : ~0ull;
+    X.staged = 1;
+  }
+  __syncwarp();
+  return true;
+}
+
 // ---- staging: metadata, kind constants, compartment state of batch b
 __device__ void mcg_batch_enter(const McgDev& D, const McgBatchArgs& A, int32_t b) {
   const McgBatchSm B = mcg_batch_sm(A);
@@ -588,10 +841,36 @@ __device__ void mcg_batch_enter(const McgDev& D, const McgBatchArgs& A, int32_t 
       g.start = tot;
       g.vol = D.k_volume[K.arr + S.comp];
       g.rvol = D.k_rvol[K.arr + S.comp];
+      g.cf = D.k_cf[K.arr + S.comp];
+      g.fifo = G.fifo;
+      if (G.fifo >= 0) {
+        g.f_base = D.fifos[G.fifo].base;
+        g.f_cap = D.fifos[G.fifo].cap;
+      }
       tot += G.size;
       ++ns;
     }
     X.has_act = act;
+    // staged delivery: static-charge and STC groups only, every STC group's
+    // calcium delay at least an epoch (its queue entries due in an epoch exist
+    // at the epoch's start), step offsets within an epoch fit a byte
+    {
+      int fast = (A.ev_cap > 0 && K.n <= m && K.n_groups <= 8 && D.ctl[2] <= 255) ? 1 : 0;
+      for (int gi = 0; fast && gi < K.n_groups; ++gi) {
+        const McgSpec& S = D.specs[D.cgs[cg0 + gi].spec];
+        X.gk[gi] = static_cast<uint8_t>(S.kind);
+        X.gseg[gi] = -1;
+        if (S.kind == MCG_SYN_STC_CHARGE) {
+          for (int q = 0; q < ns; ++q)
+            if (B.seg[tid * A.n_stc_max + q].gi == gi) X.gseg[gi] = static_cast<int8_t>(q);
+          if (X.gseg[gi] < 0 || S.ca_delay < D.ctl[2] || D.cgs[cg0 + gi].fifo < 0) fast = 0;
+        } else if (S.kind != MCG_SYN_STATIC_CHARGE) {
+          fast = 0;
+        }
+      }
+      X.fast = fast;
+      X.staged = 0;
+    }
     X.n_stc_seg = ns;
     X.stc_n = tot;
     X.hh_n = (K.dyn == MCG_DYN_HH) ? K.n : 0;
@@ -615,7 +894,7 @@ __device__ void mcg_batch_enter(const McgDev& D, const McgBatchArgs& A, int32_t 
           }
         if (B.cs[k].kb < 0) {
           B.cs[k].kb = kacc;
-          kacc += mcg_kind_block_doubles(B.kc[k].n, B.kc[k].n_species);
+          kacc += mcg_kind_block_doubles(B.kc[k].n, B.kc[k].n_species, B.kc[k].ch_lp);
         }
       }
     }
@@ -714,6 +993,7 @@ __device__ void mcg_batch_exit(const McgDev& D, const McgBatchArgs& A, int32_t b
   if (tid < nc) {
     const int c = c0 + tid;
     McgCellSm& X = B.cs[tid];
+    if (X.staged) mcg_unstage(D, A, B, tid, c);
     if (X.ndel) atomicAdd(D.delivered, X.ndel);
     X.ndel = 0;
     D.refr_until[c] = X.refr;
@@ -721,6 +1001,170 @@ __device__ void mcg_batch_exit(const McgDev& D, const McgBatchArgs& A, int32_t b
     D.armed[c] = X.armed;
   }
   __syncthreads();
+}
+
+// ---- E2: membrane and species systems of batch b (one step); out of line so
+// its register allocation does not compete with the rest of the step loop
+__device__ __noinline__ void mcg_ph_solve(const McgDev& D, const McgBatchArgs& A, int32_t b) {
+  const McgBatchSm B = mcg_batch_sm(A);
+  const int tid = threadIdx.x, T = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = T >> 5;
+  const int c0 = b * A.cells_per_cta;
+  const int nc = min(A.cells_per_cta, D.n_cells - c0);
+  const int S1 = 1 + D.sp_max;
+  const int m = D.smem_n;
+  McgCellSm* cs = B.cs;
+  const McgKind* kc = B.kc;
+  // ---- E2a. chain-scheduled constant systems (mcg_sweep.cuh): pass 1, the
+  // pre-elimination r2 of every position, warp per cell, lanes over
+  // (system, position)
+  if (A.ch_stride > 0) {
+    for (int k = warp; k < nc; k += nwarps) {
+      const McgKind& K = kc[k];
+      if (K.ch_lp == 0 || K.n > m) continue;
+      const McgCellSm& X = cs[k];
+      const int n = K.n, P = 2 * K.ch_lp + 1;
+      const McgKindOff KO = mcg_kind_off(B.ksm_o + X.kb, n, K.n_species);
+      const int32_t* PI = reinterpret_cast<const int32_t*>(mcg_smem);
+      const int ixo = 2 * (B.ksm_o + X.kb + mcg_kind_chain_off(n, K.n_species));
+      const int bo = k * A.comp_stride;
+      const bool hc = X.has_current;
+      for (int u = lane; u < S1 * P; u += 32) {
+        const int sys = u / P, pos = u - sys * P;
+        if (!mcg_chain_ok(K, X, sys, m)) continue;
+        const int node = PI[ixo + pos];
+        double r = 0.0;
+        if (node >= 0) {
+          const double* S = mcg_smem;
+          if (sys == 0) {
+            const double rhs = S[KO.glr + node] + 0.0 + (hc ? S[bo + (6 + D.sp_max) * m + node] : 0.0);
+            r = S[KO.cap + node] * S[bo + node] + rhs;
+          } else {
+            const int q = sys - 1;
+            const bool pc = q == K.prp_idx && X.prod != 0.0 && node == K.prp_comp;
+            r = S[KO.sp_cap + q * n + node] * S[bo + m + q * n + node] + (pc ? X.prod : 0.0);
+          }
+        }
+        mcg_smem[B.chs_o + k * A.ch_stride + sys * A.ch_pmax + pos] = r;
+      }
+    }
+    MCG_PH(21);
+    __syncthreads();
+    MCG_PH(18);
+  }
+  // ---- E2b. pass 2, one lane per (cell, system, chain) on threads [0, 256),
+  // beside the other systems (thread per (cell, system)) on [256, T)
+  const int nch = (A.ch_stride > 0) ? ((2 * S1 * nc + 31) & ~31) : 0;
+  const int split = nch > 0 ? min(256, T / 2) : 0;
+  if (tid < split) {
+    for (int t = tid; t < nch; t += split) {
+      const int k = t / (2 * S1), rem = t - k * 2 * S1;
+      McgChainLane L{};
+      if (k < nc) {
+        const McgKind& K = kc[k];
+        const McgCellSm& X = cs[k];
+        const int sys = rem >> 1;
+        L.on = mcg_chain_ok(K, X, sys, m) ? 1 : 0;
+        if (L.on) {
+          const int n = K.n, P = 2 * K.ch_lp + 1;
+          const int cho = B.ksm_o + X.kb + mcg_kind_chain_off(n, K.n_species);
+          L.side = rem & 1;
+          L.lp = K.ch_lp;
+          L.r2c = B.chs_o + k * A.ch_stride + sys * A.ch_pmax;
+          L.idx = 2 * cho;
+          L.fc = cho + (P + 1) / 2 + sys * 4 * P;
+          L.x = k * A.comp_stride + (sys == 0 ? 0 : m + (sys - 1) * n);
+          L.a_first = K.ch_afirst;
+        }
+      }
+      MCG_PH(19);
+      mcg_chain_lane(L);
+      MCG_PH(20);
+    }
+  } else
+  for (int t = tid - split; t < nc * S1; t += T - split) {
+    const int k = t / S1, sys = t - k * S1;
+    const int c = c0 + k;
+    const McgCellSm& X = cs[k];
+    const McgKind& K = kc[k];
+    if (mcg_chain_ok(K, X, sys, m)) continue;
+    const int n = K.n;
+    const bool in_sm = n <= m;
+    const McgCellMem M = mcg_cell_mem(D, K, c, in_sm ? mcg_comp_block(A, B, k) : nullptr);
+    const McgKindSm KS = mcg_kind_consts(D, K, B.ksm, X.kb);
+    const bool refractory = X.refractory;
+    const bool hg = X.has_gsyn, hc = X.has_current;
+    const int q = sys - 1;
+    // constant-diagonal systems (LIF-cable V without conductances, species)
+    // share one instruction stream across all cells and systems
+    const bool v_sys = sys == 0 && K.dyn == MCG_DYN_LIF && !refractory && !hg && K.v_const;
+    const bool s_sys = sys > 0 && q < K.n_species && n > 1 && K.sp_const;
+    bool ok = true;
+    if ((v_sys || s_sys) && in_sm) {
+      const McgKindOff KO = mcg_kind_off(B.ksm_o + X.kb, n, K.n_species);
+      const int bo = k * A.comp_stride, r2o = bo + (8 + D.sp_max) * m;
+      // one call for V and species (operands selected first), so lanes with
+      // different systems run the sweep in lockstep instead of serialized
+      const int qn = v_sys ? 0 : q * n;
+      const int x = v_sys ? bo : bo + m + qn, r2 = v_sys ? r2o : r2o + n + qn;
+      // right-hand side (engine.cpp:683 / 746-748):
+      //   V:       r2 = cap*v + (g_leak_rhs + 0.0 + (has_current ? rhs_cur : 0.0))
+      //   species: r2 = cap*c + (prod at the synthesis compartment, else 0.0)
+      const int pc = (!v_sys && q == K.prp_idx && X.prod != 0.0) ? K.prp_comp : -1;
+      mcg_rhs_sm(n, v_sys ? KO.cap : KO.sp_cap + qn, x, r2, v_sys, KO.glr,
+                 hc ? bo + (6 + D.sp_max) * m : -1, pc, X.prod);
+      mcg_sweep_const_sm(n, KO.par, (v_sys ? KO.ax : KO.sp_coup) + qn,
+                         (v_sys ? KO.vf : KO.sp_f) + qn, (v_sys ? KO.vd : KO.sp_d) + qn,
+                         (v_sys ? KO.vr : KO.sp_r) + qn, x, r2);
+    } else if (v_sys || s_sys) {
+      double* x = v_sys ? M.V : M.SP + int64_t(q) * n;
+      const int qq = v_sys ? 0 : q;
+      const double* coup = v_sys ? KS.ax : KS.sp_coup + qq * n;
+      const double* f = v_sys ? KS.vf : KS.sp_f + qq * n;
+      const double* d = v_sys ? KS.vd : KS.sp_d + qq * n;
+      const double* y = v_sys ? KS.vr : KS.sp_r + qq * n;
+      double* r2 = M.r2 + int64_t(v_sys ? 0 : 1 + q) * n;
+      {
+        const double* cap = v_sys ? KS.cap : KS.sp_cap + qq * n;
+        const int pc = (!v_sys && q == K.prp_idx && X.prod != 0.0) ? K.prp_comp : -1;
+        for (int i = 0; i < n; ++i) {
+          const double rhs = v_sys ? (KS.glr[i] + 0.0 + (hc ? M.rhs_cur[i] : 0.0))
+                                   : (i == pc ? X.prod : 0.0);
+          r2[i] = cap[i] * x[i] + rhs;
+        }
+      }
+      mcg_sweep_const(n, KS.par, coup, f, d, y, x, r2);
+    } else if (sys == 0) {
+      if (K.dyn == MCG_DYN_LIF_EXACT) {
+        if (!refractory) {
+          const double vinf = K.v_rev + K.r_mem * M.rhs_cur[0];
+          M.V[0] = vinf + (M.V[0] - vinf) * K.lif_exact_f;
+        }
+      } else if (K.dyn == MCG_DYN_LIF && !refractory) {
+        for (int i = 0; i < n; ++i) {
+          const double gs = KS.gl[i] + (hg ? M.gsyn[i] : 0.0);
+          const double rr = KS.glr[i] + (hg ? M.gsyn_rhs[i] : 0.0) + (hc ? M.rhs_cur[i] : 0.0);
+          M.gsyn[i] = gs;
+          M.gsyn_rhs[i] = rr;
+        }
+        ok = mcg_solve_tree(n, KS.par, KS.cap, M.gsyn, KS.ax, M.gsyn_rhs, M.V, M.diag, M.r2);
+      } else if (K.dyn == MCG_DYN_HH) {
+        ok = mcg_solve_tree(n, KS.par, KS.cap, M.gsyn, KS.ax, M.gsyn_rhs, M.V, M.diag, M.r2);
+      }
+      // singular species systems need the full solver's scratch: run them
+      // here, after V, in species order (never happens for valid recipes)
+      if (n > 1 && !K.sp_const)
+        for (int p = 0; p < K.n_species; ++p)
+          ok &= mcg_species_sys(n, p == K.prp_idx, K.prp_comp, X.prod, KS.sp_cap + p * n,
+                                KS.sp_gs + p * n, KS.sp_coup + p * n, KS.par,
+                                M.SP + int64_t(p) * n, M.r2 + int64_t(1 + p) * n, M.diag,
+                                D.s_rhs + D.comp_off[c]);
+    } else if (q < K.n_species && n == 1) {
+      mcg_species_sys(1, q == K.prp_idx, K.prp_comp, X.prod, KS.sp_cap + q, KS.sp_gs + q,
+                      KS.sp_coup + q, KS.par, M.SP + q, M.r2, M.diag, M.rhs_cur);
+    }
+    if (!ok) atomicOr(D.err, MCG_ERR_FLAG_SINGULAR);
+  }
 }
 
 // ---- one epoch [s0, s1) of the staged batch b
@@ -738,7 +1182,11 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
   const McgKind* kc = B.kc;
   const McgSpec* specs = A.n_specs_sm > 0 ? B.spec : D.specs;
 
-  // inbox merge, warp per cell (the reference's per-epoch inbox sort)
+  // inbox merge, warp per cell (the reference's per-epoch inbox sort), and
+  // the staging of the epoch's due events
+  __shared__ int s_ev_top;
+  if (tid == 0) s_ev_top = 0;
+  __syncthreads();
   for (int k = warp; k < nc; k += nwarps) {
     const int c = c0 + k;
     const int nin = D.inc_n[c];
@@ -761,8 +1209,9 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
       }
       __syncwarp();
     }
+    if (X.fast) mcg_stage_events(D, A, B, k, c, s0, s1, lane, &s_ev_top);
     if (lane == 0) {
-      X.nk = (X.cur < X.end) ? D.pend[(int64_t(c) * 2 + X.sel) * D.pend_cap + X.cur] : ~0ull;
+      if (!X.fast) X.nk = (X.cur < X.end) ? D.pend[(int64_t(c) * 2 + X.sel) * D.pend_cap + X.cur] : ~0ull;
       X.nsp = 0;
     }
   }
@@ -809,51 +1258,92 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
       X.refractory = refractory;
       double* V = (K.n <= m) ? mcg_comp_block(A, B, tid) : D.v + D.comp_off[c];
       const int64_t cg0 = D.cg_off[c];
-      uint64_t key = X.nk;
-      if (int64_t(key >> D.rank_bits) <= s) {
-        const uint64_t* pend = D.pend + (int64_t(c) * 2 + X.sel) * D.pend_cap;
-        int cur = X.cur;
-        while (int64_t(key >> D.rank_bits) <= s) {
-          const int64_t r = int64_t(key & rank_mask);
-          const int32_t grp = D.e_group[r];
-          mcg_apply_event(D, K, c, cg0, V, grp, D.e_inst[r], D.e_weight[r], 0, refractory, s,
-                          mcg_stc_ref(A, B, tid, grp));
-          ++cur;
+      if (X.staged) {
+        // staged delivery (mcg_stage_events): network events, then delayed calcium
+        const int S4 = A.stc_max;
+        int e = X.ev_cur;
+        while (e < X.ev_end && int(B.evb[e].so) == int(so)) {
+          const McgEvSm E = B.evb[e];
+          const uint32_t inst = E.inst & 0x7fffffffu;
+          if (X.gk[E.group] == MCG_SYN_STATIC_CHARGE) {
+            if (!refractory && (E.inst >> 31)) V[E.comp] += E.w;  // w * cf[comp]
+          } else {  // stc_charge, engine.cpp:493-510
+            McgSegSm& g = B.seg[tid * A.n_stc_max + X.gseg[E.group]];
+            const McgSpec& S = specs[g.spec];
+            if (g.f_tail - g.f_head >= g.f_cap) {
+              atomicOr(D.err, MCG_ERR_FLAG_FIFO);
+            } else {
+              const int64_t slot = g.f_base + (g.f_tail % g.f_cap);
+              D.fifo_step[slot] = s + S.ca_delay;
+              D.fifo_si[slot] = (uint64_t(X.iseq) << 32) | uint64_t(inst);
+              ++g.f_tail;
+            }
+            ++X.iseq;
+            if (!refractory) {
+              const int sl = X.stc_off + g.start + int(inst);
+              const double tw = B.stc[sl] + S.h0 * B.stc[S4 + sl];
+              V[g.comp] += tw * E.w * g.cf;
+            }
+          }
+          ++e;
           ++X.ndel;
-          key = (cur < X.end) ? pend[cur] : ~0ull;
         }
-        X.cur = cur;
-        X.nk = key;
-        // STC events queue delayed calcium (apply_event, engine.cpp:497-503)
-        if (K.n_stc_groups > 0) X.fifo_next = mcg_fifo_next(D, K, cg0);
-      }
-      if (X.fifo_next <= s) {
-        for (;;) {
-          int best = -1;
-          uint64_t bseq = ~0ull;
-          for (int gi = 0; gi < K.n_groups; ++gi) {
-            const McgCellGroup& G = D.cgs[cg0 + gi];
-            if (G.fifo < 0) continue;
-            const McgFifo& F = D.fifos[G.fifo];
-            if (F.head < F.tail) {
-              const int64_t slot = F.base + (F.head % F.cap);
-              if (D.fifo_step[slot] <= s) {
-                const uint64_t seq = D.fifo_si[slot] >> 32;
-                if (seq < bseq) {
-                  bseq = seq;
-                  best = gi;
+        X.ev_cur = e;
+        int q = X.in_cur;
+        while (q < X.in_end && int(B.evb[q].so) == int(so)) {
+          const McgEvSm E = B.evb[q];
+          const McgSegSm& g = B.seg[tid * A.n_stc_max + X.gseg[E.group]];
+          B.stc[2 * S4 + X.stc_off + g.start + int(E.inst)] += specs[g.spec].cpre_s;
+          ++q;
+        }
+        X.in_cur = q;
+      } else {
+        uint64_t key = X.nk;
+        if (int64_t(key >> D.rank_bits) <= s) {
+          const uint64_t* pend = D.pend + (int64_t(c) * 2 + X.sel) * D.pend_cap;
+          int cur = X.cur;
+          while (int64_t(key >> D.rank_bits) <= s) {
+            const int64_t r = int64_t(key & rank_mask);
+            const int32_t grp = D.e_group[r];
+            mcg_apply_event(D, K, c, cg0, V, grp, D.e_inst[r], D.e_weight[r], 0, refractory, s,
+                            mcg_stc_ref(A, B, tid, grp));
+            ++cur;
+            ++X.ndel;
+            key = (cur < X.end) ? pend[cur] : ~0ull;
+          }
+          X.cur = cur;
+          X.nk = key;
+          // STC events queue delayed calcium (apply_event, engine.cpp:497-503)
+          if (K.n_stc_groups > 0) X.fifo_next = mcg_fifo_next(D, K, cg0);
+        }
+        if (X.fifo_next <= s) {
+          for (;;) {
+            int best = -1;
+            uint64_t bseq = ~0ull;
+            for (int gi = 0; gi < K.n_groups; ++gi) {
+              const McgCellGroup& G = D.cgs[cg0 + gi];
+              if (G.fifo < 0) continue;
+              const McgFifo& F = D.fifos[G.fifo];
+              if (F.head < F.tail) {
+                const int64_t slot = F.base + (F.head % F.cap);
+                if (D.fifo_step[slot] <= s) {
+                  const uint64_t seq = D.fifo_si[slot] >> 32;
+                  if (seq < bseq) {
+                    bseq = seq;
+                    best = gi;
+                  }
                 }
               }
             }
+            if (best < 0) break;
+            McgFifo& F = D.fifos[D.cgs[cg0 + best].fifo];
+            const uint64_t si = D.fifo_si[F.base + (F.head % F.cap)];
+            ++F.head;
+            mcg_apply_event(D, K, c, cg0, V, best, uint32_t(si & 0xffffffffu), 0.0, 1,
+                            refractory, s, mcg_stc_ref(A, B, tid, best));
           }
-          if (best < 0) break;
-          McgFifo& F = D.fifos[D.cgs[cg0 + best].fifo];
-          const uint64_t si = D.fifo_si[F.base + (F.head % F.cap)];
-          ++F.head;
-          mcg_apply_event(D, K, c, cg0, V, best, uint32_t(si & 0xffffffffu), 0.0, 1,
-                          refractory, s, mcg_stc_ref(A, B, tid, best));
+          X.fifo_next = mcg_fifo_next(D, K, cg0);
         }
-        X.fifo_next = mcg_fifo_next(D, K, cg0);
       }
       X.has_gsyn = 0;
       X.has_current = 0;
@@ -861,6 +1351,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
       const int nr = K.n > 1 ? K.n : 1;
       for (int i = 0; i < nr; ++i) rc[i] = 0.0;
     }
+    MCG_PH(15);
     __syncthreads();
     MCG_PH(1);
 
@@ -934,7 +1425,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
       McgStcVal v[4];
       int64_t jj[4];
       uint32_t loc[4];
-#pragma unroll
+  #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int f = (r0 + u) * T + tid;
         jj[u] = -1;
@@ -949,7 +1440,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
           v[u].a = D.i_sps_abs[jj[u]];
         }
       }
-#pragma unroll
+  #pragma unroll
       for (int u = 0; u < 4; ++u) {
         if (r0 + u >= stc_rounds) break;
         const int f = (r0 + u) * T + tid;
@@ -976,6 +1467,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
         if (lane == 0) B.fmask[((r0 + u) * T + (tid - lane)) >> 5] = bal;
       }
     }
+    MCG_PH(16);
     __syncthreads();
     MCG_PH(2);
 
@@ -1005,14 +1497,14 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
             while (bits) {
               double dv[8];
               int cnt = 0;
-#pragma unroll
+  #pragma unroll
               for (int u = 0; u < 8; ++u)
                 if (bits) {
                   dv[u] = B.dbuf[f + __ffs(bits) - 1];
                   bits &= bits - 1;
                   cnt = u + 1;
                 }
-#pragma unroll
+  #pragma unroll
               for (int u = 0; u < 8; ++u)
                 if (u < cnt) acc += dv[u];
             }
@@ -1034,6 +1526,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
         X.has_current = 1;
       }
     }
+    MCG_PH(17);
     __syncthreads();
     MCG_PH(3);
 
@@ -1079,90 +1572,8 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
       MCG_PH(4);
     }
 
-
-    // ---- E2b. membrane and species systems: thread per (cell, system)
-    for (int t = tid; t < nc * S1; t += T) {
-      const int k = t / S1, sys = t - k * S1;
-      const int c = c0 + k;
-      const McgCellSm& X = cs[k];
-      const McgKind& K = kc[k];
-      const int n = K.n;
-      const bool in_sm = n <= m;
-      const McgCellMem M = mcg_cell_mem(D, K, c, in_sm ? mcg_comp_block(A, B, k) : nullptr);
-      const McgKindSm KS = mcg_kind_consts(D, K, B.ksm, X.kb);
-      const bool refractory = X.refractory;
-      const bool hg = X.has_gsyn, hc = X.has_current;
-      const int q = sys - 1;
-      // constant-diagonal systems (LIF-cable V without conductances, species)
-      // share one instruction stream across all cells and systems
-      const bool v_sys = sys == 0 && K.dyn == MCG_DYN_LIF && !refractory && !hg && K.v_const;
-      const bool s_sys = sys > 0 && q < K.n_species && n > 1 && K.sp_const;
-      bool ok = true;
-      if ((v_sys || s_sys) && in_sm) {
-        const McgKindOff KO = mcg_kind_off(B.ksm_o + X.kb, n, K.n_species);
-        const int bo = k * A.comp_stride, r2o = bo + (8 + D.sp_max) * m;
-        // one call for V and species (operands selected first), so lanes with
-        // different systems run the sweep in lockstep instead of serialized
-        const int qn = v_sys ? 0 : q * n;
-        const int x = v_sys ? bo : bo + m + qn, r2 = v_sys ? r2o : r2o + n + qn;
-        // right-hand side (engine.cpp:683 / 746-748):
-        //   V:       r2 = cap*v + (g_leak_rhs + 0.0 + (has_current ? rhs_cur : 0.0))
-        //   species: r2 = cap*c + (prod at the synthesis compartment, else 0.0)
-        const int pc = (!v_sys && q == K.prp_idx && X.prod != 0.0) ? K.prp_comp : -1;
-        mcg_rhs_sm(n, v_sys ? KO.cap : KO.sp_cap + qn, x, r2, v_sys, KO.glr,
-                   hc ? bo + (6 + D.sp_max) * m : -1, pc, X.prod);
-        mcg_sweep_const_sm(n, KO.par, (v_sys ? KO.ax : KO.sp_coup) + qn,
-                           (v_sys ? KO.vf : KO.sp_f) + qn, (v_sys ? KO.vd : KO.sp_d) + qn,
-                           (v_sys ? KO.vr : KO.sp_r) + qn, x, r2);
-      } else if (v_sys || s_sys) {
-        double* x = v_sys ? M.V : M.SP + int64_t(q) * n;
-        const int qq = v_sys ? 0 : q;
-        const double* coup = v_sys ? KS.ax : KS.sp_coup + qq * n;
-        const double* f = v_sys ? KS.vf : KS.sp_f + qq * n;
-        const double* d = v_sys ? KS.vd : KS.sp_d + qq * n;
-        const double* y = v_sys ? KS.vr : KS.sp_r + qq * n;
-        double* r2 = M.r2 + int64_t(v_sys ? 0 : 1 + q) * n;
-        {
-          const double* cap = v_sys ? KS.cap : KS.sp_cap + qq * n;
-          const int pc = (!v_sys && q == K.prp_idx && X.prod != 0.0) ? K.prp_comp : -1;
-          for (int i = 0; i < n; ++i) {
-            const double rhs = v_sys ? (KS.glr[i] + 0.0 + (hc ? M.rhs_cur[i] : 0.0))
-                                     : (i == pc ? X.prod : 0.0);
-            r2[i] = cap[i] * x[i] + rhs;
-          }
-        }
-        mcg_sweep_const(n, KS.par, coup, f, d, y, x, r2);
-      } else if (sys == 0) {
-        if (K.dyn == MCG_DYN_LIF_EXACT) {
-          if (!refractory) {
-            const double vinf = K.v_rev + K.r_mem * M.rhs_cur[0];
-            M.V[0] = vinf + (M.V[0] - vinf) * K.lif_exact_f;
-          }
-        } else if (K.dyn == MCG_DYN_LIF && !refractory) {
-          for (int i = 0; i < n; ++i) {
-            const double gs = KS.gl[i] + (hg ? M.gsyn[i] : 0.0);
-            const double rr = KS.glr[i] + (hg ? M.gsyn_rhs[i] : 0.0) + (hc ? M.rhs_cur[i] : 0.0);
-            M.gsyn[i] = gs;
-            M.gsyn_rhs[i] = rr;
-          }
-          ok = mcg_solve_tree(n, KS.par, KS.cap, M.gsyn, KS.ax, M.gsyn_rhs, M.V, M.diag, M.r2);
-        } else if (K.dyn == MCG_DYN_HH) {
-          ok = mcg_solve_tree(n, KS.par, KS.cap, M.gsyn, KS.ax, M.gsyn_rhs, M.V, M.diag, M.r2);
-        }
-        // singular species systems need the full solver's scratch: run them
-        // here, after V, in species order (never happens for valid recipes)
-        if (n > 1 && !K.sp_const)
-          for (int p = 0; p < K.n_species; ++p)
-            ok &= mcg_species_sys(n, p == K.prp_idx, K.prp_comp, X.prod, KS.sp_cap + p * n,
-                                  KS.sp_gs + p * n, KS.sp_coup + p * n, KS.par,
-                                  M.SP + int64_t(p) * n, M.r2 + int64_t(1 + p) * n, M.diag,
-                                  D.s_rhs + D.comp_off[c]);
-      } else if (q < K.n_species && n == 1) {
-        mcg_species_sys(1, q == K.prp_idx, K.prp_comp, X.prod, KS.sp_cap + q, KS.sp_gs + q,
-                        KS.sp_coup + q, KS.par, M.SP + q, M.r2, M.diag, M.rhs_cur);
-      }
-      if (!ok) atomicOr(D.err, MCG_ERR_FLAG_SINGULAR);
-    }
+    mcg_ph_solve(D, A, b);
+    MCG_PH(5);
     __syncthreads();
     MCG_PH(6);
 
@@ -1284,7 +1695,9 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
   MCG_PH(11);
 }
 
-__global__ void __launch_bounds__(512, 1) k_batch(McgDev D, McgBatchArgs A, int64_t max_len) {
+__global__ void __launch_bounds__(MCG_BATCH_THREADS, 1) k_batch(const __grid_constant__ McgDev D,
+                                                               const __grid_constant__ McgBatchArgs A,
+                                                               int64_t max_len) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   const McgBatchSm B = mcg_batch_sm(A);
@@ -1324,6 +1737,10 @@ __global__ void __launch_bounds__(512, 1) k_batch(McgDev D, McgBatchArgs A, int6
   if (resident && mine) mcg_batch_exit(D, A, blockIdx.x);
   MCG_PH(14);
   if (A.phase && threadIdx.x == 0)
-    for (int i = 0; i < MCG_NPHASE; ++i) atomicAdd(&A.phase[i], mcg_ph_acc[i]);
+    for (int i = 0; i < MCG_NPHASE; ++i) {
+      atomicAdd(&A.phase[i], mcg_ph_acc[i]);
+      if (blockIdx.x == 0) atomicAdd(&A.phase[MCG_NPHASE + i], mcg_ph_acc[i]);  // CTA 0 alone
+      atomicAdd(&A.phase[(2 + blockIdx.x) * MCG_NPHASE + i], mcg_ph_acc[i]);   // per CTA
+    }
 }
 #undef MCG_PH

@@ -107,6 +107,42 @@ bool eliminate_constant(int n, const int32_t* parent, const double* cap, const d
   return d[0] > 0.0;
 }
 
+int chain_schedule(int n, const int32_t* parent, std::vector<int32_t>& idx, int& a_first) {
+  if (n < 2) return 0;
+  std::vector<int32_t> child(n, -1), nchild(n, 0);
+  std::vector<int32_t> tops;
+  for (int i = 1; i < n; ++i) {
+    const int p = parent[i];
+    if (p < 0 || p >= i) return 0;
+    ++nchild[p];
+    child[p] = i;
+    if (p == 0) tops.push_back(i);
+  }
+  for (int i = 1; i < n; ++i)
+    if (nchild[i] > 1) return 0;
+  if (tops.empty() || tops.size() > 2) return 0;
+  // chains top -> leaf
+  std::vector<std::vector<int32_t>> ch;
+  for (int t : tops) {
+    std::vector<int32_t> c;
+    for (int i = t; i >= 0; i = child[i]) c.push_back(i);
+    ch.push_back(c);
+  }
+  if (ch.size() == 1) ch.emplace_back();
+  int ia = 0;
+  if (ch[1].size() > ch[0].size()) ia = 1;
+  const std::vector<int32_t>& A = ch[ia];
+  const std::vector<int32_t>& B = ch[1 - ia];
+  a_first = (B.empty() || A.front() > B.front()) ? 1 : 0;
+  const int lp = static_cast<int>((A.size() + 3) / 4 * 4);
+  idx.assign(2 * lp + 1, -1);
+  // leaf side padded: position lp-1 is the top, lp-1-k the k-th node below it
+  for (size_t k = 0; k < A.size(); ++k) idx[lp - 1 - k] = A[k];
+  for (size_t k = 0; k < B.size(); ++k) idx[2 * lp - 1 - k] = B[k];
+  idx[2 * lp] = 0;
+  return lp;
+}
+
 int64_t ceil_steps(double t_ms, double dt_ms) {
   return static_cast<int64_t>(std::ceil(t_ms / dt_ms - 1e-9));  // engine.cpp:21-23
 }
@@ -417,6 +453,22 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
       }
     }
     m.k_sp_off[ki + 1] = static_cast<int64_t>(m.k_sp_decay_tau.size());
+    // chain schedule of the constant systems: every eliminated diagonal of
+    // the systems that use it must have a usable reciprocal (mcg_recip != 0)
+    {
+      std::vector<int32_t> idx;
+      int a_first = 1;
+      int lp = (K.v_const || K.sp_const) ? chain_schedule(n, g.parent.data(), idx, a_first) : 0;
+      for (int i = 0; lp > 0 && i < n; ++i) {
+        if (K.v_const && m.k_vr[K.arr + i] == 0.0) lp = 0;
+        for (int sp = 0; K.sp_const && sp < spec.n_species; ++sp)
+          if (m.k_sp_r[K.sp_arr + int64_t(sp) * n + i] == 0.0) lp = 0;
+      }
+      K.ch_lp = lp;
+      K.ch_afirst = a_first;
+      K.ch_arr = static_cast<int64_t>(m.k_ch_idx.size());
+      if (lp > 0) m.k_ch_idx.insert(m.k_ch_idx.end(), idx.begin(), idx.end());
+    }
   }
 
   // ---- local cells (engine.cpp:317-348) ----

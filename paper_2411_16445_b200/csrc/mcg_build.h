@@ -61,6 +61,7 @@ struct HostModel {
   std::vector<McgKind> kinds;
   std::vector<Grid> grids;
   std::vector<int32_t> k_parent;
+  std::vector<int32_t> k_ch_idx;         // chain schedules (McgKind::ch_arr)
   std::vector<double> k_cap_dt, k_g_leak, k_g_leak_rhs, k_axial, k_g_na, k_g_k, k_cf, k_volume;
   std::vector<double> k_sp_cap_dt, k_sp_gs, k_sp_coupling, k_sp_init;
   std::vector<double> k_vf, k_vd;        // precomputed V elimination (per comp)
@@ -112,6 +113,11 @@ struct HostModel {
 // solve, which reports the NumericError at the same step as the reference).
 bool eliminate_constant(int n, const int32_t* parent, const double* cap, const double* gs,
                         const double* coupling, double* f, double* d);
+
+// Chain schedule of a tree for the lockstep sweep (mcg_sweep.cuh): if only
+// the root branches (into at most two chains), returns the padded chain length
+// LP and fills idx (2 LP + 1 positions, -1 = padding) and a_first; else 0.
+int chain_schedule(int n, const int32_t* parent, std::vector<int32_t>& idx, int& a_first);
 
 // Materialize; throws mcg::Error with the reference's messages.
 void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m);

@@ -33,6 +33,7 @@ struct McgDev {
   const McgKind* kinds;
   const McgSpec* specs;
   const int32_t* k_parent;
+  const int32_t* k_ch_idx;    // chain schedules (McgKind::ch_arr)
   const double *k_cap_dt, *k_g_leak, *k_g_leak_rhs, *k_axial, *k_g_na, *k_g_k, *k_cf, *k_volume;
   const double *k_sp_cap_dt, *k_sp_gs, *k_sp_coupling;
   // cells

@@ -100,7 +100,7 @@ struct Engine {
   // device model
   DBuf<McgKind> d_kinds;
   DBuf<McgSpec> d_specs;
-  DBuf<int32_t> d_k_parent;
+  DBuf<int32_t> d_k_parent, d_k_ch_idx;
   DBuf<double> d_k_cap_dt, d_k_g_leak, d_k_g_leak_rhs, d_k_axial, d_k_g_na, d_k_g_k, d_k_cf,
       d_k_volume, d_k_sp_cap_dt, d_k_sp_gs, d_k_sp_coupling, d_k_vf, d_k_vd, d_k_sp_f, d_k_sp_d, d_k_vr, d_k_sp_r, d_k_rvol;
   DBuf<int32_t> d_cell_kind;
@@ -163,8 +163,10 @@ struct Engine {
   std::vector<double> spk_t;
   std::vector<uint32_t> spk_gid;
   // persistent batch kernel (cell batches per CTA)
-  static constexpr int kBatchThreads = 512;
+  static constexpr int kBatchThreads = MCG_BATCH_THREADS;
   int32_t bc_cells = 1, bc_batches = 1, bc_grid = 1, bc_stc_max = 1, bc_nstc_max = 1;
+  int32_t bc_ch_pmax = 0, bc_ch_stride = 0;
+  int32_t bc_ev_cap = 0, bc_fmask_words = 0;
   int32_t bc_kind_doubles = 0, bc_specs_sm = 0, bc_stc_sm = 0;
   size_t bc_smem = 0;
   DBuf<int4> d_chunks;
@@ -177,11 +179,32 @@ struct Engine {
 
   void print_phases() {
     if (!phase_timing || !d_phase.p) return;
-    unsigned long long ph[MCG_NPHASE];
+    unsigned long long ph[2 * MCG_NPHASE];
     CK(cudaMemcpy(ph, d_phase.p, sizeof(ph), cudaMemcpyDeviceToHost));
     std::fprintf(stderr, "phase cycles (sum over CTAs):");
-    for (int i = 0; i < MCG_NPHASE; ++i) std::fprintf(stderr, " %d:%.3g", i, double(ph[i]));
-    std::fprintf(stderr, "  steps=%lld batches=%d\n", (long long)stats.steps, bc_batches);
+    for (int i = 0; i < MCG_NPHASE; ++i) std::fprintf(stderr, " %d:%llu", i, ph[i]);
+    std::fprintf(stderr, "  steps=%lld batches=%d\nphase cycles (CTA 0):", (long long)stats.steps, bc_batches);
+    for (int i = 0; i < MCG_NPHASE; ++i) std::fprintf(stderr, " %d:%llu", i, ph[MCG_NPHASE + i]);
+    std::fprintf(stderr, "  steps=%lld batches=1\n", (long long)stats.steps);
+    // per CTA: work cycles (everything but the grid-sync wait, phase 13)
+    std::vector<unsigned long long> pc(size_t(bc_grid) * MCG_NPHASE);
+    CK(cudaMemcpy(pc.data(), d_phase.p + 2 * MCG_NPHASE, pc.size() * 8, cudaMemcpyDeviceToHost));
+    std::vector<std::pair<double, int>> w;
+    for (int b = 0; b < bc_grid; ++b) {
+      double t = 0;
+      for (int i = 0; i < MCG_NPHASE; ++i)
+        if (i != 13) t += double(pc[size_t(b) * MCG_NPHASE + i]);
+      w.emplace_back(t, b);
+    }
+    std::sort(w.rbegin(), w.rend());
+    std::fprintf(stderr, "per-CTA work cycles: max %.4g (CTA %d) median %.4g min %.4g (CTA %d)\n", w[0].first,
+                 w[0].second, w[w.size() / 2].first, w.back().first, w.back().second);
+    for (int r = 0; r < 3 && r < int(w.size()); ++r) {
+      std::fprintf(stderr, "  CTA %d:", w[r].second);
+      for (int i = 0; i < MCG_NPHASE; ++i)
+        std::fprintf(stderr, " %d:%.3g", i, double(pc[size_t(w[r].second) * MCG_NPHASE + i]));
+      std::fprintf(stderr, "\n");
+    }
   }
   // stats
   mcg_stats stats{};
@@ -227,17 +250,29 @@ struct Engine {
     if (bc_nstc_max > 0xffff) throw Error(MCG_ERR_ENGINE, "too many STC placements per kind");
     // per cell: compartment block, noise draws, kind and cell records, STC
     // segments, and (upper bound) its STC slots in the fold/locator tables
+    // chain-sweep scratch: (1 + sp_max) systems x P_max positions per cell
+    bc_ch_pmax = 0;
+    for (const McgKind& K : m.kinds)
+      if (K.n <= smem_n && K.ch_lp > 0) bc_ch_pmax = std::max(bc_ch_pmax, 2 * K.ch_lp + 1);
+    bc_ch_stride = bc_ch_pmax > 0 ? (1 + sp_max) * bc_ch_pmax : 0;
     const size_t per_cell = size_t(smem_stride) * 8 + 32 * 8 + sizeof(McgKind) + sizeof(McgCellSm) +
-                            size_t(bc_nstc_max) * sizeof(McgSegSm) + size_t(cell_stc_max) * 12;
+                            size_t(bc_nstc_max) * sizeof(McgSegSm) + size_t(cell_stc_max) * 12 +
+                            size_t(bc_ch_stride) * 8;
     // staged kind constants (McgKindSm): one block per distinct kind of a batch
     size_t kb_max = 0;
     for (const McgKind& K : m.kinds)
-      if (K.n <= smem_n) kb_max = std::max<size_t>(kb_max, mcg_kind_block_doubles(K.n, K.n_species));
+      if (K.n <= smem_n)
+        kb_max = std::max<size_t>(kb_max, mcg_kind_block_doubles(K.n, K.n_species, K.ch_lp));
     // the spec table, when small, is staged once per launch
     bc_specs_sm = m.specs.size() * sizeof(McgSpec) <= 16 * 1024 ? static_cast<int32_t>(m.specs.size()) : 0;
     const size_t fixed = size_t(bc_specs_sm) * sizeof(McgSpec) + 2048;
     const size_t budget = 200 * 1024;
-    const int c_max = static_cast<int>(std::max<size_t>(1, (budget - fixed) / (per_cell + kb_max * 8)));
+    // one staged kind block per distinct kind of a batch: at most min(C, kinds)
+    const size_t nkinds = std::max<size_t>(m.kinds.size(), 1);
+    int c_max = 1;
+    while (c_max < 0xffff &&
+           fixed + size_t(c_max + 1) * per_cell + std::min<size_t>(c_max + 1, nkinds) * kb_max * 8 <= budget)
+      ++c_max;
     bc_cells = std::clamp((nl + dev_sms - 1) / std::max(dev_sms, 1), 1, std::min(c_max, 0xffff));
     bc_batches = std::max(1, (nl + bc_cells - 1) / bc_cells);
     // STC slots of the fullest batch
@@ -251,7 +286,7 @@ struct Engine {
     // fold-flag words: one per 32 slots of every 512-thread round
     const size_t fmask_words = size_t((bc_stc_max + kBatchThreads - 1) / kBatchThreads) * (kBatchThreads / 32) + 1;
     bc_smem = size_t(bc_cells) * (size_t(smem_stride) * 8 + 32 * 8 + sizeof(McgKind) + sizeof(McgCellSm) +
-                                  size_t(bc_nstc_max) * sizeof(McgSegSm)) +
+                                  size_t(bc_nstc_max) * sizeof(McgSegSm) + size_t(bc_ch_stride) * 8) +
               size_t(bc_stc_max) * (8 + 4) + size_t(bc_kind_doubles) * 8 +
               size_t(bc_specs_sm) * sizeof(McgSpec) + fmask_words * 4 + 64;
     // resident batches (one per CTA) keep their STC state in shared memory too
@@ -262,6 +297,17 @@ struct Engine {
                     ? 1 : 0;
     if (std::getenv("MCG_NO_STC_SM")) bc_stc_sm = 0;
     if (bc_stc_sm) bc_smem += size_t(bc_stc_max) * 32;
+    bc_fmask_words = static_cast<int32_t>(fmask_words);
+    // staged delivery: the epoch's due events of the resident batch in shared
+    // memory (mcg_stage_events), in whatever the opt-in limit leaves
+    bc_ev_cap = 0;
+    if (bc_stc_sm && !std::getenv("MCG_NO_STAGED_EVENTS")) {
+      const size_t lim = size_t(smem_optin) - 1024;
+      const size_t left = lim > bc_smem + 32 ? lim - bc_smem - 32 : 0;
+      bc_ev_cap = static_cast<int32_t>(std::min<size_t>(left / sizeof(McgEvSm), 4096));
+      if (bc_ev_cap < 64) bc_ev_cap = 0;
+      if (bc_ev_cap > 0) bc_smem += size_t(bc_ev_cap) * sizeof(McgEvSm) + 16;
+    }
     CK(cudaFuncSetAttribute(k_batch, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(bc_smem)));
     // leave the rest of the unified L1/shared array to L1 (STC state streams through it)
@@ -312,6 +358,7 @@ struct Engine {
     d_kinds.upload(m.kinds, st);
     d_specs.upload(m.specs, st);
     d_k_parent.upload(m.k_parent, st);
+    d_k_ch_idx.upload(m.k_ch_idx, st);
     d_k_cap_dt.upload(m.k_cap_dt, st);
     d_k_g_leak.upload(m.k_g_leak, st);
     d_k_g_leak_rhs.upload(m.k_g_leak_rhs, st);
@@ -509,6 +556,7 @@ struct Engine {
     D.kinds = d_kinds.p;
     D.specs = d_specs.p;
     D.k_parent = d_k_parent.p;
+    D.k_ch_idx = d_k_ch_idx.p;
     D.k_cap_dt = d_k_cap_dt.p;
     D.k_g_leak = d_k_g_leak.p;
     D.k_g_leak_rhs = d_k_g_leak_rhs.p;
@@ -712,9 +760,13 @@ struct Engine {
     A.kind_doubles = bc_kind_doubles;
     A.n_specs_sm = bc_specs_sm;
     A.stc_sm = bc_stc_sm;
+    A.ch_stride = bc_ch_stride;
+    A.ch_pmax = bc_ch_pmax;
+    A.ev_cap = bc_ev_cap;
+    A.fmask_words = bc_fmask_words;
     if (phase_timing) {
       if (!d_phase.p) {
-        d_phase.alloc(MCG_NPHASE);
+        d_phase.alloc(size_t(2 + bc_grid) * MCG_NPHASE);
         d_phase.zero(st);
       }
       A.phase = d_phase.p;

@@ -44,6 +44,14 @@ struct McgKind {
   // sequence (tree_solver.cpp:55-70).  v_const: the LIF-cable V system when
   // no conductance synapse is active (gs = g_leak + 0.0); sp_const: species.
   int32_t v_const, sp_const;
+  // chain schedule of the constant systems (mcg_sweep.cuh; mcg_build.cpp
+  // chain_schedule): ch_lp > 0 when the tree is a "spider" (only the root
+  // branches, at most two chains) and every eliminated diagonal is in the
+  // reciprocal-quotient range.  Positions: chain A [0, ch_lp), chain B
+  // [ch_lp, 2 ch_lp), leaf side padded, tops aligned; the root at 2 ch_lp.
+  // k_ch_idx[ch_arr + pos] = node of the position (-1: padding).
+  int32_t ch_lp, ch_afirst;
+  int64_t ch_arr;
 };
 
 // SynSpec per kind placement (recipe.hpp:82-98) + hoisted constants

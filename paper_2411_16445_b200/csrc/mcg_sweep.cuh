@@ -1,0 +1,182 @@
+// mcg_sweep.cuh — the constant-diagonal Hines solve (V, or one species, of one
+// cell) scheduled along the tree's chains, one lane per chain.
+//
+// tree_solver.cpp:46-74 eliminates leaves-to-root in descending index order,
+// rhs[par[i]] += f[i]*rhs[i], then substitutes root-to-leaves,
+// v[i] = (rhs[i] + coupling[i]*v[par[i]]) / diag[i].  With the diagonal
+// constant (McgKind::v_const / sp_const) f and the eliminated diagonal d are
+// precomputed, and what is left per step are two dependent chains of fp64
+// operations through the tree.  For a "spider" tree — every node but the root
+// has at most one child, the shape of the consolidation cells (soma halves
+// continued by an apical and a basal dendrite) — each chain
+// hanging off the root depends only on itself, so the two chains of a system
+// run on two adjacent lanes and meet at the root through one shuffle: the
+// latency is the longer chain, not the node count.
+//
+// Every fp64 operation is the reference's, with the reference's operands:
+//   r2[i]  = cap[i]*x[i] + rhs[i]                   (tree_solver.cpp:57; pass 1)
+//   r2[p] += f[c]*r2[c]   for the only child c of p  (:66): along a chain the
+//            running value is final once its predecessor is; the root adds its
+//            children's terms in descending child order, as the loop does
+//   x[i]   = (r2[i] + coup[i]*x[par[i]]) / d[i]     (:71-73)
+// The chains are stored position-major, leaf side padded to a multiple of 4
+// and tops aligned (mcg_build.cpp chain_schedule); padding positions carry
+// f = -0, coup = 0, d = y = 1 and r2 = +0, which are exact identities
+// ((-0)*x + r == r and +0 + (+-0) == +0 in round-to-nearest).
+// The division is Markstein's correctly rounded quotient from y = RN(1/d)
+// (mcg_div, mcg_device.cuh) without the per-division range test on the
+// dependent chain: the numerators' range is checked off the chain and if any
+// lies outside [2^-700, 2^700] (other than +0) the pair redoes its
+// substitution with IEEE division from the stored r2.  The host guarantees
+// d in [2^-200, 2^200] for these systems (McgKind::ch_lp > 0).
+#pragma once
+#include <stdint.h>
+
+extern __shared__ double mcg_smem[];
+
+// numerator outside the range where the reciprocal quotient is exact (or -0)
+__device__ __forceinline__ unsigned mcg_div_bad(double num) {
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(num));
+  const unsigned long long a = b & 0x7fffffffffffffffull;
+  constexpr unsigned long long lo = 0x1430000000000000ull;  // 2^-700
+  constexpr unsigned long long hi = 0x6bb0000000000000ull;  // 2^700
+  return (b != 0ull && a - lo > hi - lo) ? 1u : 0u;
+}
+
+__device__ __forceinline__ double mcg_qdiv(double x, double d, double y) {
+  const double q = __dmul_rn(x, y);
+  const double r = __fma_rn(-q, d, x);
+  return __fma_rn(r, y, q);
+}
+
+// one lane of the chain sweep (offsets into mcg_smem; idx in int32 units)
+struct McgChainLane {
+  int on;        // this lane's system takes the chain sweep this step
+  int side;      // 0: chain A (positions [0, lp)), 1: chain B ([lp, 2 lp))
+  int lp;        // positions per chain (multiple of 4); the root is at 2 lp
+  int r2c;       // r2 scratch, by position (pass 1 wrote r2 before elimination)
+  int fc;        // f | coup | d | y, by position, each 2 lp + 1 long
+  int idx;       // position -> node (-1: padding)
+  int x;         // solved state, by node
+  int a_first;   // chain A's top has the larger index
+};
+
+// all 32 lanes of the warp must call this (inactive lanes with on = 0)
+__device__ __forceinline__ void mcg_chain_lane(const McgChainLane& L) {
+  double* S = mcg_smem;
+  const int32_t* PI = reinterpret_cast<const int32_t*>(mcg_smem);
+  const int lp = L.on ? L.lp : 0;
+  const int P = 2 * L.lp + 1;
+  const int p0 = L.side * L.lp;
+  const int rb = L.r2c + p0, fb = L.fc + p0, cb = L.fc + P + p0, db = L.fc + 2 * P + p0,
+            yb = L.fc + 3 * P + p0, ib = L.idx + p0;
+
+  // ---- elimination, leaf side first; block b + 4 is loaded while block b runs
+  double cur = 0.0, fp = -0.0;
+  {
+    double r4[4], f4[4];
+    if (lp > 0) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        r4[u] = S[rb + u];
+        f4[u] = S[fb + u];
+      }
+    }
+#pragma unroll 1
+    for (int b = 0; b < lp; b += 4) {
+      double rn[4], fn[4];
+      const int nb = (b + 4 < lp) ? b + 4 : b;  // last block reloads itself (unused)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        rn[u] = S[rb + nb + u];
+        fn[u] = S[fb + nb + u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double r = r4[u] + fp * cur;
+        S[rb + b + u] = r;
+        cur = r;
+        fp = f4[u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        r4[u] = rn[u];
+        f4[u] = fn[u];
+      }
+    }
+  }
+  // ---- root: the children's terms in descending child order
+  const double t = fp * cur;  // f of this chain's top times its final r2
+  const double to = __shfl_xor_sync(0xffffffffu, t, 1);
+  const double ta = L.side == 0 ? t : to, tb = L.side == 0 ? to : t;
+  double r0 = L.on ? S[L.r2c + 2 * L.lp] : 0.0;
+  if (L.a_first) {
+    r0 = r0 + ta;
+    r0 = r0 + tb;
+  } else {
+    r0 = r0 + tb;
+    r0 = r0 + ta;
+  }
+  // ---- substitution, top first
+  unsigned bad = L.on ? mcg_div_bad(r0) : 0u;
+  double xv = 0.0;
+  if (L.on) {
+    xv = mcg_qdiv(r0, S[L.fc + 2 * P + 2 * L.lp], S[L.fc + 3 * P + 2 * L.lp]);
+    if (L.side == 0) S[L.x] = xv;
+  }
+  {
+    // blocks of two positions (register budget), next block loaded ahead
+    double r2v[2], c2v[2], d2v[2], y2v[2];
+    int i2v[2];
+    if (lp > 0) {
+      const int b = lp - 2;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        r2v[u] = S[rb + b + u];
+        c2v[u] = S[cb + b + u];
+        d2v[u] = S[db + b + u];
+        y2v[u] = S[yb + b + u];
+        i2v[u] = PI[ib + b + u];
+      }
+    }
+#pragma unroll 1
+    for (int b = lp - 2; b >= 0; b -= 2) {
+      double rn[2], cn[2], dn[2], yn[2];
+      int in[2];
+      const int nb = b >= 2 ? b - 2 : b;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        rn[u] = S[rb + nb + u];
+        cn[u] = S[cb + nb + u];
+        dn[u] = S[db + nb + u];
+        yn[u] = S[yb + nb + u];
+        in[u] = PI[ib + nb + u];
+      }
+#pragma unroll
+      for (int u = 1; u >= 0; --u) {
+        const double num = r2v[u] + c2v[u] * xv;
+        bad |= mcg_div_bad(num);
+        xv = mcg_qdiv(num, d2v[u], y2v[u]);
+        if (i2v[u] >= 0) S[L.x + i2v[u]] = xv;
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        r2v[u] = rn[u];
+        c2v[u] = cn[u];
+        d2v[u] = dn[u];
+        y2v[u] = yn[u];
+        i2v[u] = in[u];
+      }
+    }
+  }
+  bad |= __shfl_xor_sync(0xffffffffu, bad, 1);
+  if (bad && L.on) {  // rare: the substitution again with IEEE division
+    double xe = __ddiv_rn(r0, S[L.fc + 2 * P + 2 * L.lp]);
+    if (L.side == 0) S[L.x] = xe;
+    for (int p = lp - 1; p >= 0; --p) {
+      xe = __ddiv_rn(S[rb + p] + S[cb + p] * xe, S[db + p]);
+      const int i = PI[ib + p];
+      if (i >= 0) S[L.x + i] = xe;
+    }
+  }
+}

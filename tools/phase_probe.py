@@ -1,9 +1,36 @@
-import os, sys, time
+"""Per-phase cycle breakdown of k_batch (MCG_PHASE_TIMING=1) over bio-time
+windows of the config-3 workload; the engine prints cumulative totals (thread 0
+of every CTA, summed over CTAs) after each advance_to, this prints the deltas
+as µs per fine step per CTA."""
+import os, re, sys, time, subprocess
+if "--child" not in sys.argv:
+    p = subprocess.run([sys.executable, __file__, "--child"] + sys.argv[1:], capture_output=True, text=True)
+    print(p.stdout)
+    wins = [l for l in p.stdout.splitlines() if l.startswith("window")]
+    for tag in ("sum over CTAs", "CTA 0"):
+        lines = [l for l in p.stderr.splitlines() if l.startswith(f"phase cycles ({tag})")]
+        prev = None
+        print(tag)
+        for w, l in zip(wins, lines):
+            v = [float(x.split(":")[1]) for x in l.split(":", 1)[1].split() if ":" in x]
+            ctas = int(l.split("batches=")[1])
+            d = v if prev is None else [a - b for a, b in zip(v, prev)]
+            prev = v
+            steps = int(w.split()[3])
+            print(" ", w.split()[1], " ".join(f"{i}:{x / steps / ctas / 1965.0:.2f}" for i, x in enumerate(d) if x > 0))
+    cta = [l for l in p.stderr.splitlines() if "per-CTA" in l or l.startswith("  CTA")]
+    print("\n".join(cta[:8]))
+    sys.exit(0)
 os.environ["MCG_PHASE_TIMING"] = "1"
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2411_16445_b200 import network as N, Engine, EngineOptions
-c = N.ConsolidationConfig(n_cells=2000, n_exc=1600, seed=1, multi_compartment=True)
+n = int(os.environ.get("PROBE_N", "2000"))
+c = N.ConsolidationConfig(n_cells=n, n_exc=n * 4 // 5, seed=1, multi_compartment=True)
 b = N.build_consolidation_network(c, True)
 e = Engine(b.recipe, EngineOptions(0.5, 1))
-e.advance_to(1000.0)
-t = time.time(); e.advance_to(3000.0); print("wall", time.time() - t, e.stats()["steps"], flush=True)
+ctas = e.stats().get("batch_grid", 143)
+for t1 in (1000.0, 3000.0, 10000.0, 12000.0):
+    s0 = e.stats()["steps"]
+    a = time.time(); e.advance_to(t1); w = time.time() - a
+    st = e.stats()["steps"] - s0
+    print(f"window {t1:.0f} steps {st} {ctas} wall_us_per_step {1e6 * w / st:.2f}", flush=True)
