@@ -65,8 +65,14 @@ __device__ void mcg_expand(const McgEv& E, const McgDev& D, int32_t j, int64_t s
   const int64_t len = s1 - s0;
   const int64_t nthr = int64_t(gridDim.x) * blockDim.x;
   const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  // one warp per (source, step) task, lanes over the source's out-edges;
+  // consecutive tasks on different CTAs (a burst of one source's edges is
+  // spread over the grid instead of a few threads of CTA 0)
+  const int64_t nw = nthr >> 5;
+  const int64_t gw = int64_t(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
   const int64_t ntask = int64_t(E.n_tasks) * max_len;
-  for (int64_t t = tid; t < ntask; t += nthr) {
+  for (int64_t t = gw; t < ntask; t += nw) {
     const int64_t off = t % max_len;
     if (off >= len) continue;
     const McgSrcTask T = E.tasks[t / max_len];
@@ -75,9 +81,13 @@ __device__ void mcg_expand(const McgEv& E, const McgDev& D, int32_t j, int64_t s
     if (T.type == MCG_SRC_POISSON) {
       const int64_t s = s0 + off;
       if (s < T.a || s >= T.b) continue;
-      const mcg_key key = mcg_make_key(E.seed, 0x100000000ull + uint64_t(T.source), 3, 0);
-      if (!(mcg_uniform_for(&key, static_cast<uint64_t>(s)) < T.prob)) continue;
-      for (int64_t k = e0; k < e1; ++k) {
+      int fire = 0;
+      if (lane == 0) {
+        const mcg_key key = mcg_make_key(E.seed, 0x100000000ull + uint64_t(T.source), 3, 0);
+        fire = mcg_uniform_for(&key, static_cast<uint64_t>(s)) < T.prob ? 1 : 0;
+      }
+      if (!__shfl_sync(MCG_FULL, fire, 0)) continue;
+      for (int64_t k = e0 + lane; k < e1; k += 32) {
         const int64_t r = E.src_edges[k];
         mcg_push(E, j, r, s + E.e_delay[r]);
       }
@@ -86,7 +96,7 @@ __device__ void mcg_expand(const McgEv& E, const McgDev& D, int32_t j, int64_t s
         for (int64_t i = T.a; i < T.b; ++i) {
           const int64_t st = E.scripted_steps[i];
           if (st < s0 || st >= s1) continue;
-          for (int64_t k = e0; k < e1; ++k) {
+          for (int64_t k = e0 + lane; k < e1; k += 32) {
             const int64_t r = E.src_edges[k];
             mcg_push(E, j, r, st + E.e_delay[r]);
           }
@@ -98,7 +108,7 @@ __device__ void mcg_expand(const McgEv& E, const McgDev& D, int32_t j, int64_t s
           const int64_t st = static_cast<int64_t>(ceil((T.r_t0 + double(kk) * T.r_period) / E.dt - 1e-9));
           if (st >= s1) break;
           if (st < s0) continue;
-          for (int64_t k = e0; k < e1; ++k) {
+          for (int64_t k = e0 + lane; k < e1; k += 32) {
             const int64_t r = E.src_edges[k];
             mcg_push(E, j, r, st + E.e_delay[r]);
           }
@@ -108,8 +118,6 @@ __device__ void mcg_expand(const McgEv& E, const McgDev& D, int32_t j, int64_t s
   }
   // spikes of the previous epoch (engine.cpp:875-889: delivery at
   // step + 1 + delay), one warp per spike / spiking cell, lanes over out-edges
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = nthr >> 5;
   if (E.x_recv != nullptr) {  // sharded: every rank's spikes, local out-edges only
     for (int r = 0; r < E.x_world; ++r) {
       const int64_t* blk = E.x_recv + r * E.x_block;
@@ -196,11 +204,11 @@ struct McgKindSm {
 
 // + one spare word (mcg_sweep_const_sm), then the chain section when the kind
 // has a chain schedule (lp > 0, P = 2 lp + 1 positions): the position -> node
-// list (int32) and, per system (V, then each species), f | coup | d | y in
-// position order (mcg_sweep.cuh)
+// list (int32) and, per system (V, then each species), f | coup | d | y | cap |
+// g_leak_rhs (V; 0 for species) in position order (mcg_sweep.cuh)
 __host__ __device__ __forceinline__ int mcg_kind_block_doubles(int n, int S, int lp) {
   const int P = 2 * lp + 1;
-  return (9 + 6 * S) * n + (n + 1) / 2 + 1 + (lp > 0 ? (P + 1) / 2 + 4 * (1 + S) * P : 0);
+  return (9 + 6 * S) * n + (n + 1) / 2 + 1 + (lp > 0 ? (P + 1) / 2 + 6 * (1 + S) * P : 0);
 }
 __host__ __device__ __forceinline__ int mcg_kind_chain_off(int n, int S) {  // doubles
   return (9 + 6 * S) * n + (n + 1) / 2 + 1;
@@ -250,19 +258,23 @@ __device__ __forceinline__ void mcg_kind_stage(const McgDev& D, const McgKind& K
     for (int i = threadIdx.x; i < (1 + S) * P; i += T) {
       const int sy = i / P, pos = i - sy * P;
       const int node = D.k_ch_idx[K.ch_arr + pos];
-      double f = -0.0, c = 0.0, d = 1.0, y = 1.0;  // padding: exact identities
+      double f = -0.0, c = 0.0, d = 1.0, y = 1.0, cp = 0.0, gl = 0.0;  // padding: exact identities
       if (node >= 0) {
         const int64_t o = (sy == 0) ? K.arr + node : K.sp_arr + int64_t(sy - 1) * n + node;
         f = (sy == 0) ? D.k_vf[o] : D.k_sp_f[o];
         c = (sy == 0) ? D.k_axial[o] : D.k_sp_coupling[o];
         d = (sy == 0) ? D.k_vd[o] : D.k_sp_d[o];
         y = (sy == 0) ? D.k_vr[o] : D.k_sp_r[o];
+        cp = (sy == 0) ? D.k_cap_dt[o] : D.k_sp_cap_dt[o];
+        gl = (sy == 0) ? D.k_g_leak_rhs[o] : 0.0;
       }
-      double* q = sysb + sy * 4 * P;
+      double* q = sysb + sy * 6 * P;
       q[pos] = f;
       q[P + pos] = c;
       q[2 * P + pos] = d;
       q[3 * P + pos] = y;
+      q[4 * P + pos] = cp;
+      q[5 * P + pos] = gl;
     }
   }
 }
@@ -1015,45 +1027,9 @@ __device__ __noinline__ void mcg_ph_solve(const McgDev& D, const McgBatchArgs& A
   const int m = D.smem_n;
   McgCellSm* cs = B.cs;
   const McgKind* kc = B.kc;
-  // ---- E2a. chain-scheduled constant systems (mcg_sweep.cuh): pass 1, the
-  // pre-elimination r2 of every position, warp per cell, lanes over
-  // (system, position)
-  if (A.ch_stride > 0) {
-    for (int k = warp; k < nc; k += nwarps) {
-      const McgKind& K = kc[k];
-      if (K.ch_lp == 0 || K.n > m) continue;
-      const McgCellSm& X = cs[k];
-      const int n = K.n, P = 2 * K.ch_lp + 1;
-      const McgKindOff KO = mcg_kind_off(B.ksm_o + X.kb, n, K.n_species);
-      const int32_t* PI = reinterpret_cast<const int32_t*>(mcg_smem);
-      const int ixo = 2 * (B.ksm_o + X.kb + mcg_kind_chain_off(n, K.n_species));
-      const int bo = k * A.comp_stride;
-      const bool hc = X.has_current;
-      for (int u = lane; u < S1 * P; u += 32) {
-        const int sys = u / P, pos = u - sys * P;
-        if (!mcg_chain_ok(K, X, sys, m)) continue;
-        const int node = PI[ixo + pos];
-        double r = 0.0;
-        if (node >= 0) {
-          const double* S = mcg_smem;
-          if (sys == 0) {
-            const double rhs = S[KO.glr + node] + 0.0 + (hc ? S[bo + (6 + D.sp_max) * m + node] : 0.0);
-            r = S[KO.cap + node] * S[bo + node] + rhs;
-          } else {
-            const int q = sys - 1;
-            const bool pc = q == K.prp_idx && X.prod != 0.0 && node == K.prp_comp;
-            r = S[KO.sp_cap + q * n + node] * S[bo + m + q * n + node] + (pc ? X.prod : 0.0);
-          }
-        }
-        mcg_smem[B.chs_o + k * A.ch_stride + sys * A.ch_pmax + pos] = r;
-      }
-    }
-    MCG_PH(21);
-    __syncthreads();
-    MCG_PH(18);
-  }
-  // ---- E2b. pass 2, one lane per (cell, system, chain) on threads [0, 256),
-  // beside the other systems (thread per (cell, system)) on [256, T)
+  // ---- E2a. chain-scheduled constant systems (mcg_sweep.cuh), one lane per
+  // (cell, system, chain) on threads [0, split), beside the other systems
+  // (thread per (cell, system)) on [split, T)
   const int nch = (A.ch_stride > 0) ? ((2 * S1 * nc + 31) & ~31) : 0;
   const int split = nch > 0 ? min(256, T / 2) : 0;
   if (tid < split) {
@@ -1072,9 +1048,16 @@ __device__ __noinline__ void mcg_ph_solve(const McgDev& D, const McgBatchArgs& A
           L.lp = K.ch_lp;
           L.r2c = B.chs_o + k * A.ch_stride + sys * A.ch_pmax;
           L.idx = 2 * cho;
-          L.fc = cho + (P + 1) / 2 + sys * 4 * P;
+          L.fc = cho + (P + 1) / 2 + sys * 6 * P;
           L.x = k * A.comp_stride + (sys == 0 ? 0 : m + (sys - 1) * n);
           L.a_first = K.ch_afirst;
+          L.v = sys == 0;
+          // right-hand sides (engine.cpp:683 / 746-748): V: g_leak_rhs + 0.0 +
+          // rhs_current (if any current); species: production at the
+          // synthesis compartment
+          L.rc = (sys == 0 && X.has_current) ? k * A.comp_stride + (6 + D.sp_max) * m : -1;
+          L.pc = (sys > 0 && sys - 1 == K.prp_idx && X.prod != 0.0) ? K.prp_comp : -1;
+          L.prod = X.prod;
         }
       }
       MCG_PH(19);

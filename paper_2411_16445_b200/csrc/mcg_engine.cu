@@ -205,6 +205,7 @@ struct Engine {
         std::fprintf(stderr, " %d:%.3g", i, double(pc[size_t(w[r].second) * MCG_NPHASE + i]));
       std::fprintf(stderr, "\n");
     }
+    d_phase.zero(st);  // per advance_to call
   }
   // stats
   mcg_stats stats{};

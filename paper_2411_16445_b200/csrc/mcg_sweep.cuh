@@ -14,7 +14,7 @@
 // latency is the longer chain, not the node count.
 //
 // Every fp64 operation is the reference's, with the reference's operands:
-//   r2[i]  = cap[i]*x[i] + rhs[i]                   (tree_solver.cpp:57; pass 1)
+//   r2[i]  = cap[i]*x[i] + rhs[i]                   (tree_solver.cpp:57)
 //   r2[p] += f[c]*r2[c]   for the only child c of p  (:66): along a chain the
 //            running value is final once its predecessor is; the root adds its
 //            children's terms in descending child order, as the loop does
@@ -54,12 +54,25 @@ struct McgChainLane {
   int on;        // this lane's system takes the chain sweep this step
   int side;      // 0: chain A (positions [0, lp)), 1: chain B ([lp, 2 lp))
   int lp;        // positions per chain (multiple of 4); the root is at 2 lp
-  int r2c;       // r2 scratch, by position (pass 1 wrote r2 before elimination)
-  int fc;        // f | coup | d | y, by position, each 2 lp + 1 long
+  int r2c;       // r2 after elimination, by position
+  int fc;        // f | coup | d | y | cap | g_leak_rhs, by position, each 2 lp + 1 long
   int idx;       // position -> node (-1: padding)
   int x;         // solved state, by node
   int a_first;   // chain A's top has the larger index
+  int v;         // V system (else species)
+  int rc;        // V: rhs_current by node (-1: no current this step)
+  int pc;        // species: synthesis compartment (-1: no production)
+  double prod;   // species: production at pc
 };
+
+// r2 of a position before elimination, cap*x + rhs (tree_solver.cpp:57), with
+// the reference's right-hand sides (engine.cpp:683 / 746-748); padding
+// positions (node < 0) give +0
+__device__ __forceinline__ double mcg_chain_rinit(const McgChainLane& L, int node, double cap,
+                                                  double gl, double x, double rc) {
+  const double rhs = L.v ? (gl + 0.0 + (L.rc >= 0 ? rc : 0.0)) : (node == L.pc ? L.prod : 0.0);
+  return cap * x + rhs;
+}
 
 // all 32 lanes of the warp must call this (inactive lanes with on = 0)
 __device__ __forceinline__ void mcg_chain_lane(const McgChainLane& L) {
@@ -71,26 +84,42 @@ __device__ __forceinline__ void mcg_chain_lane(const McgChainLane& L) {
   const int rb = L.r2c + p0, fb = L.fc + p0, cb = L.fc + P + p0, db = L.fc + 2 * P + p0,
             yb = L.fc + 3 * P + p0, ib = L.idx + p0;
 
-  // ---- elimination, leaf side first; block b + 4 is loaded while block b runs
+  // ---- elimination, leaf side first.  Block b's links run while block b + 4's
+  // r2 is formed from operands loaded one block ahead, whose node indices were
+  // loaded two blocks ahead
+  const int capb = L.fc + 4 * P + p0, glb = L.fc + 5 * P + p0;
   double cur = 0.0, fp = -0.0;
   {
     double r4[4], f4[4];
-    if (lp > 0) {
+    int i4[4];  // node indices of the block after the one r4 holds
+    auto load_idx = [&](int b, int* o) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) o[u] = (b < lp) ? PI[ib + b + u] : -1;
+    };
+    auto form = [&](int b, const int* id, double* r, double* f) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        r4[u] = S[rb + u];
-        f4[u] = S[fb + u];
+        const int node = id[u];
+        const double x = node >= 0 ? S[L.x + node] : 0.0;
+        const double rc = (node >= 0 && L.rc >= 0) ? S[L.rc + node] : 0.0;
+        const double gl = L.v ? S[glb + b + u] : 0.0;
+        r[u] = mcg_chain_rinit(L, node, S[capb + b + u], gl, x, rc);
+        f[u] = S[fb + b + u];
       }
+    };
+    if (lp > 0) {
+      int i0[4];
+      load_idx(0, i0);
+      load_idx(4, i4);
+      form(0, i0, r4, f4);
     }
 #pragma unroll 1
     for (int b = 0; b < lp; b += 4) {
+      int in[4];
+      load_idx(b + 8, in);
       double rn[4], fn[4];
-      const int nb = (b + 4 < lp) ? b + 4 : b;  // last block reloads itself (unused)
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        rn[u] = S[rb + nb + u];
-        fn[u] = S[fb + nb + u];
-      }
+      const int nb = (b + 4 < lp) ? b + 4 : b;  // the last block forms itself again (unused)
+      form(nb, i4, rn, fn);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const double r = r4[u] + fp * cur;
@@ -102,6 +131,7 @@ __device__ __forceinline__ void mcg_chain_lane(const McgChainLane& L) {
       for (int u = 0; u < 4; ++u) {
         r4[u] = rn[u];
         f4[u] = fn[u];
+        i4[u] = in[u];
       }
     }
   }
@@ -109,7 +139,12 @@ __device__ __forceinline__ void mcg_chain_lane(const McgChainLane& L) {
   const double t = fp * cur;  // f of this chain's top times its final r2
   const double to = __shfl_xor_sync(0xffffffffu, t, 1);
   const double ta = L.side == 0 ? t : to, tb = L.side == 0 ? to : t;
-  double r0 = L.on ? S[L.r2c + 2 * L.lp] : 0.0;
+  double r0 = 0.0;
+  if (L.on) {
+    const int pr = L.fc + 2 * L.lp;  // root position
+    r0 = mcg_chain_rinit(L, 0, S[pr + 4 * P], L.v ? S[pr + 5 * P] : 0.0, S[L.x],
+                         L.rc >= 0 ? S[L.rc] : 0.0);
+  }
   if (L.a_first) {
     r0 = r0 + ta;
     r0 = r0 + tb;

@@ -14,12 +14,18 @@ if "--child" not in sys.argv:
         for w, l in zip(wins, lines):
             v = [float(x.split(":")[1]) for x in l.split(":", 1)[1].split() if ":" in x]
             ctas = int(l.split("batches=")[1])
-            d = v if prev is None else [a - b for a, b in zip(v, prev)]
+            d = v  # the engine resets its counters after every advance_to
             prev = v
             steps = int(w.split()[3])
             print(" ", w.split()[1], " ".join(f"{i}:{x / steps / ctas / 1965.0:.2f}" for i, x in enumerate(d) if x > 0))
     cta = [l for l in p.stderr.splitlines() if "per-CTA" in l or l.startswith("  CTA")]
-    print("\n".join(cta[:8]))
+    for w in range(len(cta) // 4):  # per window: summary + top 3 CTAs, cycles per step
+        steps = int(wins[w].split()[3]) if w < len(wins) else 1
+        print(wins[w].split()[1] if w < len(wins) else "", cta[4 * w])
+        for l in cta[4 * w + 1:4 * w + 4]:
+            head, rest = l.split(":", 1)
+            vals = [x.split(":") for x in rest.split()]
+            print("   ", head.strip(), " ".join(f"{i}:{float(x) / steps / 1965:.2f}" for i, x in vals if float(x) > 0))
     sys.exit(0)
 os.environ["MCG_PHASE_TIMING"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
