@@ -31,7 +31,7 @@
 
 #define MCG_NPHASE 24
 #ifndef MCG_BATCH_THREADS
-#define MCG_BATCH_THREADS 512
+#define MCG_BATCH_THREADS 256
 #endif
 
 struct McgBatchArgs {
