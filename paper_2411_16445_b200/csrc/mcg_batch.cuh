@@ -188,6 +188,8 @@ struct McgSegSm {
   double cf;                // charge factor of the placement's compartment
   int64_t f_base, f_head, f_tail;  // delayed-calcium queue (McgFifo), resident copy
   int32_t f_cap, fifo;
+  int32_t prp_sm;           // mcg_smem offset of the PRP value at comp (-1: global / none)
+  int32_t late;             // the cell has a PRP pool (stc_late_step runs)
 };
 
 // per-kind constants the sweeps read every step, staged in shared memory once
@@ -854,6 +856,9 @@ __device__ void mcg_batch_enter(const McgDev& D, const McgBatchArgs& A, int32_t 
       g.vol = D.k_volume[K.arr + S.comp];
       g.rvol = D.k_rvol[K.arr + S.comp];
       g.cf = D.k_cf[K.arr + S.comp];
+      g.late = K.prp_idx >= 0 ? 1 : 0;
+      g.prp_sm = (K.prp_idx >= 0 && K.n <= m)
+                     ? tid * A.comp_stride + m + K.prp_idx * K.n + S.comp : -1;
       g.fifo = G.fifo;
       if (G.fifo >= 0) {
         g.f_base = D.fifos[G.fifo].base;
@@ -1180,7 +1185,15 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
       __syncwarp();
       const uint64_t* pold = D.pend + (int64_t(c) * 2 + X.sel) * D.pend_cap;
       uint64_t* out = D.pend + (int64_t(c) * 2 + (1 - X.sel)) * D.pend_cap;
-      if (lane == 0) {
+      if (X.cur >= X.end) {  // nothing pending from earlier epochs: copy
+        for (int i = lane; i < nin; i += 32) out[i] = in[i];
+        __syncwarp();
+        if (lane == 0) {
+          X.end = nin;
+          X.cur = 0;
+          X.sel = 1 - X.sel;
+        }
+      } else if (lane == 0) {
         int a = X.cur, bb = 0, o = 0;
         const int e = X.end;
         while (a < e && bb < nin) out[o++] = (pold[a] <= in[bb]) ? pold[a++] : in[bb++];
@@ -1376,31 +1389,37 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
       for (int f0 = tid - lane; f0 < stc_total; f0 += T) {
         const int f = f0 + lane;
         bool changed = false;
+        double dl = 0.0;
         if (f < stc_total) {
           const uint32_t loc = B.floc[f];
           const int k = int(loc >> 16);
           const McgSegSm& g = B.seg[k * A.n_stc_max + int(loc & 0xffffu)];
-          const McgKind& K = kc[k];
           const int c = c0 + k;
-          const bool late = K.prp_idx >= 0;
+          const bool late = g.late;
           double prp = 0.0;
           if (late) {
-            const double* SPb =
-                (K.n <= m) ? mcg_comp_block(A, B, k) + m : D.species + D.sp_off[c];
-            prp = SPb[K.prp_idx * K.n + g.comp];
+            if (g.prp_sm >= 0) {
+              prp = mcg_smem[g.prp_sm];
+            } else {
+              const McgKind& K = kc[k];
+              prp = D.species[D.sp_off[c] + K.prp_idx * K.n + g.comp];
+            }
           }
           McgStcVal v{B.stc[f], B.stc[S4 + f], B.stc[2 * S4 + f], B.stc[3 * S4 + f]};
           double delta = 0.0;
           changed = mcg_stc_step(specs[g.spec], D.dt, D.seed, D.gid0 + uint32_t(c), g.gi,
                                  f - cs[k].stc_off - g.start, s, late, prp, g.vol, g.rvol, v,
                                  delta);
-          B.dbuf[f] = delta;
+          dl = delta;
           B.stc[f] = v.h;
           B.stc[S4 + f] = v.z;
           B.stc[2 * S4 + f] = v.c;
           B.stc[3 * S4 + f] = v.a;
         }
+        // changed flags as a ballot; the block's changed deltas stored
+        // compacted in instance order (the fold walks them contiguously)
         const unsigned bal = __ballot_sync(MCG_FULL, changed);
+        if (changed) B.dbuf[f0 + __popc(bal & mcg_lanemask_lt())] = dl;
         if (lane == 0) B.fmask[f0 >> 5] = bal;
       }
     } else
@@ -1408,6 +1427,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
       McgStcVal v[4];
       int64_t jj[4];
       uint32_t loc[4];
+      double dlt[4];
   #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int f = (r0 + u) * T + tid;
@@ -1440,14 +1460,16 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
           const int li = f - cs[k].stc_off - g.start;
           changed = mcg_stc_step(specs[g.spec], D.dt, D.seed, D.gid0 + uint32_t(c), g.gi, li, s,
                                  late, prp, g.vol, g.rvol, v[u], delta);
-          B.dbuf[f] = delta;
+          dlt[u] = delta;
           D.i_stc_h[jj[u]] = v[u].h;
           D.i_stc_z[jj[u]] = v[u].z;
           D.i_stc_c[jj[u]] = v[u].c;
           if (changed) D.i_sps_abs[jj[u]] = v[u].a;
         }
         const unsigned bal = __ballot_sync(MCG_FULL, changed);
-        if (lane == 0) B.fmask[((r0 + u) * T + (tid - lane)) >> 5] = bal;
+        const int fw = (r0 + u) * T + (tid - lane);
+        if (changed) B.dbuf[fw + __popc(bal & mcg_lanemask_lt())] = dlt[u];
+        if (lane == 0) B.fmask[fw >> 5] = bal;
       }
     }
     MCG_PH(16);
@@ -1471,26 +1493,24 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
           // every instance of a placement sits on the placement's compartment
           double acc = sps[g.comp];
           while (f < fe) {
-            const int w = f >> 5;
-            uint32_t bits = B.fmask[w] >> (f & 31);
-            const int lim = min(32 - (f & 31), fe - f);
-            if (lim < 32) bits &= (1u << lim) - 1u;
-            // the adds stay in instance order; the loads of up to 8 changed
-            // slots are issued ahead of them
-            while (bits) {
-              double dv[8];
-              int cnt = 0;
-  #pragma unroll
-              for (int u = 0; u < 8; ++u)
-                if (bits) {
-                  dv[u] = B.dbuf[f + __ffs(bits) - 1];
-                  bits &= bits - 1;
-                  cnt = u + 1;
-                }
-  #pragma unroll
-              for (int u = 0; u < 8; ++u)
-                if (u < cnt) acc += dv[u];
+            // this 32-slot block's changed deltas of the segment: a contiguous
+            // run of the block's compacted deltas; the adds stay in instance order
+            const int w = f >> 5, lo = f & 31;
+            const int lim = min(32 - lo, fe - f);
+            const uint32_t bal = B.fmask[w];
+            const uint32_t m_lo = (1u << lo) - 1u;
+            const uint32_t m_hi = (lo + lim == 32) ? 0xffffffffu : ((1u << (lo + lim)) - 1u);
+            const double* p = B.dbuf + (w << 5);
+            int i = __popc(bal & m_lo);
+            const int i1 = __popc(bal & m_hi);
+            for (; i + 4 <= i1; i += 4) {
+              const double a0 = p[i], a1 = p[i + 1], a2 = p[i + 2], a3 = p[i + 3];
+              acc += a0;
+              acc += a1;
+              acc += a2;
+              acc += a3;
             }
+            for (; i < i1; ++i) acc += p[i];
             f += lim;
           }
           sps[g.comp] = acc;
