@@ -311,6 +311,39 @@ mcg_status mcg_device_math(int32_t device, int32_t func, const double* in, int64
 mcg_status mcg_er_connect(int32_t device, uint64_t seed, uint32_t n, double p, uint32_t src_begin,
                           uint32_t src_end, uint32_t* src, uint32_t* dst, int64_t* count);
 
+/* ---- standalone protocol drivers ------------------- */
+
+/* GbParams (mechanisms.hpp:80-92), field order as the reference's aggregate */
+typedef struct {
+  double tau_w_ms, w_star, gamma_p, gamma_d, theta_p, theta_d, sigma_pl, tau_c_ms;
+  double c_pre, c_post, t_c_delay_ms;
+} mcg_gb_params;
+/* GbPairingProtocol (mechanisms.hpp:276-283) */
+typedef struct {
+  int32_t n_pairs;
+  int32_t trials;
+  double period_ms, settle_ms, dt_ms;
+  uint64_t seed;
+} mcg_gb_protocol;
+/* GbCurvePoint (mechanisms.hpp:285-292) */
+typedef struct {
+  double delta_t_ms, mean_initial, mean_final, mean_change, change_ci_half, ratio;
+} mcg_gb_point;
+/* Every pairing trial of gb_pairing_trial (mechanisms.cpp:40-90) on the device,
+ * one thread per (delta, trial): w0[d * trials + t] and wf[...] are the initial
+ * and final weights of trial t at deltas[d] (delta_index = d). */
+mcg_status mcg_gb_trials(int32_t device, const mcg_gb_params* p, const double* deltas,
+                         int32_t n_deltas, const mcg_gb_protocol* proto, double* w0, double* wf);
+/* gb_dp_curve (mechanisms.cpp:92-119): the trials on the device, the per-delta
+ * means and confidence intervals (mean_ci, analysis.cpp:82-94) on the host in
+ * the reference's summation order. */
+mcg_status mcg_gb_dp_curve(int32_t device, const mcg_gb_params* p, const double* deltas,
+                           int32_t n_deltas, const mcg_gb_protocol* proto, mcg_gb_point* out);
+/* stdp_window (mechanisms.cpp:9-38) for n deltas, one thread per delta:
+ * out[i] = weight change per pair at deltas[i]. */
+mcg_status mcg_stdp_window(int32_t device, const mcg_stdp_params* p, const double* deltas,
+                           int32_t n, int32_t n_pairs, double period_ms, double* out);
+
 #ifdef __cplusplus
 }
 #endif

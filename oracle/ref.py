@@ -94,6 +94,13 @@ def lib():
             "ref_discretize": (C.c_int, [P(A.mcg_kind), C.c_int, vp, vp, vp, vp, vp]),
             "ref_run_stc_protocol": (C.c_int, [C.c_int, C.c_uint64, P(C.c_double),
                                                P(C.c_double), P(C.c_double)]),
+            "ref_gb_pairing_trial": (C.c_double, [P(A.mcg_gb_params), C.c_double,
+                                                  P(A.mcg_gb_protocol), C.c_uint64, C.c_uint64,
+                                                  P(C.c_double)]),
+            "ref_gb_dp_curve": (C.c_int, [P(A.mcg_gb_params), vp, C.c_int, P(A.mcg_gb_protocol),
+                                          vp]),
+            "ref_stdp_window": (C.c_double, [P(A.mcg_stdp_params), C.c_double, C.c_int,
+                                             C.c_double]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -271,3 +278,39 @@ def run_stc_protocol(proto, trial):
     h, z, p = C.c_double(), C.c_double(), C.c_double()
     _chk(lib().ref_run_stc_protocol(proto, trial, C.byref(h), C.byref(z), C.byref(p)))
     return h.value, z.value, p.value
+
+
+# ---- protocol drivers (mechanisms.cpp:9-119), the reference's own functions
+def _gb_structs(p, proto):
+    from dataclasses import fields
+    from paper_2411_16445_b200.protocols import GbParams
+    cp = A.mcg_gb_params(*[float(getattr(p, f.name)) for f in fields(GbParams)])
+    cq = A.mcg_gb_protocol(int(proto.n_pairs), int(proto.trials), float(proto.period_ms),
+                           float(proto.settle_ms), float(proto.dt_ms), int(proto.seed))
+    return cp, cq
+
+
+def gb_pairing_trial(p, delta_t_ms, proto, trial, delta_index=0):
+    """(final w, w0) of the reference's gb_pairing_trial."""
+    cp, cq = _gb_structs(p, proto)
+    w0 = C.c_double()
+    wf = lib().ref_gb_pairing_trial(C.byref(cp), float(delta_t_ms), C.byref(cq), trial,
+                                    delta_index, C.byref(w0))
+    return wf, w0.value
+
+
+def gb_dp_curve(p, deltas, proto):
+    """The reference's gb_dp_curve as a list of 6-tuples (GbCurvePoint fields)."""
+    cp, cq = _gb_structs(p, proto)
+    d = np.ascontiguousarray(deltas, np.float64)
+    out = (A.mcg_gb_point * max(d.size, 1))()
+    _chk(lib().ref_gb_dp_curve(C.byref(cp), d.ctypes.data, d.size, C.byref(cq), out))
+    return [tuple(getattr(out[i], f) for f, _ in A.mcg_gb_point._fields_) for i in range(d.size)]
+
+
+def stdp_window(delta_t_ms, p=None, n_pairs=60, period_ms=1000.0):
+    from paper_2411_16445_b200.recipe import StdpParams
+    p = p or StdpParams()
+    cp = A.mcg_stdp_params(p.tau_pre_ms, p.tau_post_ms, p.a_pre_uS, p.a_post_uS, p.w0_uS,
+                           p.wmax_uS)
+    return lib().ref_stdp_window(C.byref(cp), float(delta_t_ms), int(n_pairs), float(period_ms))

@@ -16,6 +16,7 @@
 #include "mcg.h"
 #include "mcsim/bench.hpp"
 #include "mcsim/engine.hpp"
+#include "mcsim/mechanisms.hpp"
 #include "mcsim/network.hpp"
 #include "mcsim/rng.hpp"
 #include "mcsim/tree_solver.hpp"
@@ -666,6 +667,61 @@ int ref_run_stc_protocol(int proto, uint64_t trial, double* h_final, double* z_f
     *z_final = r.z_final;
     *p_final = r.p_final;
   });
+}
+
+// gb_pairing_trial / gb_dp_curve / stdp_window (mechanisms.cpp:9-119)
+static GbParams gb_from(const mcg_gb_params* q) {
+  GbParams p;
+  p.tau_w_ms = q->tau_w_ms;
+  p.w_star = q->w_star;
+  p.gamma_p = q->gamma_p;
+  p.gamma_d = q->gamma_d;
+  p.theta_p = q->theta_p;
+  p.theta_d = q->theta_d;
+  p.sigma_pl = q->sigma_pl;
+  p.tau_c_ms = q->tau_c_ms;
+  p.c_pre = q->c_pre;
+  p.c_post = q->c_post;
+  p.t_c_delay_ms = q->t_c_delay_ms;
+  return p;
+}
+static GbPairingProtocol proto_from(const mcg_gb_protocol* q) {
+  GbPairingProtocol r;
+  r.n_pairs = q->n_pairs;
+  r.period_ms = q->period_ms;
+  r.settle_ms = q->settle_ms;
+  r.dt_ms = q->dt_ms;
+  r.trials = q->trials;
+  r.seed = q->seed;
+  return r;
+}
+double ref_gb_pairing_trial(const mcg_gb_params* p, double delta_t_ms, const mcg_gb_protocol* proto,
+                            uint64_t trial, uint64_t delta_index, double* w0) {
+  return gb_pairing_trial(gb_from(p), delta_t_ms, proto_from(proto), trial, delta_index, w0);
+}
+int ref_gb_dp_curve(const mcg_gb_params* p, const double* deltas, int n, const mcg_gb_protocol* proto,
+                    mcg_gb_point* out) {
+  return guard([&] {
+    const auto c = gb_dp_curve(gb_from(p), std::vector<double>(deltas, deltas + n), proto_from(proto));
+    for (int i = 0; i < n; ++i) {
+      out[i].delta_t_ms = c[i].delta_t_ms;
+      out[i].mean_initial = c[i].mean_initial;
+      out[i].mean_final = c[i].mean_final;
+      out[i].mean_change = c[i].mean_change;
+      out[i].change_ci_half = c[i].change_ci_half;
+      out[i].ratio = c[i].ratio;
+    }
+  });
+}
+double ref_stdp_window(const mcg_stdp_params* q, double delta_t_ms, int n_pairs, double period_ms) {
+  StdpParams p;
+  p.tau_pre_ms = q->tau_pre_ms;
+  p.tau_post_ms = q->tau_post_ms;
+  p.a_pre_uS = q->a_pre_uS;
+  p.a_post_uS = q->a_post_uS;
+  p.w0_uS = q->w0_uS;
+  p.wmax_uS = q->wmax_uS;
+  return stdp_window(delta_t_ms, p, n_pairs, period_ms);
 }
 
 }  // extern "C"

@@ -112,6 +112,22 @@ class mcg_stats(C.Structure):
                 ("advance_ms", C.c_double), ("advance_calls", C.c_int64)]
 
 
+class mcg_gb_params(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("tau_w_ms", "w_star", "gamma_p", "gamma_d", "theta_p",
+                                          "theta_d", "sigma_pl", "tau_c_ms", "c_pre", "c_post",
+                                          "t_c_delay_ms")]
+
+
+class mcg_gb_protocol(C.Structure):
+    _fields_ = [("n_pairs", C.c_int32), ("trials", C.c_int32), ("period_ms", C.c_double),
+                ("settle_ms", C.c_double), ("dt_ms", C.c_double), ("seed", C.c_uint64)]
+
+
+class mcg_gb_point(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("delta_t_ms", "mean_initial", "mean_final",
+                                          "mean_change", "change_ci_half", "ratio")]
+
+
 # field ids (mcg.h)
 FIELD = dict(v=0, species=1, hh_m=2, hh_h=3, hh_n=4, detector_prev_v=5, refractory_until=6,
              detector_armed=7, syn_comp=8, syn_weight=9, syn_kernel=10, stdp_a_pre=11,
@@ -126,7 +142,8 @@ EXPORTS = ("mcg_create", "mcg_destroy", "mcg_last_error", "mcg_abi_version", "mc
            "mcg_group_size", "mcg_cell_parent", "mcg_read_state", "mcg_write_state",
            "mcg_get_stats", "mcg_set_timing", "mcg_device_math",
            "mcg_er_connect", "mcg_shard_spike_cap", "mcg_shard_gid_begin", "mcg_shard_gid_end",
-           "mcg_shard_set_buffers", "mcg_shard_run_epoch", "mcg_partition")
+           "mcg_shard_set_buffers", "mcg_shard_run_epoch", "mcg_partition",
+           "mcg_gb_trials", "mcg_gb_dp_curve", "mcg_stdp_window")
 
 _lib = None
 
@@ -172,6 +189,12 @@ def _declare(L):
         "mcg_shard_set_buffers": (C.c_int32, [eng, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32]),
         "mcg_shard_run_epoch": (C.c_int32, [eng, C.c_double]),
         "mcg_partition": (C.c_int32, [P(mcg_recipe), C.c_int32, C.c_void_p]),
+        "mcg_gb_trials": (C.c_int32, [C.c_int32, P(mcg_gb_params), C.c_void_p, C.c_int32,
+                                      P(mcg_gb_protocol), C.c_void_p, C.c_void_p]),
+        "mcg_gb_dp_curve": (C.c_int32, [C.c_int32, P(mcg_gb_params), C.c_void_p, C.c_int32,
+                                        P(mcg_gb_protocol), C.c_void_p]),
+        "mcg_stdp_window": (C.c_int32, [C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
+                                        C.c_double, C.c_void_p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

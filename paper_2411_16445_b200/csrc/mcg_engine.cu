@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "mcg_batch.cuh"
+#include "mcg_protocols.cuh"
 #include "mcg_build.h"
 
 namespace mcg {
@@ -1343,5 +1344,172 @@ extern "C" mcg_status mcg_er_connect(int32_t device, uint64_t seed, uint32_t n, 
     cudaFree(d_cnt);
     cudaFree(d_off);
     *count = total;
+  });
+}
+
+// ---- standalone protocol drivers (mcg_protocols.cuh) ------------------------------
+namespace {
+// the calcium jump schedule of gb_pairing_trial (mechanisms.cpp:46-58), sorted
+// with the same std::sort call; returns n_steps (:60-61)
+int64_t gb_schedule(const mcg_gb_params& p, double delta_t_ms, const mcg_gb_protocol& proto,
+                    std::vector<std::pair<int64_t, double>>& jumps) {
+  const double dt = proto.dt_ms;
+  const auto step_of = [dt](double t) { return static_cast<int64_t>(std::ceil(t / dt - 1e-9)); };
+  jumps.clear();
+  jumps.reserve(2 * proto.n_pairs);
+  const double t0 = 100.0 + std::max(0.0, -delta_t_ms);
+  for (int k = 0; k < proto.n_pairs; ++k) {
+    const double t_pre = t0 + k * proto.period_ms;
+    jumps.emplace_back(step_of(t_pre + p.t_c_delay_ms), p.c_pre);
+    jumps.emplace_back(step_of(t_pre + delta_t_ms), p.c_post);
+  }
+  std::sort(jumps.begin(), jumps.end(),
+            [](const auto& a, const auto& b) { return a.first < b.first; });
+  return step_of(t0 + proto.n_pairs * proto.period_ms + proto.settle_ms);
+}
+}  // namespace
+
+extern "C" mcg_status mcg_gb_trials(int32_t device, const mcg_gb_params* p, const double* deltas,
+                                    int32_t n_deltas, const mcg_gb_protocol* proto, double* w0,
+                                    double* wf) {
+  return guarded([&] {
+    using mcg::cuda_check;
+    if (!p || !proto || (n_deltas > 0 && (!deltas || !w0 || !wf)))
+      throw mcg::Error(MCG_ERR_ARGUMENT, "gb_trials: null argument");
+    if (n_deltas <= 0 || proto->trials <= 0) return;
+    if (!(proto->dt_ms > 0)) throw mcg::Error(MCG_ERR_ARGUMENT, "gb_trials: dt must be positive");
+    CK(cudaSetDevice(device));
+    std::vector<int64_t> jstep, nsteps(n_deltas);
+    std::vector<double> jamt;
+    std::vector<int32_t> joff(n_deltas + 1, 0);
+    std::vector<std::pair<int64_t, double>> jumps;
+    for (int d = 0; d < n_deltas; ++d) {
+      nsteps[d] = gb_schedule(*p, deltas[d], *proto, jumps);
+      for (const auto& j : jumps) {
+        jstep.push_back(j.first);
+        jamt.push_back(j.second);
+      }
+      joff[d + 1] = static_cast<int32_t>(jstep.size());
+    }
+    McgGbDev P{};
+    P.tau_w = p->tau_w_ms;
+    P.w_star = p->w_star;
+    P.gamma_p = p->gamma_p;
+    P.gamma_d = p->gamma_d;
+    P.theta_p = p->theta_p;
+    P.theta_d = p->theta_d;
+    P.sigma = p->sigma_pl;
+    P.r_tau_w = mcg::mcg_recip(p->tau_w_ms);
+    P.cdecay = std::exp(-proto->dt_ms / p->tau_c_ms);
+    P.nz1 = p->sigma_pl * std::sqrt(double(1) / p->tau_w_ms) * std::sqrt(proto->dt_ms);
+    P.nz2 = p->sigma_pl * std::sqrt(double(2) / p->tau_w_ms) * std::sqrt(proto->dt_ms);
+    P.dt = proto->dt_ms;
+    P.seed = proto->seed;
+    P.trials = proto->trials;
+    P.n_deltas = n_deltas;
+    const int64_t nt = int64_t(proto->trials) * n_deltas;
+    mcg::DBuf<int64_t> d_js, d_ns;
+    mcg::DBuf<double> d_ja, d_w0, d_wf;
+    mcg::DBuf<int32_t> d_jo;
+    d_js.upload(jstep, 0);
+    d_ja.upload(jamt, 0);
+    d_jo.upload(joff, 0);
+    d_ns.upload(nsteps, 0);
+    d_w0.alloc(nt);
+    d_wf.alloc(nt);
+    k_gb_trials<<<static_cast<unsigned>((nt + 127) / 128), 128>>>(P, d_js.p, d_ja.p, d_jo.p, d_ns.p,
+                                                                   d_w0.p, d_wf.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(w0, d_w0.p, nt * sizeof(double), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(wf, d_wf.p, nt * sizeof(double), cudaMemcpyDeviceToHost));
+  });
+}
+
+extern "C" mcg_status mcg_gb_dp_curve(int32_t device, const mcg_gb_params* p, const double* deltas,
+                                      int32_t n_deltas, const mcg_gb_protocol* proto,
+                                      mcg_gb_point* out) {
+  if (!proto || !out || n_deltas < 0) {
+    mcg::g_last_error = "gb_dp_curve: null argument";
+    return MCG_ERR_ARGUMENT;
+  }
+  const int T = proto->trials;
+  std::vector<double> w0(size_t(std::max(T, 0)) * std::max(n_deltas, 0)), wf(w0.size());
+  const mcg_status st = mcg_gb_trials(device, p, deltas, n_deltas, proto, w0.data(), wf.data());
+  if (st != MCG_OK) return st;
+  // gb_dp_curve's reductions (mechanisms.cpp:99-116) and mean_ci (analysis.cpp:82-94)
+  for (int d = 0; d < n_deltas; ++d) {
+    std::vector<double> change(T);
+    double sum_w0 = 0, sum_wf = 0;
+    for (int tr = 0; tr < T; ++tr) {
+      const double a = w0[size_t(d) * T + tr], b = wf[size_t(d) * T + tr];
+      change[tr] = b - a;
+      sum_w0 += a;
+      sum_wf += b;
+    }
+    double mean = 0, half = 0;
+    if (T > 0) {
+      for (double s : change) mean += s;
+      mean /= T;
+      if (T >= 2) {
+        double var = 0;
+        for (double s : change) var += (s - mean) * (s - mean);
+        var /= (T - 1);
+        half = 1.959963984540054 * std::sqrt(var / T);
+      }
+    }
+    mcg_gb_point& pt = out[d];
+    pt.delta_t_ms = deltas[d];
+    pt.mean_initial = sum_w0 / T;
+    pt.mean_final = sum_wf / T;
+    pt.mean_change = mean;
+    pt.change_ci_half = half;
+    pt.ratio = pt.mean_initial != 0 ? pt.mean_final / pt.mean_initial : 0.0;
+  }
+  return MCG_OK;
+}
+
+extern "C" mcg_status mcg_stdp_window(int32_t device, const mcg_stdp_params* p,
+                                      const double* deltas, int32_t n, int32_t n_pairs,
+                                      double period_ms, double* out) {
+  return guarded([&] {
+    using mcg::cuda_check;
+    if (!p || (n > 0 && (!deltas || !out))) throw mcg::Error(MCG_ERR_ARGUMENT, "stdp_window: null argument");
+    if (n <= 0) return;
+    CK(cudaSetDevice(device));
+    // the pairing events of stdp_window (mechanisms.cpp:12-24), stable-sorted
+    struct Ev {
+      double t;
+      bool pre;
+    };
+    std::vector<double> et;
+    std::vector<uint8_t> ep;
+    std::vector<int32_t> eo(n + 1, 0);
+    for (int i = 0; i < n; ++i) {
+      const double delta_t_ms = deltas[i];
+      std::vector<Ev> events;
+      events.reserve(2 * n_pairs);
+      const double t0 = std::max(0.0, -delta_t_ms);
+      for (int k = 0; k < n_pairs; ++k) {
+        events.push_back({t0 + k * period_ms, true});
+        events.push_back({t0 + k * period_ms + delta_t_ms, false});
+      }
+      std::stable_sort(events.begin(), events.end(), [](const Ev& a, const Ev& b) { return a.t < b.t; });
+      for (const Ev& e : events) {
+        et.push_back(e.t);
+        ep.push_back(e.pre ? 1 : 0);
+      }
+      eo[i + 1] = static_cast<int32_t>(et.size());
+    }
+    McgStdpDev P{p->tau_pre_ms, p->tau_post_ms, p->a_pre_uS, p->a_post_uS, p->w0_uS, n, n_pairs};
+    mcg::DBuf<double> d_t, d_out;
+    mcg::DBuf<uint8_t> d_p;
+    mcg::DBuf<int32_t> d_o;
+    d_t.upload(et, 0);
+    d_p.upload(ep, 0);
+    d_o.upload(eo, 0);
+    d_out.alloc(n);
+    k_stdp_window<<<(n + 127) / 128, 128>>>(P, d_t.p, d_p.p, d_o.p, d_out.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(out, d_out.p, n * sizeof(double), cudaMemcpyDeviceToHost));
   });
 }

@@ -106,8 +106,8 @@ __global__ void bench_chain(int reps, long long* cyc, const double* g_init) {
   int32_t* PI = reinterpret_cast<int32_t*>(S);
   const int n = 31, lp = 20, P = 2 * lp + 1;
   const int idx = 0;                  // int32 units, P ints
-  const int fc = 64;                  // doubles: f|c|d|y each P
-  const int r2c = fc + 4 * P + 8, x = r2c + P + 8, cap = x + n + 8;
+  const int fc = 64;                  // doubles: f|c|d|y|cap|glr each P
+  const int r2c = fc + 6 * P + 8, x = r2c + P + 8, cap = x + n + 8;
   if (threadIdx.x == 0) {
     for (int p = 0; p < P; ++p) PI[idx + p] = -1;
     int k = 0;
@@ -123,12 +123,14 @@ __global__ void bench_chain(int reps, long long* cyc, const double* g_init) {
       S[fc + P + p] = i < 0 ? 0.0 : g_init[2 * n + i];
       S[fc + 2 * P + p] = i < 0 ? 1.0 : g_init[n + i];
       S[fc + 3 * P + p] = i < 0 ? 1.0 : 1.0 / g_init[n + i];
+      S[fc + 4 * P + p] = i < 0 ? 0.0 : g_init[3 * n + i];
+      S[fc + 5 * P + p] = i < 0 ? 0.0 : 0.25;
       S[r2c + p] = i < 0 ? 0.0 : 1.5;
     }
     for (int i = 0; i < n; ++i) S[x + i] = -65.0 + i;
   }
   __syncthreads();
-  McgChainLane L{threadIdx.x < 2, int(threadIdx.x & 1), lp, r2c, fc, idx, x, 0};
+  McgChainLane L{threadIdx.x < 2, int(threadIdx.x & 1), lp, r2c, fc, idx, x, 0, 1, -1, -1, 0.0};
   long long t0 = clock64();
   for (int r = 0; r < reps; ++r) {
     mcg_chain_lane(L);
