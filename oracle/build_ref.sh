@@ -29,4 +29,5 @@ for p in "${pids[@]:-}"; do [ -n "$p" ] && wait "$p"; done
 $CXX -shared -o "$OUT/libmcsim_ref.so.tmp" "${objs[@]}" -lpthread -lm
 mv "$OUT/libmcsim_ref.so.tmp" "$OUT/libmcsim_ref.so"
 gcc -O2 -fPIC -shared "$HERE/glibc_eval.c" -o "$OUT/libglibc_eval.so" -lm
+$CXX -std=c++20 -O2 -I"$REF/include" "$HERE/ref_csv.cpp" "$OUT/obj/csvio.o" -o "$OUT/ref_csv"
 echo "built $OUT/libmcsim_ref.so"

@@ -314,3 +314,31 @@ def stdp_window(delta_t_ms, p=None, n_pairs=60, period_ms=1000.0):
     cp = A.mcg_stdp_params(p.tau_pre_ms, p.tau_post_ms, p.a_pre_uS, p.a_post_uS, p.w0_uS,
                            p.wmax_uS)
     return lib().ref_stdp_window(C.byref(cp), float(delta_t_ms), int(n_pairs), float(period_ms))
+
+
+# the reference's CSV writers (csvio.cpp) run as a small executable built from
+# its own sources (oracle/ref_csv.cpp): in-process iostreams of the statically
+# linked C++ runtime of libmcsim_ref.so do not survive inside Python
+CSV_EXE = os.path.join(os.path.dirname(LIB_PATH), "ref_csv")
+
+
+def _ref_csv(kind, path, a, b, b_dtype):
+    import subprocess
+    import tempfile
+    a = np.ascontiguousarray(a, np.float64)
+    b = np.ascontiguousarray(b, b_dtype)
+    with tempfile.NamedTemporaryFile(suffix=".bin", delete=False) as f:
+        f.write(np.int64(a.size).tobytes() + a.tobytes() + b.tobytes())
+        name = f.name
+    try:
+        subprocess.run([CSV_EXE, kind, name, path], check=True)
+    finally:
+        os.unlink(name)
+
+
+def write_spikes_csv(path, t_s, gid):
+    _ref_csv("spikes", path, t_s, gid, np.uint32)
+
+
+def write_trace_csv(path, t_s, v):
+    _ref_csv("trace", path, t_s, v, np.float64)

@@ -203,6 +203,20 @@ class Engine:
                                     g.ctypes.data_as(C.c_void_p)))
         return t, g
 
+    def write_spikes_csv(self, path: str) -> None:
+        """spikes.csv of the run so far: times in seconds (t_ms * 1e-3, as the
+        reference's drivers convert, network.cpp:104), rows by (t, gid),
+        %.17g (csvio.cpp:58-69)."""
+        from .csvio import write_spikes_csv
+        t, g = self.spike_arrays()
+        write_spikes_csv(path, t * 1e-3, g)
+
+    def write_trace_csv(self, probe: int, path: str) -> None:
+        """One probe's trace as time_s,value (csvio.cpp:34-39), t_ms * 1e-3."""
+        from .csvio import write_trace_csv
+        t, v = self.trace_arrays(probe)
+        write_trace_csv(path, t * 1e-3, v)
+
     def spikes(self) -> List[SpikeRecord]:
         t, g = self.spike_arrays()
         return [SpikeRecord(float(a), int(b)) for a, b in zip(t, g)]
