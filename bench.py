@@ -189,6 +189,65 @@ def run_reference_arm(args):
     return 0
 
 
+def other_configs():
+    """Secondary measurements of the same run (not the headline): the
+    north-star 4000-neuron network, config 5 (100k cells x 48 comps, in-degree
+    of config 3) on one GPU with its HBM roofline, and the acceptance-3
+    pairing curve (gb_dp_curve, 13 deltas x 4000 trials, dt 0.05 ms) on the
+    device.  Device-timed (engine CUDA events) over a window after warm-up."""
+    import time as _t
+    from paper_2411_16445_b200 import Engine, EngineOptions
+    from paper_2411_16445_b200 import network as N
+    from paper_2411_16445_b200 import protocols as PR
+    out = {}
+    peak, _ = measured_peak_hbm()
+    for name, n, dend, t_warm, t_end in (("target_4000", 4000, N.DendriteSize.small_dendrites, 500.0, 2500.0),
+                                         ("config5_100k", 100000, N.DendriteSize.large_dendrites, 100.0, 600.0)):
+        ne = n * 4 // 5
+        c = N.ConsolidationConfig(n_cells=n, n_exc=ne, p_conn=min(0.1, 0.1 * 1600 / ne), seed=SEED,
+                                  multi_compartment=True, dend_size=dend, dt_ms=DT_MS)
+        t0 = _t.perf_counter()
+        b = N.build_consolidation_network(c, True)
+        e = Engine(b.recipe, EngineOptions(DT_MS, SEED))
+        setup = _t.perf_counter() - t0
+        e.set_timing(True)
+        e.advance_to(t_warm)
+        s0 = e.stats()
+        e.advance_to(t_end)
+        s1 = e.stats()
+        sec = (s1["advance_ms"] - s0["advance_ms"]) * 1e-3
+        steps = s1["steps"] - s0["steps"]
+        ev = (s1["events_delivered"] - s0["events_delivered"]) / max(steps, 1)
+        bstep = (16 * s1["total_comps"] + 16 * s1["species_comps"] + 64 * s1["stc_synapses"]
+                 + 48 * s1["hh_comps"] + 32 * ev + 24 * n)
+        ach = bstep * steps / sec / 1e9
+        out[name] = {"n_cells": n, "compartments": s1["total_comps"], "stc_synapses": s1["stc_synapses"],
+                     "p_conn": c.p_conn, "bio_ms": t_end - t_warm,
+                     "sim_s_per_wall_s": (t_end - t_warm) * 1e-3 / sec,
+                     "us_per_fine_step": 1e6 * sec / steps,
+                     "compartment_updates_per_s": s1["total_comps"] * steps / sec,
+                     "faster_than_real_time": (t_end - t_warm) * 1e-3 / sec > 1.0,
+                     "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                                  "frac": ach / peak, "bytes_per_fine_step": bstep},
+                     "setup_s": setup}
+        e.close()
+        del b
+    p = PR.GbParams()
+    deltas = [-100.0, -50.0, -30.0, -20.0, -10.0, -5.0, 0.0, 5.0, 10.0, 20.0, 30.0, 50.0, 100.0]
+    proto = PR.GbPairingProtocol(dt_ms=0.05, trials=4000, seed=999)
+    import torch
+    torch.cuda.synchronize()
+    t0 = _t.perf_counter()
+    curve = [PR.gb_dp_curve(p, [d], proto)[0] for d in deltas]  # acceptance.cpp:131
+    wall = _t.perf_counter() - t0
+    n_steps = int(math.ceil((100.0 + 100.0 + 60 * 1000.0 + 5000.0) / 0.05))
+    out["gb_dp_curve_acceptance3"] = {"deltas": len(deltas), "trials": proto.trials, "dt_ms": proto.dt_ms,
+                                      "wall_s": wall,
+                                      "trial_steps_per_s": len(deltas) * proto.trials * n_steps / wall,
+                                      "mean_change": [pt.mean_change for pt in curve]}
+    return out
+
+
 def run_gpu_arm(args):
     import numpy as np
     import torch
@@ -270,6 +329,8 @@ def run_gpu_arm(args):
     if rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline(flat.view, args.cpu_sample_ms)
 
+    other = None if args.no_other else other_configs()
+
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
@@ -289,6 +350,7 @@ def run_gpu_arm(args):
         "clocks": clk,
         "batch_kernel_share": kern_ms * 1e-3 / total,
         "wall_ms_per_step": 1e3 * wall_total / args.steps,
+        "other_configs": other,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -409,6 +471,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-sample-ms", type=float, default=2000.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other", action="store_true", help="skip the secondary configurations")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
