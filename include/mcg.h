@@ -311,6 +311,16 @@ mcg_status mcg_device_math(int32_t device, int32_t func, const double* in, int64
 mcg_status mcg_er_connect(int32_t device, uint64_t seed, uint32_t n, double p, uint32_t src_begin,
                           uint32_t src_end, uint32_t* src, uint32_t* dst, int64_t* count);
 
+/* ---- checkpoints ----------------------------------- */
+
+/* Engine::make_checkpoint + Checkpoint::serialize (engine.cpp:1070-1093,
+ * 1150-1233): the engine's state as MCSCKPT1 bytes, byte-identical to the
+ * reference's for the same run.  buf == NULL: *size only. */
+mcg_status mcg_checkpoint(mcg_engine* eng, uint8_t* buf, int64_t cap, int64_t* size);
+/* Checkpoint::deserialize + Engine::restore (engine.cpp:1095-1140, 1235-1325);
+ * accepts the reference's checkpoints (same validation and messages). */
+mcg_status mcg_restore(mcg_engine* eng, const uint8_t* buf, int64_t size);
+
 /* ---- standalone protocol drivers ------------------- */
 
 /* GbParams (mechanisms.hpp:80-92), field order as the reference's aggregate */

@@ -101,6 +101,8 @@ def lib():
                                           vp]),
             "ref_stdp_window": (C.c_double, [P(A.mcg_stdp_params), C.c_double, C.c_int,
                                              C.c_double]),
+            "ref_make_checkpoint": (C.c_int, [vp, vp, C.c_int64, P(C.c_int64)]),
+            "ref_restore": (C.c_int, [vp, vp, C.c_int64]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -210,6 +212,17 @@ class RefEngine:
 
     def clear_spikes(self):
         lib().ref_clear_spikes(self._h)
+
+    def make_checkpoint(self) -> bytes:
+        n = C.c_int64()
+        _chk(lib().ref_make_checkpoint(self._h, None, 0, C.byref(n)))
+        buf = (C.c_uint8 * max(n.value, 1))()
+        _chk(lib().ref_make_checkpoint(self._h, buf, n.value, C.byref(n)))
+        return bytes(buf)[:n.value]
+
+    def restore(self, data: bytes):
+        buf = (C.c_uint8 * max(len(data), 1)).from_buffer_copy(bytes(data) or b"\0")
+        _chk(lib().ref_restore(self._h, buf, len(data)))
 
     def trace_arrays(self, p):
         n = lib().ref_trace_len(self._h, p)

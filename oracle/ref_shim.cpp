@@ -8,6 +8,7 @@
 // both engines run the reference's own topology.  Only tests/, smoke() and
 // bench.py's cpu_baseline / --impl reference legs may load this library.
 #include <cstring>
+#include <span>
 #include <map>
 #include <memory>
 #include <string>
@@ -722,6 +723,23 @@ double ref_stdp_window(const mcg_stdp_params* q, double delta_t_ms, int n_pairs,
   p.w0_uS = q->w0_uS;
   p.wmax_uS = q->wmax_uS;
   return stdp_window(delta_t_ms, p, n_pairs, period_ms);
+}
+
+// Engine::make_checkpoint + serialize / deserialize + restore (engine.cpp:1036-1325)
+int ref_make_checkpoint(ref_engine* e, uint8_t* buf, int64_t cap, int64_t* size) {
+  return guard([&] {
+    const auto b = e->eng->make_checkpoint().serialize();
+    *size = static_cast<int64_t>(b.size());
+    if (buf) {
+      if (cap < *size) throw EngineError("checkpoint: buffer too small");
+      std::memcpy(buf, b.data(), b.size());
+    }
+  });
+}
+int ref_restore(ref_engine* e, const uint8_t* buf, int64_t size) {
+  return guard([&] {
+    e->eng->restore(Checkpoint::deserialize(std::span<const uint8_t>(buf, static_cast<size_t>(size))));
+  });
 }
 
 }  // extern "C"

@@ -5,7 +5,7 @@ reference (proj/src/engine.cpp) — runs as hand-written sm_100a kernels behind
 the C ABI in include/mcg.h.  This package is the host-side mirror of the
 reference's Recipe / Engine API plus its network builders.
 """
-from .engine import CellView, Engine, EngineOptions, GroupView, SpikeRecord  # noqa: F401
+from .engine import CellView, Checkpoint, Engine, EngineOptions, GroupView, SpikeRecord  # noqa: F401
 from .recipe import (CellKindSpec, ConnectionSpec, ConnectionTable, EngineError,  # noqa: F401
                      HhMembrane, HomeostasisParams, LifMembrane, MorphologyError, NoMembrane,
                      NumericError, PlacementSpec, PoissonSource, PoissonWindow, ProbeSpec,

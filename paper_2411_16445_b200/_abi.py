@@ -143,7 +143,7 @@ EXPORTS = ("mcg_create", "mcg_destroy", "mcg_last_error", "mcg_abi_version", "mc
            "mcg_get_stats", "mcg_set_timing", "mcg_device_math",
            "mcg_er_connect", "mcg_shard_spike_cap", "mcg_shard_gid_begin", "mcg_shard_gid_end",
            "mcg_shard_set_buffers", "mcg_shard_run_epoch", "mcg_partition",
-           "mcg_gb_trials", "mcg_gb_dp_curve", "mcg_stdp_window")
+           "mcg_gb_trials", "mcg_gb_dp_curve", "mcg_stdp_window", "mcg_checkpoint", "mcg_restore")
 
 _lib = None
 
@@ -189,6 +189,8 @@ def _declare(L):
         "mcg_shard_set_buffers": (C.c_int32, [eng, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32]),
         "mcg_shard_run_epoch": (C.c_int32, [eng, C.c_double]),
         "mcg_partition": (C.c_int32, [P(mcg_recipe), C.c_int32, C.c_void_p]),
+        "mcg_checkpoint": (C.c_int32, [eng, C.c_void_p, C.c_int64, P(C.c_int64)]),
+        "mcg_restore": (C.c_int32, [eng, C.c_void_p, C.c_int64]),
         "mcg_gb_trials": (C.c_int32, [C.c_int32, P(mcg_gb_params), C.c_void_p, C.c_int32,
                                       P(mcg_gb_protocol), C.c_void_p, C.c_void_p]),
         "mcg_gb_dp_curve": (C.c_int32, [C.c_int32, P(mcg_gb_params), C.c_void_p, C.c_int32,

@@ -168,15 +168,17 @@ struct McgCellSm {
   int8_t gseg[8];           // per group: STC segment index (-1: none)
 };
 
-// one staged event (16 B): network events carry the weight (static charge:
+// one staged event (24 B): network events carry the weight (static charge:
 // weight x charge factor, the product apply_event forms) and the target
 // compartment; delayed-calcium events only their group and instance
 struct McgEvSm {
   double w;
   uint32_t inst;            // | 0x80000000 when the raw weight is nonzero
+  uint32_t src;             // EventRec.src (kept in delayed-calcium entries for checkpoints)
   uint16_t comp;
   uint8_t group;
   uint8_t so;               // step - s0
+  uint32_t pad;
 };
 
 // one STC group of a cell, in group order
@@ -735,6 +737,8 @@ __device__ bool mcg_stage_events(const McgDev& D, const McgBatchArgs& A, const M
       e.w = w * D.k_cf[K.arr + comp];
     }
     e.inst = inst | (w != 0.0 ? 0x80000000u : 0u);
+    e.src = D.e_src[r];
+    e.pad = 0;
     B.evb[beg + t] = e;
   }
   // delayed calcium: one segment's entries in queue order, or a merge by seq
@@ -753,6 +757,8 @@ __device__ bool mcg_stage_events(const McgDev& D, const McgBatchArgs& A, const M
           McgEvSm e;
           e.w = 0.0;
           e.inst = uint32_t(D.fifo_si[slot] & 0xffffffffu);
+          e.src = 0;
+          e.pad = 0;
           e.comp = 0;
           e.group = static_cast<uint8_t>(g.gi);
           e.so = static_cast<uint8_t>(D.fifo_step[slot] - s0);
@@ -791,6 +797,8 @@ __device__ bool mcg_stage_events(const McgDev& D, const McgBatchArgs& A, const M
       McgEvSm e;
       e.w = 0.0;
       e.inst = uint32_t(D.fifo_si[slot] & 0xffffffffu);
+          e.src = 0;
+          e.pad = 0;
       e.comp = 0;
       e.group = static_cast<uint8_t>(g.gi);
       e.so = static_cast<uint8_t>(bst - s0);
@@ -1272,6 +1280,8 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
               const int64_t slot = g.f_base + (g.f_tail % g.f_cap);
               D.fifo_step[slot] = s + S.ca_delay;
               D.fifo_si[slot] = (uint64_t(X.iseq) << 32) | uint64_t(inst);
+              D.fifo_src[slot] = E.src;
+              D.fifo_w[slot] = E.w;
               ++g.f_tail;
             }
             ++X.iseq;
@@ -1302,7 +1312,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
             const int64_t r = int64_t(key & rank_mask);
             const int32_t grp = D.e_group[r];
             mcg_apply_event(D, K, c, cg0, V, grp, D.e_inst[r], D.e_weight[r], 0, refractory, s,
-                            mcg_stc_ref(A, B, tid, grp));
+                            mcg_stc_ref(A, B, tid, grp), D.e_src[r]);
             ++cur;
             ++X.ndel;
             key = (cur < X.end) ? pend[cur] : ~0ull;

@@ -610,6 +610,8 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
   m.e_inst.resize(ne);
   m.e_weight.resize(ne);
   m.e_delay.resize(ne);
+  m.e_src.resize(ne);
+  m.e_seq.resize(ne);
   m.out_begin.assign(r.n_cells, 0);
   m.out_end.assign(r.n_cells, 0);
   std::vector<std::vector<int64_t>> src_lists(r.n_sources);
@@ -620,6 +622,8 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
     m.e_inst[i] = e.inst;
     m.e_weight[i] = e.w;
     m.e_delay[i] = e.delay;
+    m.e_src[i] = e.src_key;
+    m.e_seq[i] = e.seq;
     m.max_delay_steps = std::max(m.max_delay_steps, e.delay);
     if (e.source < 0) {
       if (m.out_end[e.src_key] == 0 && m.out_begin[e.src_key] == 0) m.out_begin[e.src_key] = i;

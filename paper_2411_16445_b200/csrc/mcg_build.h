@@ -93,6 +93,7 @@ struct HostModel {
   std::vector<int32_t> e_dst, e_group;
   std::vector<uint32_t> e_inst;
   std::vector<double> e_weight;
+  std::vector<uint32_t> e_src, e_seq;       // EventRec.src / seq of each edge (EventOrder)
   std::vector<int64_t> e_delay;
   std::vector<int64_t> out_begin, out_end;  // per global gid
   std::vector<int64_t> src_edge_off;        // per source CSR into src_edges

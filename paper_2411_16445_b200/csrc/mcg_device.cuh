@@ -58,6 +58,8 @@ struct McgDev {
   McgFifo* fifos;
   int64_t* fifo_step;
   uint64_t* fifo_si;
+  uint32_t* fifo_src;         // the originating event's src and weight, kept for
+  double* fifo_w;             // checkpoints (the reference's internal EventRec copies them)
   const int32_t* i_comp;
   double *i_weight, *i_kernel;
   int32_t* i_active;
@@ -82,6 +84,7 @@ struct McgDev {
   const int32_t* e_group;
   const uint32_t* e_inst;
   const double* e_weight;
+  const uint32_t* e_src;      // EventRec.src of each edge (gid, 0xFFFFFFFF for sources)
   const int64_t* e_delay;
   // spikes of this epoch: [cell][sp_cap]
   int32_t sp_cap;
@@ -146,7 +149,8 @@ struct McgStcSm {
 // ---- apply_events (engine.cpp:452-513); lane 0 only -----------------------
 __device__ void mcg_apply_event(const McgDev& D, const McgKind& K, int c, int64_t cg0,
                                 double* V, int32_t group, uint32_t inst, double w, int etype,
-                                bool refractory, int64_t s, McgStcSm R = McgStcSm{nullptr, 0, -1}) {
+                                bool refractory, int64_t s, McgStcSm R = McgStcSm{nullptr, 0, -1},
+                                uint32_t src = 0) {
   McgCellGroup& G = D.cgs[cg0 + group];
   const McgSpec& S = D.specs[G.spec];
   const int64_t j = G.inst + inst;
@@ -214,6 +218,8 @@ __device__ void mcg_apply_event(const McgDev& D, const McgKind& K, int c, int64_
           const int64_t slot = F.base + (F.tail % F.cap);
           D.fifo_step[slot] = s + S.ca_delay;
           D.fifo_si[slot] = (uint64_t(D.internal_seq[c]) << 32) | uint64_t(inst);
+          D.fifo_src[slot] = src;
+          D.fifo_w[slot] = w;
           ++F.tail;
         }
         ++D.internal_seq[c];

@@ -20,9 +20,11 @@
 #include <memory>
 #include <string>
 #include <vector>
+#include <unordered_map>
 
 #include "mcg_batch.cuh"
 #include "mcg_protocols.cuh"
+#include "mcg_checkpoint.h"
 #include "mcg_build.h"
 
 namespace mcg {
@@ -117,6 +119,8 @@ struct Engine {
   DBuf<McgFifo> d_fifos;
   DBuf<int64_t> d_fifo_step;
   DBuf<uint64_t> d_fifo_si;
+  DBuf<uint32_t> d_fifo_src;
+  DBuf<double> d_fifo_w;
   DBuf<int32_t> d_i_comp, d_i_active;
   DBuf<double> d_i_weight, d_i_kernel, d_i_stdp_pre, d_i_stdp_post, d_i_stdp_w, d_i_homeo_w,
       d_i_stc_h, d_i_stc_z, d_i_stc_c, d_i_sps_abs;
@@ -125,6 +129,7 @@ struct Engine {
   DBuf<int32_t> d_e_dst, d_e_group;
   DBuf<uint32_t> d_e_inst;
   DBuf<double> d_e_weight;
+  DBuf<uint32_t> d_e_src;
   DBuf<int64_t> d_e_delay, d_out_begin, d_out_end, d_src_edge_off, d_src_edges;
   int32_t rank_bits = 1;
   // sources
@@ -411,6 +416,8 @@ struct Engine {
     d_fifos.upload(m.fifos, st);
     d_fifo_step.alloc(std::max<int64_t>(m.fifo_total, 1));
     d_fifo_si.alloc(std::max<int64_t>(m.fifo_total, 1));
+    d_fifo_src.alloc(std::max<int64_t>(m.fifo_total, 1));
+    d_fifo_w.alloc(std::max<int64_t>(m.fifo_total, 1));
     d_i_comp.upload(m.i_comp, st);
     d_i_active.alloc(std::max<size_t>(m.i_comp.size(), 1));
     d_i_weight.upload(m.i_weight, st);
@@ -428,6 +435,7 @@ struct Engine {
     d_e_group.upload(m.e_group, st);
     d_e_inst.upload(m.e_inst, st);
     d_e_weight.upload(m.e_weight, st);
+    d_e_src.upload(m.e_src, st);
     d_e_delay.upload(m.e_delay, st);
     d_out_begin.upload(m.out_begin, st);
     d_out_end.upload(m.out_end, st);
@@ -605,6 +613,8 @@ struct Engine {
     D.fifos = d_fifos.p;
     D.fifo_step = d_fifo_step.p;
     D.fifo_si = d_fifo_si.p;
+    D.fifo_src = d_fifo_src.p;
+    D.fifo_w = d_fifo_w.p;
     D.i_comp = d_i_comp.p;
     D.i_weight = d_i_weight.p;
     D.i_kernel = d_i_kernel.p;
@@ -633,6 +643,7 @@ struct Engine {
     D.e_group = d_e_group.p;
     D.e_inst = d_e_inst.p;
     D.e_weight = d_e_weight.p;
+    D.e_src = d_e_src.p;
     D.e_delay = d_e_delay.p;
     D.sp_cap = sp_cap;
     D.sp_count = d_sp_count.p;
@@ -1056,6 +1067,332 @@ struct Engine {
       default: throw Error(MCG_ERR_ARGUMENT, "unknown field");
     }
   }
+
+  // ---- checkpoints (engine.cpp:1036-1325) ----------------------------------
+  template <class T>
+  std::vector<T> download(const DBuf<T>& b, size_t n) {
+    std::vector<T> h(n);
+    if (n) CK(cudaMemcpyAsync(h.data(), b.p, n * sizeof(T), cudaMemcpyDeviceToHost, st));
+    return h;
+  }
+  template <class T>
+  void upload_to(DBuf<T>& b, const std::vector<T>& h) {
+    if (!h.empty()) CK(cudaMemcpyAsync(b.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+  }
+
+  // Engine::make_checkpoint (engine.cpp:1150-1233).  The pending inbox of a
+  // cell is what the reference holds after its last exchange: the unconsumed
+  // sorted events, then the events the last epoch's spikes pushed (Impl::
+  // exchange, :875-889: cells in gid order, spikes in step order, out-edges in
+  // seq order), which this engine expands only at the next epoch's start.
+  std::vector<uint8_t> make_checkpoint() {
+    if (m.world > 1) throw Error(MCG_ERR_ENGINE, "checkpoint: not supported for a sharded engine");
+    const int nl = n_local();
+    const size_t nv = m.v.size(), nsp = m.species.size(), ni = m.i_comp.size();
+    const auto v = download(d_v, nv), hm = download(d_hh_m, nv), hh = download(d_hh_h, nv),
+               hn = download(d_hh_n, nv), sp = download(d_species, nsp),
+               det = download(d_det_prev, size_t(nl));
+    const auto armed = download(d_armed, size_t(nl));
+    const auto refr = download(d_refr, size_t(nl));
+    const auto iseq = download(d_iseq, size_t(nl));
+    const auto ker = download(d_i_kernel, ni), wgt = download(d_i_weight, ni),
+               spre = download(d_i_stdp_pre, ni), spost = download(d_i_stdp_post, ni),
+               sw = download(d_i_stdp_w, ni), hw = download(d_i_homeo_w, ni),
+               sh = download(d_i_stc_h, ni), sz = download(d_i_stc_z, ni), sc = download(d_i_stc_c, ni),
+               sa = download(d_i_sps_abs, ni);
+    const auto slast = download(d_i_stdp_last, ni);
+    const auto pend = download(d_pend, size_t(std::max(nl, 1)) * 2 * pend_cap);
+    const auto psel = download(d_pend_sel, size_t(nl)), poff = download(d_pend_off, size_t(nl)),
+               pn = download(d_pend_n, size_t(nl));
+    const auto fifos = download(d_fifos, m.fifos.size());
+    const size_t nf = size_t(std::max<int64_t>(m.fifo_total, 1));
+    const auto fstep = download(d_fifo_step, nf);
+    const auto fsi = download(d_fifo_si, nf);
+    const auto fsrc = download(d_fifo_src, nf);
+    const auto fw = download(d_fifo_w, nf);
+    const auto spc = download(d_sp_count, size_t(nl));
+    const auto sps = download(d_sp_step, size_t(std::max(nl, 1)) * sp_cap);
+    CK(cudaStreamSynchronize(st));
+
+    // the last epoch's exchange, per destination
+    std::vector<std::vector<CkEvent>> extra(nl);
+    for (int c = 0; c < nl; ++c) {
+      const uint32_t gid = m.gid_begin + uint32_t(c);
+      for (int q = 0; q < spc[c] && q < sp_cap; ++q) {
+        const int64_t st0 = sps[size_t(c) * sp_cap + q];
+        for (int64_t r = m.out_begin[gid]; r < m.out_end[gid]; ++r)
+          extra[m.e_dst[r]].push_back(CkEvent{st0 + 1 + m.e_delay[r], gid, m.e_seq[r],
+                                              uint16_t(m.e_group[r]), 0, m.e_inst[r], m.e_weight[r]});
+      }
+    }
+    const uint64_t mask = (1ull << rank_bits) - 1;
+    Ckpt ck;
+    ck.u64["meta/step"] = {static_cast<uint64_t>(step)};
+    ck.f64["meta/dt_ms"] = {m.dt};
+    for (int c = 0; c < nl; ++c) {
+      const McgKind& K = m.kinds[m.cell_kind[c]];
+      const int n = K.n;
+      const int64_t co = m.comp_off[c];
+      const std::string pre = "cell/" + std::to_string(m.gid_begin + uint32_t(c)) + "/";
+      if (K.dyn != MCG_DYN_NONE) ck.f64[pre + "v"].assign(v.begin() + co, v.begin() + co + n);
+      ck.f64[pre + "det"] = {det[c]};
+      ck.u64[pre + "flags"] = {static_cast<uint64_t>(refr[c]), armed[c] ? 1ull : 0ull, uint64_t(iseq[c])};
+      for (int q = 0; q < K.n_species; ++q) {
+        const int64_t o = m.sp_off[c] + int64_t(q) * n;
+        ck.f64[pre + "species/" + std::to_string(q)].assign(sp.begin() + o, sp.begin() + o + n);
+      }
+      if (K.dyn == MCG_DYN_HH) {
+        ck.f64[pre + "hh_m"].assign(hm.begin() + co, hm.begin() + co + n);
+        ck.f64[pre + "hh_h"].assign(hh.begin() + co, hh.begin() + co + n);
+        ck.f64[pre + "hh_n"].assign(hn.begin() + co, hn.begin() + co + n);
+      }
+      std::vector<CkEvent> internal;
+      for (int gi = 0; gi < K.n_groups; ++gi) {
+        const McgCellGroup& G = m.cgs[m.cg_off[c] + gi];
+        const McgSpec& S = m.specs[G.spec];
+        const std::string gp = pre + "g" + std::to_string(gi) + "/";
+        const int64_t a = G.inst, b = G.inst + G.size;
+        ck.f64[gp + "kernel"].assign(ker.begin() + a, ker.begin() + b);
+        ck.f64[gp + "weight"].assign(wgt.begin() + a, wgt.begin() + b);
+        if (G.size > 0 && S.kind == MCG_SYN_STDP_COND) {
+          ck.f64[gp + "stdp_a_pre"].assign(spre.begin() + a, spre.begin() + b);
+          ck.f64[gp + "stdp_a_post"].assign(spost.begin() + a, spost.begin() + b);
+          ck.f64[gp + "stdp_w"].assign(sw.begin() + a, sw.begin() + b);
+          std::vector<uint64_t> ls(G.size);
+          for (int i = 0; i < G.size; ++i) ls[i] = static_cast<uint64_t>(slast[a + i]);
+          ck.u64[gp + "stdp_last"] = ls;
+        }
+        if (G.size > 0 && S.kind == MCG_SYN_HOMEO_CURRENT)
+          ck.f64[gp + "homeo_w"].assign(hw.begin() + a, hw.begin() + b);
+        if (G.size > 0 && S.kind == MCG_SYN_STC_CHARGE) {
+          ck.f64[gp + "stc_h"].assign(sh.begin() + a, sh.begin() + b);
+          ck.f64[gp + "stc_z"].assign(sz.begin() + a, sz.begin() + b);
+          ck.f64[gp + "stc_c"].assign(sc.begin() + a, sc.begin() + b);
+          ck.f64[gp + "stc_sps"].assign(sa.begin() + a, sa.begin() + b);
+        }
+        if (G.fifo >= 0) {  // delayed-calcium queue -> internal events
+          const McgFifo& F = fifos[G.fifo];
+          for (int64_t h = F.head; h < F.tail; ++h) {
+            const int64_t slot = F.base + (h % F.cap);
+            internal.push_back(CkEvent{fstep[slot], fsrc[slot], uint32_t(fsi[slot] >> 32), uint16_t(gi), 1,
+                                       uint32_t(fsi[slot] & 0xffffffffu), fw[slot]});
+          }
+        }
+      }
+      std::vector<CkEvent> inbox;
+      const uint64_t* pl = pend.data() + (size_t(c) * 2 + psel[c]) * pend_cap;
+      for (int i = poff[c]; i < pn[c]; ++i) {
+        const int64_t r = int64_t(pl[i] & mask);
+        inbox.push_back(CkEvent{int64_t(pl[i] >> rank_bits), m.e_src[r], m.e_seq[r],
+                                uint16_t(m.e_group[r]), 0, m.e_inst[r], m.e_weight[r]});
+      }
+      inbox.insert(inbox.end(), extra[c].begin(), extra[c].end());
+      std::sort(internal.begin(), internal.end(), [](const CkEvent& x, const CkEvent& y) {
+        if (x.step != y.step) return x.step < y.step;
+        return x.seq < y.seq;
+      });
+      ck_pack(ck, pre + "inbox", inbox);
+      ck_pack(ck, pre + "internal", internal);
+    }
+    return ck_serialize(ck);
+  }
+
+  // Checkpoint::deserialize + Engine::restore (engine.cpp:1095-1140, 1235-1325)
+  void restore(const uint8_t* bytes, size_t size) {
+    if (m.world > 1) throw Error(MCG_ERR_ENGINE, "checkpoint: not supported for a sharded engine");
+    const Ckpt ck = ck_deserialize(bytes, size);
+    auto getf = [&](const std::string& n) -> const std::vector<double>& {
+      auto it = ck.f64.find(n);
+      if (it == ck.f64.end()) throw Error(MCG_ERR_ENGINE, "checkpoint: missing " + n);
+      return it->second;
+    };
+    auto getu = [&](const std::string& n) -> const std::vector<uint64_t>& {
+      auto it = ck.u64.find(n);
+      if (it == ck.u64.end()) throw Error(MCG_ERR_ENGINE, "checkpoint: missing " + n);
+      return it->second;
+    };
+    auto sized = [](const std::vector<double>& a, size_t n) -> const std::vector<double>& {
+      if (a.size() != n) throw Error(MCG_ERR_ENGINE, "checkpoint: state size mismatch");
+      return a;
+    };
+    const auto& dtv = getf("meta/dt_ms");
+    if (dtv.empty() || std::fabs(dtv[0] - m.dt) > 1e-15) throw Error(MCG_ERR_ENGINE, "checkpoint: dt mismatch");
+    const auto& stv = getu("meta/step");
+    if (stv.empty()) throw Error(MCG_ERR_ENGINE, "checkpoint: missing meta/step");
+    const int nl = n_local();
+    const size_t nv = m.v.size(), nsp = m.species.size(), ni = m.i_comp.size();
+    auto v = download(d_v, nv), hm = download(d_hh_m, nv), hh = download(d_hh_h, nv),
+         hn = download(d_hh_n, nv), sp = download(d_species, nsp), det = download(d_det_prev, size_t(nl));
+    auto armed = download(d_armed, size_t(nl));
+    auto refr = download(d_refr, size_t(nl));
+    auto iseq = download(d_iseq, size_t(nl));
+    auto ker = download(d_i_kernel, ni), wgt = download(d_i_weight, ni), spre = download(d_i_stdp_pre, ni),
+         spost = download(d_i_stdp_post, ni), sw = download(d_i_stdp_w, ni), hw = download(d_i_homeo_w, ni),
+         sh = download(d_i_stc_h, ni), sz = download(d_i_stc_z, ni), sc = download(d_i_stc_c, ni),
+         sa = download(d_i_sps_abs, ni);
+    auto slast = download(d_i_stdp_last, ni);
+    auto act = download(d_i_active, std::max<size_t>(ni, 1));
+    auto cgs = download(d_cgs, m.cgs.size());
+    auto fifos = download(d_fifos, m.fifos.size());
+    const size_t nf = size_t(std::max<int64_t>(m.fifo_total, 1));
+    std::vector<int64_t> fstep(nf, 0);
+    std::vector<uint64_t> fsi(nf, 0);
+    std::vector<uint32_t> fsrc(nf, 0);
+    std::vector<double> fw(nf, 0.0);
+    CK(cudaStreamSynchronize(st));
+    // (src, seq) -> edge rank: EventRec identity of a pending network event
+    std::unordered_map<uint64_t, int64_t> rank_of;
+    rank_of.reserve(m.e_src.size() * 2);
+    for (size_t r = 0; r < m.e_src.size(); ++r) rank_of[(uint64_t(m.e_src[r]) << 32) | m.e_seq[r]] = int64_t(r);
+    std::vector<std::vector<uint64_t>> keys(nl);
+    int64_t kmax = 0;
+    for (int c = 0; c < nl; ++c) {
+      const McgKind& K = m.kinds[m.cell_kind[c]];
+      const int n = K.n;
+      const int64_t co = m.comp_off[c];
+      const std::string pre = "cell/" + std::to_string(m.gid_begin + uint32_t(c)) + "/";
+      if (K.dyn != MCG_DYN_NONE) {
+        const auto& a = sized(getf(pre + "v"), n);
+        std::copy(a.begin(), a.end(), v.begin() + co);
+      }
+      const auto& dv = getf(pre + "det");
+      if (dv.empty()) throw Error(MCG_ERR_ENGINE, "checkpoint: state size mismatch");
+      det[c] = dv[0];
+      const auto& fl = getu(pre + "flags");
+      if (fl.size() < 3) throw Error(MCG_ERR_ENGINE, "checkpoint: state size mismatch");
+      refr[c] = static_cast<int64_t>(fl[0]);
+      armed[c] = fl[1] != 0 ? 1 : 0;
+      iseq[c] = static_cast<uint32_t>(fl[2]);
+      for (int q = 0; q < K.n_species; ++q) {
+        const auto& a = sized(getf(pre + "species/" + std::to_string(q)), n);
+        std::copy(a.begin(), a.end(), sp.begin() + m.sp_off[c] + int64_t(q) * n);
+      }
+      if (K.dyn == MCG_DYN_HH) {
+        std::copy(sized(getf(pre + "hh_m"), n).begin(), sized(getf(pre + "hh_m"), n).end(), hm.begin() + co);
+        std::copy(sized(getf(pre + "hh_h"), n).begin(), sized(getf(pre + "hh_h"), n).end(), hh.begin() + co);
+        std::copy(sized(getf(pre + "hh_n"), n).begin(), sized(getf(pre + "hh_n"), n).end(), hn.begin() + co);
+      }
+      for (int gi = 0; gi < K.n_groups; ++gi) {
+        McgCellGroup& G = cgs[m.cg_off[c] + gi];
+        const McgSpec& S = m.specs[G.spec];
+        const std::string gp = pre + "g" + std::to_string(gi) + "/";
+        const int64_t a = G.inst;
+        const auto& kk = sized(getf(gp + "kernel"), G.size);
+        const auto& ww = sized(getf(gp + "weight"), G.size);
+        std::copy(kk.begin(), kk.end(), ker.begin() + a);
+        std::copy(ww.begin(), ww.end(), wgt.begin() + a);
+        if (S.kind == MCG_SYN_STATIC_COND || S.kind == MCG_SYN_STDP_COND ||
+            S.kind == MCG_SYN_STATIC_CURRENT || S.kind == MCG_SYN_HOMEO_CURRENT) {
+          int na = 0;  // active list in instance order (engine.cpp:1262-1264)
+          for (int i = 0; i < G.size; ++i)
+            if (kk[i] != 0.0) act[a + na++] = i;
+          G.active_n = na;
+        }
+        if (G.size > 0 && S.kind == MCG_SYN_STDP_COND) {
+          const auto& x = sized(getf(gp + "stdp_a_pre"), G.size);
+          const auto& y = sized(getf(gp + "stdp_a_post"), G.size);
+          const auto& z = sized(getf(gp + "stdp_w"), G.size);
+          const auto& l = getu(gp + "stdp_last");
+          if (l.size() != size_t(G.size)) throw Error(MCG_ERR_ENGINE, "checkpoint: state size mismatch");
+          for (int i = 0; i < G.size; ++i) {
+            spre[a + i] = x[i];
+            spost[a + i] = y[i];
+            sw[a + i] = z[i];
+            slast[a + i] = static_cast<int64_t>(l[i]);
+          }
+        }
+        if (G.size > 0 && S.kind == MCG_SYN_HOMEO_CURRENT) {
+          const auto& x = sized(getf(gp + "homeo_w"), G.size);
+          std::copy(x.begin(), x.end(), hw.begin() + a);
+        }
+        if (G.size > 0 && S.kind == MCG_SYN_STC_CHARGE) {
+          const auto& x = sized(getf(gp + "stc_h"), G.size);
+          const auto& y = sized(getf(gp + "stc_z"), G.size);
+          const auto& z = sized(getf(gp + "stc_c"), G.size);
+          const auto& q = sized(getf(gp + "stc_sps"), G.size);
+          std::copy(x.begin(), x.end(), sh.begin() + a);
+          std::copy(y.begin(), y.end(), sz.begin() + a);
+          std::copy(z.begin(), z.end(), sc.begin() + a);
+          std::copy(q.begin(), q.end(), sa.begin() + a);
+        }
+        if (G.fifo >= 0) fifos[G.fifo].head = fifos[G.fifo].tail = 0;
+      }
+      // pending network events -> sorted keys
+      for (const CkEvent& e : ck_unpack(getu(pre + "inbox_meta"), getf(pre + "inbox_w"))) {
+        auto it = rank_of.find((uint64_t(e.src) << 32) | e.seq);
+        if (it == rank_of.end() || e.etype != 0) throw Error(MCG_ERR_ENGINE, "checkpoint: event does not match the recipe");
+        const int64_t r = it->second;
+        if (m.e_dst[r] != c || m.e_group[r] != e.group || m.e_inst[r] != e.instance ||
+            std::memcmp(&m.e_weight[r], &e.weight, 8) != 0 || e.step < 0)
+          throw Error(MCG_ERR_ENGINE, "checkpoint: event does not match the recipe");
+        keys[c].push_back((uint64_t(e.step) << rank_bits) | uint64_t(r));
+      }
+      std::sort(keys[c].begin(), keys[c].end());
+      kmax = std::max<int64_t>(kmax, int64_t(keys[c].size()));
+      // delayed calcium -> the groups' queues, in (step, seq) order
+      std::vector<CkEvent> internal = ck_unpack(getu(pre + "internal_meta"), getf(pre + "internal_w"));
+      std::sort(internal.begin(), internal.end(), [](const CkEvent& x, const CkEvent& y) {
+        if (x.step != y.step) return x.step < y.step;
+        return x.seq < y.seq;
+      });
+      for (const CkEvent& e : internal) {
+        if (e.group >= K.n_groups || e.etype != 1) throw Error(MCG_ERR_ENGINE, "checkpoint: event does not match the recipe");
+        const McgCellGroup& G = cgs[m.cg_off[c] + e.group];
+        if (G.fifo < 0) throw Error(MCG_ERR_ENGINE, "checkpoint: event does not match the recipe");
+        McgFifo& F = fifos[G.fifo];
+        if (F.tail - F.head >= F.cap) throw Error(MCG_ERR_ENGINE, "internal event queue overflow");
+        const int64_t slot = F.base + (F.tail % F.cap);
+        fstep[slot] = e.step;
+        fsi[slot] = (uint64_t(e.seq) << 32) | e.instance;
+        fsrc[slot] = e.src;
+        fw[slot] = e.weight;
+        ++F.tail;
+      }
+    }
+    while (kmax > pend_cap) grow_inboxes();
+    std::vector<uint64_t> pend(size_t(std::max(nl, 1)) * 2 * pend_cap, 0);
+    std::vector<int32_t> psel(nl, 0), poff(nl, 0), pn(nl, 0);
+    for (int c = 0; c < nl; ++c) {
+      std::copy(keys[c].begin(), keys[c].end(), pend.begin() + size_t(c) * 2 * pend_cap);
+      pn[c] = static_cast<int32_t>(keys[c].size());
+    }
+    upload_to(d_v, v);
+    upload_to(d_hh_m, hm);
+    upload_to(d_hh_h, hh);
+    upload_to(d_hh_n, hn);
+    upload_to(d_species, sp);
+    upload_to(d_det_prev, det);
+    upload_to(d_armed, armed);
+    upload_to(d_refr, refr);
+    upload_to(d_iseq, iseq);
+    upload_to(d_i_kernel, ker);
+    upload_to(d_i_weight, wgt);
+    upload_to(d_i_stdp_pre, spre);
+    upload_to(d_i_stdp_post, spost);
+    upload_to(d_i_stdp_w, sw);
+    upload_to(d_i_stdp_last, slast);
+    upload_to(d_i_homeo_w, hw);
+    upload_to(d_i_stc_h, sh);
+    upload_to(d_i_stc_z, sz);
+    upload_to(d_i_stc_c, sc);
+    upload_to(d_i_sps_abs, sa);
+    upload_to(d_i_active, act);
+    upload_to(d_cgs, cgs);
+    upload_to(d_fifos, fifos);
+    upload_to(d_fifo_step, fstep);
+    upload_to(d_fifo_si, fsi);
+    upload_to(d_fifo_src, fsrc);
+    upload_to(d_fifo_w, fw);
+    upload_to(d_pend, pend);
+    upload_to(d_pend_sel, psel);
+    upload_to(d_pend_off, poff);
+    upload_to(d_pend_n, pn);
+    d_inc_n.zero(st);
+    d_sp_count.zero(st);
+    CK(cudaStreamSynchronize(st));
+    step = static_cast<int64_t>(stv[0]);
+    refresh_dev();
+  }
 };
 
 }  // namespace mcg
@@ -1174,6 +1511,25 @@ int32_t mcg_cell_parent(const mcg_engine* eng, uint32_t gid, int32_t comp) {
   const auto& K = E.m.kinds[E.m.cell_kind[gid - E.m.gid_begin]];
   if (comp < 0 || comp >= K.n) return -2;
   return E.m.k_parent[K.arr + comp];
+}
+
+mcg_status mcg_checkpoint(mcg_engine* eng, uint8_t* buf, int64_t cap, int64_t* size) {
+  return guarded([&] {
+    if (!eng || !size) throw mcg::Error(MCG_ERR_ARGUMENT, "checkpoint: null argument");
+    const std::vector<uint8_t> b = eng->e.make_checkpoint();
+    *size = static_cast<int64_t>(b.size());
+    if (buf) {
+      if (cap < *size) throw mcg::Error(MCG_ERR_ARGUMENT, "checkpoint: buffer too small");
+      std::memcpy(buf, b.data(), b.size());
+    }
+  });
+}
+
+mcg_status mcg_restore(mcg_engine* eng, const uint8_t* buf, int64_t size) {
+  return guarded([&] {
+    if (!eng || (!buf && size > 0) || size < 0) throw mcg::Error(MCG_ERR_ARGUMENT, "restore: null argument");
+    eng->e.restore(buf, static_cast<size_t>(size));
+  });
 }
 
 mcg_status mcg_read_state(mcg_engine* eng, int32_t field, uint32_t gid, int32_t index,

@@ -45,6 +45,74 @@ def _check(status: int):
         raise _ERR.get(status, RuntimeError)(msg)
 
 
+class Checkpoint:
+    """The reference's Checkpoint (engine.hpp:107-124): named f64 / u64 arrays,
+    serialized as MCSCKPT1 (engine.cpp:1070-1148)."""
+
+    MAGIC = b"MCSCKPT1"
+
+    def __init__(self, data: bytes = b""):
+        self.data = bytes(data)
+
+    def serialize(self) -> bytes:
+        return self.data
+
+    @staticmethod
+    def deserialize(data: bytes) -> Tuple[dict, dict]:
+        """(f64, u64) name -> array, with the reference's validation and
+        messages (EngineError)."""
+        import struct
+        d = bytes(data)
+        if len(d) < 16 or d[:8] != Checkpoint.MAGIC:
+            raise EngineError("checkpoint: bad magic")
+        pos = 8
+
+        def take(n):
+            nonlocal pos
+            if pos + n > len(d):
+                raise EngineError("checkpoint: truncated")
+            out = d[pos:pos + n]
+            pos += n
+            return out
+        if struct.unpack("<I", take(4))[0] != 1:
+            raise EngineError("checkpoint: version mismatch")
+        if struct.unpack("<I", take(4))[0] != 0x01020304:
+            raise EngineError("checkpoint: endianness mismatch")
+        f64, u64 = {}, {}
+        while pos < len(d):
+            nlen = struct.unpack("<I", take(4))[0]
+            name = take(nlen).decode()
+            if pos >= len(d):
+                raise EngineError("checkpoint: truncated")
+            typ = d[pos]
+            pos += 1
+            count = struct.unpack("<Q", take(8))[0]
+            if count > (len(d) - pos) // 8:
+                raise EngineError("checkpoint: corrupted length header")
+            raw = take(8 * count)
+            if typ == 0:
+                f64[name] = np.frombuffer(raw, "<f8").copy()
+            elif typ == 1:
+                u64[name] = np.frombuffer(raw, "<u8").copy()
+            else:
+                raise EngineError("checkpoint: unknown record type")
+        return f64, u64
+
+    def save(self, path: str) -> None:  # Checkpoint::save (engine.cpp:1134-1140)
+        with open(path, "wb") as f:
+            f.write(self.data)
+
+    @staticmethod
+    def load(path: str) -> "Checkpoint":
+        try:
+            with open(path, "rb") as f:
+                data = f.read()
+        except OSError:
+            raise EngineError("checkpoint: cannot open " + path)
+        Checkpoint.deserialize(data)
+        return Checkpoint(data)
+
+
 class GroupView:
     """SynGroupRT mirror (engine.hpp:71-85): per-instance arrays read on access."""
 
@@ -202,6 +270,23 @@ class Engine:
             _check(L.mcg_get_spikes(self._h, 0, n, t.ctypes.data_as(C.c_void_p),
                                     g.ctypes.data_as(C.c_void_p)))
         return t, g
+
+    def make_checkpoint(self) -> "Checkpoint":
+        """Engine::make_checkpoint (engine.cpp:1150-1233): MCSCKPT1 bytes,
+        identical to the reference engine's at the same point of the same run."""
+        L = A.lib()
+        n = C.c_int64()
+        _check(L.mcg_checkpoint(self._h, None, 0, C.byref(n)))
+        buf = (C.c_uint8 * max(n.value, 1))()
+        _check(L.mcg_checkpoint(self._h, buf, n.value, C.byref(n)))
+        return Checkpoint(bytes(buf)[:n.value])
+
+    def restore(self, ck: "Checkpoint") -> None:
+        """Engine::restore (engine.cpp:1235-1325); takes the reference's
+        checkpoints as well."""
+        data = ck.data if isinstance(ck, Checkpoint) else bytes(ck)
+        buf = (C.c_uint8 * max(len(data), 1)).from_buffer_copy(data or b"\0")
+        _check(A.lib().mcg_restore(self._h, buf, len(data)))
 
     def write_spikes_csv(self, path: str) -> None:
         """spikes.csv of the run so far: times in seconds (t_ms * 1e-3, as the
