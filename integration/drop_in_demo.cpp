@@ -47,7 +47,16 @@ static int compare(A& ref, B& gpu, const mcsim::Recipe& r, double t_ms) {
         }
       }
   }
-  std::printf("OK %zu spikes identical, t = %.1f ms\n", s0.size(), t_ms);
+  // checkpoints: the same MCSCKPT1 bytes, and each engine restores the other's
+  const auto b0 = ref.make_checkpoint().serialize();
+  const auto b1 = gpu.make_checkpoint().serialize();
+  if (b0 != b1) {
+    std::printf("FAIL checkpoints differ (%zu vs %zu bytes)\n", b0.size(), b1.size());
+    return 1;
+  }
+  gpu.restore(mcsim::Checkpoint::deserialize(b0));
+  std::printf("OK %zu spikes identical, checkpoints identical (%zu bytes), t = %.1f ms\n",
+              s0.size(), b0.size(), t_ms);
   return 0;
 }
 

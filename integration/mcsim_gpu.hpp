@@ -273,6 +273,23 @@ class Engine {
 
   int num_cells() const { return mcg_num_cells(eng_); }
 
+  // Engine::make_checkpoint / restore (engine.hpp:139-140): the bytes are
+  // MCSCKPT1, so the reference's own Checkpoint type carries them and either
+  // engine restores the other's checkpoints
+  mcsim::Checkpoint make_checkpoint() {
+    flush_mirrors();
+    int64_t n = 0;
+    check(mcg_checkpoint(eng_, nullptr, 0, &n));
+    std::vector<std::uint8_t> b(static_cast<std::size_t>(n));
+    check(mcg_checkpoint(eng_, b.data(), n, &n));
+    return mcsim::Checkpoint::deserialize(b);
+  }
+  void restore(const mcsim::Checkpoint& c) {
+    const std::vector<std::uint8_t> b = c.serialize();
+    check(mcg_restore(eng_, b.data(), static_cast<int64_t>(b.size())));
+    invalidate();
+  }
+
   // lazily synced host mirror of one cell (written back before the next advance)
   mcsim::CellRT& cell(std::uint32_t gid) {
     auto it = cells_.find(gid);
