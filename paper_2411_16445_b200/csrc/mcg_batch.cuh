@@ -1415,16 +1415,22 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
               prp = D.species[D.sp_off[c] + K.prp_idx * K.n + g.comp];
             }
           }
-          McgStcVal v{B.stc[f], B.stc[S4 + f], B.stc[2 * S4 + f], B.stc[3 * S4 + f]};
-          double delta = 0.0;
-          changed = mcg_stc_step(specs[g.spec], D.dt, D.seed, D.gid0 + uint32_t(c), g.gi,
-                                 f - cs[k].stc_off - g.start, s, late, prp, g.vol, g.rvol, v,
-                                 delta);
-          dl = delta;
-          B.stc[f] = v.h;
-          B.stc[S4 + f] = v.z;
-          B.stc[2 * S4 + f] = v.c;
-          B.stc[3 * S4 + f] = v.a;
+          const McgSpec& S = specs[g.spec];
+          const double h = B.stc[f], cc = B.stc[2 * S4 + f], a = B.stc[3 * S4 + f];
+          if (mcg_stc_at_rest(S, late, prp, h, cc, a)) {
+            B.stc[2 * S4 + f] = cc * S.cf;  // the step reduces to the calcium decay
+          } else {
+            McgStcVal v{h, B.stc[S4 + f], cc, a};
+            double delta = 0.0;
+            changed = mcg_stc_step(S, D.dt, D.seed, D.gid0 + uint32_t(c), g.gi,
+                                   f - cs[k].stc_off - g.start, s, late, prp, g.vol, g.rvol, v,
+                                   delta);
+            dl = delta;
+            B.stc[f] = v.h;
+            B.stc[S4 + f] = v.z;
+            B.stc[2 * S4 + f] = v.c;
+            B.stc[3 * S4 + f] = v.a;
+          }
         }
         // changed flags as a ballot; the block's changed deltas stored
         // compacted in instance order (the fold walks them contiguously)
@@ -1448,7 +1454,6 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
           const McgSegSm& g = B.seg[k * A.n_stc_max + q];
           jj[u] = g.inst + (f - cs[k].stc_off - g.start);
           v[u].h = D.i_stc_h[jj[u]];
-          v[u].z = D.i_stc_z[jj[u]];
           v[u].c = D.i_stc_c[jj[u]];
           v[u].a = D.i_sps_abs[jj[u]];
         }
@@ -1466,15 +1471,21 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
           const double* SPb = (K.n <= m) ? mcg_comp_block(A, B, k) + m : D.species + D.sp_off[c];
           const bool late = K.prp_idx >= 0;
           const double prp = late ? SPb[int64_t(K.prp_idx) * K.n + g.comp] : 0.0;
-          double delta = 0.0;
-          const int li = f - cs[k].stc_off - g.start;
-          changed = mcg_stc_step(specs[g.spec], D.dt, D.seed, D.gid0 + uint32_t(c), g.gi, li, s,
-                                 late, prp, g.vol, g.rvol, v[u], delta);
-          dlt[u] = delta;
-          D.i_stc_h[jj[u]] = v[u].h;
-          D.i_stc_z[jj[u]] = v[u].z;
-          D.i_stc_c[jj[u]] = v[u].c;
-          if (changed) D.i_sps_abs[jj[u]] = v[u].a;
+          const McgSpec& S = specs[g.spec];
+          if (mcg_stc_at_rest(S, late, prp, v[u].h, v[u].c, v[u].a)) {
+            D.i_stc_c[jj[u]] = v[u].c * S.cf;  // the step reduces to the calcium decay
+          } else {
+            v[u].z = D.i_stc_z[jj[u]];
+            double delta = 0.0;
+            const int li = f - cs[k].stc_off - g.start;
+            changed = mcg_stc_step(S, D.dt, D.seed, D.gid0 + uint32_t(c), g.gi, li, s, late, prp,
+                                   g.vol, g.rvol, v[u], delta);
+            dlt[u] = delta;
+            D.i_stc_h[jj[u]] = v[u].h;
+            D.i_stc_z[jj[u]] = v[u].z;
+            D.i_stc_c[jj[u]] = v[u].c;
+            if (changed) D.i_sps_abs[jj[u]] = v[u].a;
+          }
         }
         const unsigned bal = __ballot_sync(MCG_FULL, changed);
         const int fw = (r0 + u) * T + (tid - lane);

@@ -307,6 +307,20 @@ __device__ __noinline__ double mcg_stc_noise(uint64_t seed, uint32_t gid, int gi
   return mcg_normal_for(&key, static_cast<uint64_t>(s));
 }
 
+// A synapse at rest — h exactly at its baseline, calcium above neither
+// threshold, |h - h0| already folded as 0 — takes a step that only decays its
+// calcium: stc_early_step adds exactly +0 to h (0.1*(h0 - h) = +0, no noise),
+// |h - h0| = +0 equals the folded value, and stc_late_step (when it runs: a
+// nonnegative tag threshold, finite PRP and f_int) adds a signed zero to z,
+// which is never -0 (it starts at +0 and only changes by nonzero sums).
+__device__ __forceinline__ bool mcg_stc_at_rest(const McgSpec& S, bool late, double prp, double h,
+                                                double c, double a) {
+  return __double_as_longlong(h) == __double_as_longlong(S.h0) && !(c > S.theta_p) &&
+         !(c > S.theta_d) && a == 0.0 &&
+         (!late || prp <= 0.0 ||
+          (S.theta_tag >= 0.0 && prp <= 1.7976931348623157e308 && fabs(S.f_int) <= 1.7976931348623157e308));
+}
+
 __device__ __forceinline__ bool mcg_stc_step(const McgSpec& S, double dt, uint64_t seed,
                                              uint32_t gid, int gi, int i, int64_t s, bool late,
                                              double prp, double vol, double rvol, McgStcVal& v,

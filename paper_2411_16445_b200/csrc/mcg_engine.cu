@@ -309,7 +309,7 @@ struct Engine {
     // memory (mcg_stage_events), in whatever the opt-in limit leaves
     bc_ev_cap = 0;
     if (bc_stc_sm && !std::getenv("MCG_NO_STAGED_EVENTS")) {
-      const size_t lim = size_t(smem_optin) - 1024;
+      const size_t lim = size_t(smem_optin) - 4096;  // static shared memory of the kernel
       const size_t left = lim > bc_smem + 32 ? lim - bc_smem - 32 : 0;
       bc_ev_cap = static_cast<int32_t>(std::min<size_t>(left / sizeof(McgEvSm), 4096));
       if (bc_ev_cap < 64) bc_ev_cap = 0;
