@@ -1253,7 +1253,10 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
       __syncthreads();
       MCG_PH(0);
     }
-    // ---- A. delivery (owner thread): inbox, then internal (engine.cpp:549-560)
+    // ---- A. delivery (owner thread): inbox, then internal (engine.cpp:549-560);
+    // the other threads clear the STC changed flags of the step
+    if (A.stc_sm && tid >= nc)
+      for (int w = tid - nc; w <= (stc_total >> 5); w += T - nc) B.fmask[w] = 0u;
     if (tid < nc) {
       const int c = c0 + tid;
       McgCellSm& X = cs[tid];
@@ -1394,17 +1397,18 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
     // ---- C. STC synapses of every cell of the batch, one flat index space
     // (engine.cpp:617-646), four instances per thread in flight; changed
     // flags as warp ballots for the fold
-    if (A.stc_sm) {  // state in shared memory: one instance per thread and round
+    if (A.stc_sm) {
+      // state in shared memory: warp per cell, lanes over its instances, the
+      // placement's constants (spec, PRP level, volume) loaded once per warp;
+      // changed slots set their flag bit (fmask, cleared in phase A) and leave
+      // their SPS delta at their own slot of dbuf
       const int S4 = A.stc_max;
-      for (int f0 = tid - lane; f0 < stc_total; f0 += T) {
-        const int f = f0 + lane;
-        bool changed = false;
-        double dl = 0.0;
-        if (f < stc_total) {
-          const uint32_t loc = B.floc[f];
-          const int k = int(loc >> 16);
-          const McgSegSm& g = B.seg[k * A.n_stc_max + int(loc & 0xffffu)];
-          const int c = c0 + k;
+      for (int k = warp; k < nc; k += nwarps) {
+        const McgCellSm& X = cs[k];
+        const int c = c0 + k;
+        for (int q = 0; q < X.n_stc_seg; ++q) {
+          const McgSegSm& g = B.seg[k * A.n_stc_max + q];
+          const McgSpec& S = specs[g.spec];
           const bool late = g.late;
           double prp = 0.0;
           if (late) {
@@ -1415,28 +1419,28 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
               prp = D.species[D.sp_off[c] + K.prp_idx * K.n + g.comp];
             }
           }
-          const McgSpec& S = specs[g.spec];
-          const double h = B.stc[f], cc = B.stc[2 * S4 + f], a = B.stc[3 * S4 + f];
-          if (mcg_stc_at_rest(S, late, prp, h, cc, a)) {
-            B.stc[2 * S4 + f] = cc * S.cf;  // the step reduces to the calcium decay
-          } else {
+          const int fb = X.stc_off + g.start;
+          for (int i = lane; i < g.size; i += 32) {
+            const int f = fb + i;
+            const double h = B.stc[f], cc = B.stc[2 * S4 + f], a = B.stc[3 * S4 + f];
+            if (mcg_stc_at_rest(S, late, prp, h, cc, a)) {
+              B.stc[2 * S4 + f] = cc * S.cf;  // the step reduces to the calcium decay
+              continue;
+            }
             McgStcVal v{h, B.stc[S4 + f], cc, a};
             double delta = 0.0;
-            changed = mcg_stc_step(S, D.dt, D.seed, D.gid0 + uint32_t(c), g.gi,
-                                   f - cs[k].stc_off - g.start, s, late, prp, g.vol, g.rvol, v,
-                                   delta);
-            dl = delta;
+            const bool changed = mcg_stc_step(S, D.dt, D.seed, D.gid0 + uint32_t(c), g.gi, i, s,
+                                              late, prp, g.vol, g.rvol, v, delta);
             B.stc[f] = v.h;
             B.stc[S4 + f] = v.z;
             B.stc[2 * S4 + f] = v.c;
             B.stc[3 * S4 + f] = v.a;
+            if (changed) {
+              B.dbuf[f] = delta;
+              atomicOr(&B.fmask[f >> 5], 1u << (f & 31));
+            }
           }
         }
-        // changed flags as a ballot; the block's changed deltas stored
-        // compacted in instance order (the fold walks them contiguously)
-        const unsigned bal = __ballot_sync(MCG_FULL, changed);
-        if (changed) B.dbuf[f0 + __popc(bal & mcg_lanemask_lt())] = dl;
-        if (lane == 0) B.fmask[f0 >> 5] = bal;
       }
     } else
     for (int r0 = 0; r0 < stc_rounds; r0 += 4) {
@@ -1489,7 +1493,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
         }
         const unsigned bal = __ballot_sync(MCG_FULL, changed);
         const int fw = (r0 + u) * T + (tid - lane);
-        if (changed) B.dbuf[fw + __popc(bal & mcg_lanemask_lt())] = dlt[u];
+        if (changed) B.dbuf[f] = dlt[u];
         if (lane == 0) B.fmask[fw >> 5] = bal;
       }
     }
@@ -1514,24 +1518,15 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
           // every instance of a placement sits on the placement's compartment
           double acc = sps[g.comp];
           while (f < fe) {
-            // this 32-slot block's changed deltas of the segment: a contiguous
-            // run of the block's compacted deltas; the adds stay in instance order
+            // the segment's changed slots of this 32-slot word, in instance order
             const int w = f >> 5, lo = f & 31;
             const int lim = min(32 - lo, fe - f);
-            const uint32_t bal = B.fmask[w];
-            const uint32_t m_lo = (1u << lo) - 1u;
-            const uint32_t m_hi = (lo + lim == 32) ? 0xffffffffu : ((1u << (lo + lim)) - 1u);
-            const double* p = B.dbuf + (w << 5);
-            int i = __popc(bal & m_lo);
-            const int i1 = __popc(bal & m_hi);
-            for (; i + 4 <= i1; i += 4) {
-              const double a0 = p[i], a1 = p[i + 1], a2 = p[i + 2], a3 = p[i + 3];
-              acc += a0;
-              acc += a1;
-              acc += a2;
-              acc += a3;
+            uint32_t bits = B.fmask[w] >> lo;
+            if (lim < 32) bits &= (1u << lim) - 1u;
+            while (bits) {
+              acc += B.dbuf[f + __ffs(bits) - 1];
+              bits &= bits - 1u;
             }
-            for (; i < i1; ++i) acc += p[i];
             f += lim;
           }
           sps[g.comp] = acc;
