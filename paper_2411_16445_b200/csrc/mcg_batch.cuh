@@ -192,6 +192,8 @@ struct McgSegSm {
   int32_t f_cap, fifo;
   int32_t prp_sm;           // mcg_smem offset of the PRP value at comp (-1: global / none)
   int32_t late;             // the cell has a PRP pool (stc_late_step runs)
+  int64_t ca_delay;         // spec fields the staged delivery reads (McgSpec copies,
+  double h0, cpre_s;        // so the delivery chain stays in shared memory)
 };
 
 // per-kind constants the sweeps read every step, staged in shared memory once
@@ -864,6 +866,9 @@ __device__ void mcg_batch_enter(const McgDev& D, const McgBatchArgs& A, int32_t 
       g.vol = D.k_volume[K.arr + S.comp];
       g.rvol = D.k_rvol[K.arr + S.comp];
       g.cf = D.k_cf[K.arr + S.comp];
+      g.ca_delay = S.ca_delay;
+      g.h0 = S.h0;
+      g.cpre_s = S.cpre_s;
       g.late = K.prp_idx >= 0 ? 1 : 0;
       g.prp_sm = (K.prp_idx >= 0 && K.n <= m)
                      ? tid * A.comp_stride + m + K.prp_idx * K.n + S.comp : -1;
@@ -1276,12 +1281,11 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
             if (!refractory && (E.inst >> 31)) V[E.comp] += E.w;  // w * cf[comp]
           } else {  // stc_charge, engine.cpp:493-510
             McgSegSm& g = B.seg[tid * A.n_stc_max + X.gseg[E.group]];
-            const McgSpec& S = specs[g.spec];
             if (g.f_tail - g.f_head >= g.f_cap) {
               atomicOr(D.err, MCG_ERR_FLAG_FIFO);
             } else {
               const int64_t slot = g.f_base + (g.f_tail % g.f_cap);
-              D.fifo_step[slot] = s + S.ca_delay;
+              D.fifo_step[slot] = s + g.ca_delay;
               D.fifo_si[slot] = (uint64_t(X.iseq) << 32) | uint64_t(inst);
               D.fifo_src[slot] = E.src;
               D.fifo_w[slot] = E.w;
@@ -1290,7 +1294,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
             ++X.iseq;
             if (!refractory) {
               const int sl = X.stc_off + g.start + int(inst);
-              const double tw = B.stc[sl] + S.h0 * B.stc[S4 + sl];
+              const double tw = B.stc[sl] + g.h0 * B.stc[S4 + sl];
               V[g.comp] += tw * E.w * g.cf;
             }
           }
@@ -1302,7 +1306,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
         while (q < X.in_end && int(B.evb[q].so) == int(so)) {
           const McgEvSm E = B.evb[q];
           const McgSegSm& g = B.seg[tid * A.n_stc_max + X.gseg[E.group]];
-          B.stc[2 * S4 + X.stc_off + g.start + int(E.inst)] += specs[g.spec].cpre_s;
+          B.stc[2 * S4 + X.stc_off + g.start + int(E.inst)] += g.cpre_s;
           ++q;
         }
         X.in_cur = q;
@@ -1409,6 +1413,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
         for (int q = 0; q < X.n_stc_seg; ++q) {
           const McgSegSm& g = B.seg[k * A.n_stc_max + q];
           const McgSpec& S = specs[g.spec];
+          const McgStcRest R = mcg_stc_rest_of(S);
           const bool late = g.late;
           double prp = 0.0;
           if (late) {
@@ -1423,8 +1428,8 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
           for (int i = lane; i < g.size; i += 32) {
             const int f = fb + i;
             const double h = B.stc[f], cc = B.stc[2 * S4 + f], a = B.stc[3 * S4 + f];
-            if (mcg_stc_at_rest(S, late, prp, h, cc, a)) {
-              B.stc[2 * S4 + f] = cc * S.cf;  // the step reduces to the calcium decay
+            if (mcg_stc_at_rest(R, late, prp, h, cc, a)) {
+              B.stc[2 * S4 + f] = cc * R.cf;  // the step reduces to the calcium decay
               continue;
             }
             McgStcVal v{h, B.stc[S4 + f], cc, a};
@@ -1476,8 +1481,9 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
           const bool late = K.prp_idx >= 0;
           const double prp = late ? SPb[int64_t(K.prp_idx) * K.n + g.comp] : 0.0;
           const McgSpec& S = specs[g.spec];
-          if (mcg_stc_at_rest(S, late, prp, v[u].h, v[u].c, v[u].a)) {
-            D.i_stc_c[jj[u]] = v[u].c * S.cf;  // the step reduces to the calcium decay
+          const McgStcRest R = mcg_stc_rest_of(S);
+          if (mcg_stc_at_rest(R, late, prp, v[u].h, v[u].c, v[u].a)) {
+            D.i_stc_c[jj[u]] = v[u].c * R.cf;  // the step reduces to the calcium decay
           } else {
             v[u].z = D.i_stc_z[jj[u]];
             double delta = 0.0;

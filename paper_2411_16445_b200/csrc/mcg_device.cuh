@@ -313,12 +313,28 @@ __device__ __noinline__ double mcg_stc_noise(uint64_t seed, uint32_t gid, int gi
 // |h - h0| = +0 equals the folded value, and stc_late_step (when it runs: a
 // nonnegative tag threshold, finite PRP and f_int) adds a signed zero to z,
 // which is never -0 (it starts at +0 and only changes by nonzero sums).
-__device__ __forceinline__ bool mcg_stc_at_rest(const McgSpec& S, bool late, double prp, double h,
+// the spec fields the test reads, loaded once per placement (a register copy:
+// the spec table may live in global or shared memory)
+struct McgStcRest {
+  long long h0_bits;
+  double theta_p, theta_d, cf;
+  bool late_noop;  // stc_late_step at h == h0 adds a signed zero for any finite PRP
+};
+
+__device__ __forceinline__ McgStcRest mcg_stc_rest_of(const McgSpec& S) {
+  McgStcRest r;
+  r.h0_bits = __double_as_longlong(S.h0);
+  r.theta_p = S.theta_p;
+  r.theta_d = S.theta_d;
+  r.cf = S.cf;
+  r.late_noop = S.theta_tag >= 0.0 && fabs(S.f_int) <= 1.7976931348623157e308;
+  return r;
+}
+
+__device__ __forceinline__ bool mcg_stc_at_rest(const McgStcRest& R, bool late, double prp, double h,
                                                 double c, double a) {
-  return __double_as_longlong(h) == __double_as_longlong(S.h0) && !(c > S.theta_p) &&
-         !(c > S.theta_d) && a == 0.0 &&
-         (!late || prp <= 0.0 ||
-          (S.theta_tag >= 0.0 && prp <= 1.7976931348623157e308 && fabs(S.f_int) <= 1.7976931348623157e308));
+  return __double_as_longlong(h) == R.h0_bits && !(c > R.theta_p) && !(c > R.theta_d) && a == 0.0 &&
+         (!late || prp <= 0.0 || (R.late_noop && prp <= 1.7976931348623157e308));
 }
 
 __device__ __forceinline__ bool mcg_stc_step(const McgSpec& S, double dt, uint64_t seed,
