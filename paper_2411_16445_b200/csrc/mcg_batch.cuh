@@ -974,9 +974,9 @@ __device__ void mcg_batch_enter(const McgDev& D, const McgBatchArgs& A, int32_t 
     for (int i = tid; i < K.n_species * n; i += T) base[m + i] = gs[i];
     if (K.dyn == MCG_DYN_HH)
       for (int i = tid; i < n; i += T) {
-        base[(1 + D.sp_max) * m + i] = D.hh_m[co + i];
-        base[(2 + D.sp_max) * m + i] = D.hh_h[co + i];
-        base[(3 + D.sp_max) * m + i] = D.hh_n[co + i];
+        base[(2 + D.sp_max) * m + i] = D.hh_m[co + i];
+        base[(3 + D.sp_max) * m + i] = D.hh_h[co + i];
+        base[(4 + D.sp_max) * m + i] = D.hh_n[co + i];
       }
   }
   __syncthreads();
@@ -1001,9 +1001,9 @@ __device__ void mcg_batch_exit(const McgDev& D, const McgBatchArgs& A, int32_t b
     for (int i = tid; i < K.n_species * n; i += T) gs[i] = base[m + i];
     if (K.dyn == MCG_DYN_HH)
       for (int i = tid; i < n; i += T) {
-        D.hh_m[co + i] = base[(1 + D.sp_max) * m + i];
-        D.hh_h[co + i] = base[(2 + D.sp_max) * m + i];
-        D.hh_n[co + i] = base[(3 + D.sp_max) * m + i];
+        D.hh_m[co + i] = base[(2 + D.sp_max) * m + i];
+        D.hh_h[co + i] = base[(3 + D.sp_max) * m + i];
+        D.hh_n[co + i] = base[(4 + D.sp_max) * m + i];
       }
   }
   if (A.stc_sm) {
@@ -1073,7 +1073,7 @@ __device__ __noinline__ void mcg_ph_solve(const McgDev& D, const McgBatchArgs& A
           // right-hand sides (engine.cpp:683 / 746-748): V: g_leak_rhs + 0.0 +
           // rhs_current (if any current); species: production at the
           // synthesis compartment
-          L.rc = (sys == 0 && X.has_current) ? k * A.comp_stride + (6 + D.sp_max) * m : -1;
+          L.rc = (sys == 0 && X.has_current) ? k * A.comp_stride + (1 + D.sp_max) * m : -1;
           L.pc = (sys > 0 && sys - 1 == K.prp_idx && X.prod != 0.0) ? K.prp_comp : -1;
           L.prod = X.prod;
         }
@@ -1113,7 +1113,7 @@ __device__ __noinline__ void mcg_ph_solve(const McgDev& D, const McgBatchArgs& A
       //   species: r2 = cap*c + (prod at the synthesis compartment, else 0.0)
       const int pc = (!v_sys && q == K.prp_idx && X.prod != 0.0) ? K.prp_comp : -1;
       mcg_rhs_sm(n, v_sys ? KO.cap : KO.sp_cap + qn, x, r2, v_sys, KO.glr,
-                 hc ? bo + (6 + D.sp_max) * m : -1, pc, X.prod);
+                 hc ? bo + (1 + D.sp_max) * m : -1, pc, X.prod);
       mcg_sweep_const_sm(n, KO.par, (v_sys ? KO.ax : KO.sp_coup) + qn,
                          (v_sys ? KO.vf : KO.sp_f) + qn, (v_sys ? KO.vd : KO.sp_d) + qn,
                          (v_sys ? KO.vr : KO.sp_r) + qn, x, r2);
@@ -1360,7 +1360,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
       }
       X.has_gsyn = 0;
       X.has_current = 0;
-      double* rc = (K.n <= m) ? V + (6 + D.sp_max) * m : D.s_rhs_cur + D.comp_off[c];
+      double* rc = (K.n <= m) ? V + (1 + D.sp_max) * m : D.s_rhs_cur + D.comp_off[c];
       const int nr = K.n > 1 ? K.n : 1;
       for (int i = 0; i < nr; ++i) rc[i] = 0.0;
     }
@@ -1546,7 +1546,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
       if (X.lif && K.has_bg && !bg_gated) {
         double ib = K.i_bg;
         if (K.sig_bg != 0.0) ib += K.sig_bg * B.nbuf[tid * 32 + int(so & 31)];
-        double* rc = in_sm ? base + (6 + D.sp_max) * m : D.s_rhs_cur + D.comp_off[c];
+        double* rc = in_sm ? base + (1 + D.sp_max) * m : D.s_rhs_cur + D.comp_off[c];
         rc[K.noise_comp] += ib;
         X.has_current = 1;
       }

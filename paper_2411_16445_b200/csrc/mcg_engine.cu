@@ -173,6 +173,7 @@ struct Engine {
   int32_t bc_cells = 1, bc_batches = 1, bc_grid = 1, bc_stc_max = 1, bc_nstc_max = 1;
   int32_t bc_ch_pmax = 0, bc_ch_stride = 0;
   int32_t bc_ev_cap = 0, bc_fmask_words = 0;
+  int32_t bc_stride = 0;  // doubles per staged cell's compartment block
   int32_t bc_kind_doubles = 0, bc_specs_sm = 0, bc_stc_sm = 0;
   size_t bc_smem = 0;
   DBuf<int4> d_chunks;
@@ -255,6 +256,22 @@ struct Engine {
       bc_nstc_max = std::max(bc_nstc_max, ng);
     }
     if (bc_nstc_max > 0xffff) throw Error(MCG_ERR_ENGINE, "too many STC placements per kind");
+    // compartment block per staged cell: the full layout (mcg_cell_mem), or just
+    // V | SP | rhs_cur when every staged kind is a LIF with only charge-type
+    // synapses and its cable systems take the chain sweep (no HH gates,
+    // conductances or solver scratch are ever touched)
+    bool lean = !std::getenv("MCG_FULL_BLOCK");
+    for (size_t ki = 0; ki < m.kinds.size() && lean; ++ki) {
+      const McgKind& K = m.kinds[ki];
+      if (K.n > smem_n) continue;
+      if (K.dyn != MCG_DYN_LIF && K.dyn != MCG_DYN_LIF_EXACT) lean = false;
+      if (K.n > 1 && !(K.ch_lp > 0 && K.v_const && (K.n_species == 0 || K.sp_const))) lean = false;
+      for (int gi = 0; gi < K.n_groups && lean; ++gi) {
+        const int kd = m.specs[K.spec0 + gi].kind;
+        if (kd != MCG_SYN_STATIC_CHARGE && kd != MCG_SYN_STC_CHARGE) lean = false;
+      }
+    }
+    bc_stride = lean ? (2 + sp_max) * smem_n : smem_stride;
     // per cell: compartment block, noise draws, kind and cell records, STC
     // segments, and (upper bound) its STC slots in the fold/locator tables
     // chain-sweep scratch: (1 + sp_max) systems x P_max positions per cell
@@ -262,7 +279,7 @@ struct Engine {
     for (const McgKind& K : m.kinds)
       if (K.n <= smem_n && K.ch_lp > 0) bc_ch_pmax = std::max(bc_ch_pmax, 2 * K.ch_lp + 1);
     bc_ch_stride = bc_ch_pmax > 0 ? (1 + sp_max) * bc_ch_pmax : 0;
-    const size_t per_cell = size_t(smem_stride) * 8 + 32 * 8 + sizeof(McgKind) + sizeof(McgCellSm) +
+    const size_t per_cell = size_t(bc_stride) * 8 + 32 * 8 + sizeof(McgKind) + sizeof(McgCellSm) +
                             size_t(bc_nstc_max) * sizeof(McgSegSm) + size_t(cell_stc_max) * 12 +
                             size_t(bc_ch_stride) * 8;
     // staged kind constants (McgKindSm): one block per distinct kind of a batch
@@ -292,7 +309,7 @@ struct Engine {
     bc_kind_doubles = static_cast<int32_t>(std::min<size_t>(bc_cells, m.kinds.size()) * kb_max);
     // fold-flag words: one per 32 slots of every 512-thread round
     const size_t fmask_words = size_t((bc_stc_max + kBatchThreads - 1) / kBatchThreads) * (kBatchThreads / 32) + 1;
-    bc_smem = size_t(bc_cells) * (size_t(smem_stride) * 8 + 32 * 8 + sizeof(McgKind) + sizeof(McgCellSm) +
+    bc_smem = size_t(bc_cells) * (size_t(bc_stride) * 8 + 32 * 8 + sizeof(McgKind) + sizeof(McgCellSm) +
                                   size_t(bc_nstc_max) * sizeof(McgSegSm) + size_t(bc_ch_stride) * 8) +
               size_t(bc_stc_max) * (8 + 4) + size_t(bc_kind_doubles) * 8 +
               size_t(bc_specs_sm) * sizeof(McgSpec) + fmask_words * 4 + 64;
@@ -767,7 +784,7 @@ struct Engine {
     A.n_epochs = static_cast<int32_t>(planned);
     A.cells_per_cta = bc_cells;
     A.n_batches = bc_batches;
-    A.comp_stride = smem_stride;
+    A.comp_stride = bc_stride;
     A.stc_max = bc_stc_max;
     A.n_stc_max = bc_nstc_max;
     A.kind_doubles = bc_kind_doubles;

@@ -44,14 +44,16 @@ __device__ __forceinline__ McgCellMem mcg_cell_mem(const McgDev& D, const McgKin
   if (smem_warp != nullptr && n <= D.smem_n) {
     const int m = D.smem_n;
     double* p = smem_warp;
+    // V | SP | rhs_cur first: a LIF-only launch of the batch kernel keeps just
+    // these (McgBatchArgs::comp_stride = (2 + sp_max) m, see setup_batch_kernel)
     M.V = p; p += m;
     M.SP = p; p += int64_t(D.sp_max) * m;
+    M.rhs_cur = p; p += m;
     M.HM = p; p += m;
     M.HH = p; p += m;
     M.HN = p; p += m;
     M.gsyn = p; p += m;
     M.gsyn_rhs = p; p += m;
-    M.rhs_cur = p; p += m;
     M.diag = p; p += m;
     M.r2 = p;
   } else {
