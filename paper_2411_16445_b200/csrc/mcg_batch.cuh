@@ -30,6 +30,7 @@
 #include "mcg_sweep.cuh"
 
 #define MCG_NPHASE 24
+#define MCG_LANE_INTS 10
 #ifndef MCG_BATCH_THREADS
 #define MCG_BATCH_THREADS 256
 #endif
@@ -49,6 +50,7 @@ struct McgBatchArgs {
   int32_t ch_pmax;         // P_max = max over kinds of 2 ch_lp + 1
   int32_t ev_cap;          // staged-delivery event buffer entries (0: off)
   int32_t fmask_words;     // changed-flag words (fmask)
+  int32_t nch_max;         // chain-sweep lanes of a batch (lane descriptor table rows)
   unsigned long long* phase;  // optional per-phase cycle totals (MCG_NPHASE)
   double* log_t;           // spike log of the launch
   uint32_t* log_gid;
@@ -545,6 +547,7 @@ struct McgBatchSm {
   uint32_t* floc;   // stc_max: (cell << 16) | group of each STC instance slot
   uint32_t* fmask;  // stc_max / 32 changed-flag words
   McgEvSm* evb;     // staged events (ev_cap entries)
+  int* lanes;       // nch_max x MCG_LANE_INTS static chain-lane descriptors
   int ksm_o;        // offset of ksm in mcg_smem (doubles)
   int chs_o;        // offset of the chain-sweep scratch (C x ch_stride doubles)
 };
@@ -568,7 +571,8 @@ __device__ __forceinline__ McgBatchSm mcg_batch_sm(const McgBatchArgs& A) {
   B.floc = reinterpret_cast<uint32_t*>(B.spec + A.n_specs_sm);
   B.fmask = B.floc + A.stc_max;
   {
-    const uintptr_t e = reinterpret_cast<uintptr_t>(B.fmask + A.fmask_words);
+    B.lanes = reinterpret_cast<int*>(B.fmask + A.fmask_words);
+    const uintptr_t e = reinterpret_cast<uintptr_t>(B.lanes + A.nch_max * MCG_LANE_INTS);
     B.evb = reinterpret_cast<McgEvSm*>((e + 15) & ~uintptr_t(15));
   }
   return B;
@@ -721,7 +725,6 @@ __device__ bool mcg_stage_events(const McgDev& D, const McgBatchArgs& A, const M
     return false;
   }
   const uint64_t rank_mask = (1ull << D.rank_bits) - 1;
-  const int64_t cg0 = D.cg_off[c];
   for (int t = lane; t < nd; t += 32) {
     const uint64_t key = pend[X.cur + t];
     const int64_t r = int64_t(key & rank_mask);
@@ -734,9 +737,8 @@ __device__ bool mcg_stage_events(const McgDev& D, const McgBatchArgs& A, const M
     e.comp = 0;
     e.w = w;
     if (X.gk[grp] == MCG_SYN_STATIC_CHARGE) {  // apply_event: V[comp] += w * cf[comp]
-      const int comp = D.i_comp[D.cgs[cg0 + grp].inst + inst];
-      e.comp = static_cast<uint16_t>(comp);
-      e.w = w * D.k_cf[K.arr + comp];
+      e.comp = static_cast<uint16_t>(D.e_comp[r]);
+      e.w = D.e_wcf[r];
     }
     e.inst = inst | (w != 0.0 ? 0x80000000u : 0u);
     e.src = D.e_src[r];
@@ -820,6 +822,38 @@ __device__ bool mcg_stage_events(const McgDev& D, const McgBatchArgs& A, const M
   }
   __syncwarp();
   return true;
+}
+
+// static part of every chain-sweep lane of batch b (mcg_ph_solve): lane t is
+// (cell t / 2S1, system (t mod 2S1) / 2, side t mod 2); the per-step part
+// (refractory / conductance state, currents, production) is added each step
+__device__ void mcg_lanes_init(const McgDev& D, const McgBatchArgs& A, const McgBatchSm& B,
+                               int nc) {
+  const int S1 = 1 + D.sp_max, m = D.smem_n;
+  for (int t = threadIdx.x; t < A.nch_max; t += blockDim.x) {
+    int* L = B.lanes + t * MCG_LANE_INTS;
+    const int k = t / (2 * S1), rem = t - k * 2 * S1, sys = rem >> 1;
+    for (int i = 0; i < MCG_LANE_INTS; ++i) L[i] = 0;
+    L[0] = -1;
+    if (k >= nc) continue;
+    const McgKind& K = B.kc[k];
+    const McgCellSm& X = B.cs[k];
+    const bool ok = K.ch_lp > 0 && K.n <= m &&
+                    (sys == 0 ? (K.dyn == MCG_DYN_LIF && K.v_const)
+                              : (sys - 1 < K.n_species && K.n > 1 && K.sp_const));
+    const int n = K.n, P = 2 * K.ch_lp + 1;
+    const int cho = B.ksm_o + X.kb + mcg_kind_chain_off(n, K.n_species);
+    L[0] = k;
+    L[1] = sys;
+    L[2] = rem & 1;
+    L[3] = K.ch_lp;
+    L[4] = B.chs_o + k * A.ch_stride + sys * A.ch_pmax;
+    L[5] = 2 * cho;
+    L[6] = cho + (P + 1) / 2 + sys * 6 * P;
+    L[7] = k * A.comp_stride + (sys == 0 ? 0 : m + (sys - 1) * n);
+    L[8] = (ok ? 1 : 0) | (K.ch_afirst ? 2 : 0);
+    L[9] = (sys > 0 && sys - 1 == K.prp_idx) ? K.prp_comp : -1;
+  }
 }
 
 // ---- staging: metadata, kind constants, compartment state of batch b
@@ -979,6 +1013,7 @@ __device__ void mcg_batch_enter(const McgDev& D, const McgBatchArgs& A, int32_t 
         base[(4 + D.sp_max) * m + i] = D.hh_n[co + i];
       }
   }
+  if (A.nch_max > 0) mcg_lanes_init(D, A, B, nc);
   __syncthreads();
 }
 
@@ -1052,31 +1087,27 @@ __device__ __noinline__ void mcg_ph_solve(const McgDev& D, const McgBatchArgs& A
   const int split = nch > 0 ? min(256, T / 2) : 0;
   if (tid < split) {
     for (int t = tid; t < nch; t += split) {
-      const int k = t / (2 * S1), rem = t - k * 2 * S1;
       McgChainLane L{};
-      if (k < nc) {
-        const McgKind& K = kc[k];
+      const int* LD = B.lanes + t * MCG_LANE_INTS;  // static part (mcg_lanes_init)
+      const int k = LD[0];
+      if (k >= 0 && (LD[8] & 1)) {
         const McgCellSm& X = cs[k];
-        const int sys = rem >> 1;
-        L.on = mcg_chain_ok(K, X, sys, m) ? 1 : 0;
-        if (L.on) {
-          const int n = K.n, P = 2 * K.ch_lp + 1;
-          const int cho = B.ksm_o + X.kb + mcg_kind_chain_off(n, K.n_species);
-          L.side = rem & 1;
-          L.lp = K.ch_lp;
-          L.r2c = B.chs_o + k * A.ch_stride + sys * A.ch_pmax;
-          L.idx = 2 * cho;
-          L.fc = cho + (P + 1) / 2 + sys * 6 * P;
-          L.x = k * A.comp_stride + (sys == 0 ? 0 : m + (sys - 1) * n);
-          L.a_first = K.ch_afirst;
-          L.v = sys == 0;
-          // right-hand sides (engine.cpp:683 / 746-748): V: g_leak_rhs + 0.0 +
-          // rhs_current (if any current); species: production at the
-          // synthesis compartment
-          L.rc = (sys == 0 && X.has_current) ? k * A.comp_stride + (1 + D.sp_max) * m : -1;
-          L.pc = (sys > 0 && sys - 1 == K.prp_idx && X.prod != 0.0) ? K.prp_comp : -1;
-          L.prod = X.prod;
-        }
+        const int sys = LD[1];
+        L.on = (sys != 0 || (!X.refractory && !X.has_gsyn)) ? 1 : 0;
+        L.side = LD[2];
+        L.lp = LD[3];
+        L.r2c = LD[4];
+        L.idx = LD[5];
+        L.fc = LD[6];
+        L.x = LD[7];
+        L.a_first = (LD[8] >> 1) & 1;
+        L.v = sys == 0;
+        // right-hand sides (engine.cpp:683 / 746-748): V: g_leak_rhs + 0.0 +
+        // rhs_current (if any current); species: production at the
+        // synthesis compartment
+        L.rc = (sys == 0 && X.has_current) ? k * A.comp_stride + (1 + D.sp_max) * m : -1;
+        L.pc = (LD[9] >= 0 && X.prod != 0.0) ? LD[9] : -1;
+        L.prod = X.prod;
       }
       MCG_PH(19);
       mcg_chain_lane(L);

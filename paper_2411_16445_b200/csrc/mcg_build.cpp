@@ -745,6 +745,23 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
       for (int i = 0; i < K.n; ++i)
         if (m.k_g_na[K.arr + i] != 0.0) ++m.hh_comps;
   }
+  // static-charge edges: the instance's compartment and w * cf[comp] (the
+  // product apply_event forms, engine.cpp:455-459), so staged delivery reads
+  // one edge record instead of chasing group -> instance -> compartment
+  {
+    const int64_t ne = static_cast<int64_t>(m.e_dst.size());
+    m.e_comp.assign(ne, -1);
+    m.e_wcf.assign(ne, 0.0);
+    for (int64_t r = 0; r < ne; ++r) {
+      const int c = m.e_dst[r];
+      const McgCellGroup& G = m.cgs[m.cg_off[c] + m.e_group[r]];
+      if (m.specs[G.spec].kind != MCG_SYN_STATIC_CHARGE) continue;
+      const McgKind& K = m.kinds[m.cell_kind[c]];
+      const int comp = m.i_comp[G.inst + m.e_inst[r]];
+      m.e_comp[r] = comp;
+      m.e_wcf[r] = m.e_weight[r] * m.k_cf[K.arr + comp];
+    }
+  }
 }
 
 }  // namespace mcg

@@ -94,6 +94,8 @@ struct HostModel {
   std::vector<uint32_t> e_inst;
   std::vector<double> e_weight;
   std::vector<uint32_t> e_src, e_seq;       // EventRec.src / seq of each edge (EventOrder)
+  std::vector<int32_t> e_comp;              // static-charge edges: target compartment (else -1)
+  std::vector<double> e_wcf;                // and weight * charge_factor[comp] (engine.cpp:457)
   std::vector<int64_t> e_delay;
   std::vector<int64_t> out_begin, out_end;  // per global gid
   std::vector<int64_t> src_edge_off;        // per source CSR into src_edges

@@ -85,6 +85,8 @@ struct McgDev {
   const uint32_t* e_inst;
   const double* e_weight;
   const uint32_t* e_src;      // EventRec.src of each edge (gid, 0xFFFFFFFF for sources)
+  const int32_t* e_comp;      // static-charge edges: compartment, w * cf (mcg_build.cpp)
+  const double* e_wcf;
   const int64_t* e_delay;
   // spikes of this epoch: [cell][sp_cap]
   int32_t sp_cap;

@@ -130,6 +130,8 @@ struct Engine {
   DBuf<uint32_t> d_e_inst;
   DBuf<double> d_e_weight;
   DBuf<uint32_t> d_e_src;
+  DBuf<int32_t> d_e_comp;
+  DBuf<double> d_e_wcf;
   DBuf<int64_t> d_e_delay, d_out_begin, d_out_end, d_src_edge_off, d_src_edges;
   int32_t rank_bits = 1;
   // sources
@@ -174,6 +176,7 @@ struct Engine {
   int32_t bc_ch_pmax = 0, bc_ch_stride = 0;
   int32_t bc_ev_cap = 0, bc_fmask_words = 0;
   int32_t bc_stride = 0;  // doubles per staged cell's compartment block
+  int32_t bc_nch_max = 0;  // chain-sweep lane descriptors per batch
   int32_t bc_kind_doubles = 0, bc_specs_sm = 0, bc_stc_sm = 0;
   size_t bc_smem = 0;
   DBuf<int4> d_chunks;
@@ -309,7 +312,9 @@ struct Engine {
     bc_kind_doubles = static_cast<int32_t>(std::min<size_t>(bc_cells, m.kinds.size()) * kb_max);
     // fold-flag words: one per 32 slots of every 512-thread round
     const size_t fmask_words = size_t((bc_stc_max + kBatchThreads - 1) / kBatchThreads) * (kBatchThreads / 32) + 1;
-    bc_smem = size_t(bc_cells) * (size_t(bc_stride) * 8 + 32 * 8 + sizeof(McgKind) + sizeof(McgCellSm) +
+    bc_nch_max = bc_ch_stride > 0 ? (2 * (1 + sp_max) * bc_cells + 31) / 32 * 32 : 0;
+    bc_smem = size_t(bc_nch_max) * MCG_LANE_INTS * 4 + 16 +
+              size_t(bc_cells) * (size_t(bc_stride) * 8 + 32 * 8 + sizeof(McgKind) + sizeof(McgCellSm) +
                                   size_t(bc_nstc_max) * sizeof(McgSegSm) + size_t(bc_ch_stride) * 8) +
               size_t(bc_stc_max) * (8 + 4) + size_t(bc_kind_doubles) * 8 +
               size_t(bc_specs_sm) * sizeof(McgSpec) + fmask_words * 4 + 64;
@@ -453,6 +458,8 @@ struct Engine {
     d_e_inst.upload(m.e_inst, st);
     d_e_weight.upload(m.e_weight, st);
     d_e_src.upload(m.e_src, st);
+    d_e_comp.upload(m.e_comp, st);
+    d_e_wcf.upload(m.e_wcf, st);
     d_e_delay.upload(m.e_delay, st);
     d_out_begin.upload(m.out_begin, st);
     d_out_end.upload(m.out_end, st);
@@ -661,6 +668,8 @@ struct Engine {
     D.e_inst = d_e_inst.p;
     D.e_weight = d_e_weight.p;
     D.e_src = d_e_src.p;
+    D.e_comp = d_e_comp.p;
+    D.e_wcf = d_e_wcf.p;
     D.e_delay = d_e_delay.p;
     D.sp_cap = sp_cap;
     D.sp_count = d_sp_count.p;
@@ -793,6 +802,7 @@ struct Engine {
     A.ch_stride = bc_ch_stride;
     A.ch_pmax = bc_ch_pmax;
     A.ev_cap = bc_ev_cap;
+    A.nch_max = bc_nch_max;
     A.fmask_words = bc_fmask_words;
     if (phase_timing) {
       if (!d_phase.p) {
