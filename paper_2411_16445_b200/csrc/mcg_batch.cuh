@@ -1560,9 +1560,24 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
             const int lim = min(32 - lo, fe - f);
             uint32_t bits = B.fmask[w] >> lo;
             if (lim < 32) bits &= (1u << lim) - 1u;
+            // up to four slots' loads are issued ahead of their in-order adds
             while (bits) {
-              acc += B.dbuf[f + __ffs(bits) - 1];
+              const int i0 = __ffs(bits) - 1;
               bits &= bits - 1u;
+              const int i1 = bits ? __ffs(bits) - 1 : -1;
+              bits &= bits - 1u;
+              const int i2 = bits ? __ffs(bits) - 1 : -1;
+              bits &= bits - 1u;
+              const int i3 = bits ? __ffs(bits) - 1 : -1;
+              bits &= bits - 1u;
+              const double a0 = B.dbuf[f + i0];
+              const double a1 = i1 >= 0 ? B.dbuf[f + i1] : 0.0;
+              const double a2 = i2 >= 0 ? B.dbuf[f + i2] : 0.0;
+              const double a3 = i3 >= 0 ? B.dbuf[f + i3] : 0.0;
+              acc += a0;
+              if (i1 >= 0) acc += a1;
+              if (i2 >= 0) acc += a2;
+              if (i3 >= 0) acc += a3;
             }
             f += lim;
           }
