@@ -51,6 +51,7 @@ struct McgBatchArgs {
   int32_t ev_cap;          // staged-delivery event buffer entries (0: off)
   int32_t fmask_words;     // changed-flag words (fmask)
   int32_t nch_max;         // chain-sweep lanes of a batch (lane descriptor table rows)
+  int32_t lean;            // LIF-only launch (compartment block V | SP | rhs_cur)
   unsigned long long* phase;  // optional per-phase cycle totals (MCG_NPHASE)
   double* log_t;           // spike log of the launch
   uint32_t* log_gid;
@@ -856,6 +857,12 @@ __device__ void mcg_lanes_init(const McgDev& D, const McgBatchArgs& A, const Mcg
   }
 }
 
+// kind blocks currently staged (offset, kind) per slot, kept across the
+// batches of one launch (reset at launch start)
+#define MCG_KSLOTS 16
+__shared__ int mcg_kslot_off[MCG_KSLOTS];
+__shared__ long long mcg_kslot_arr[MCG_KSLOTS];
+
 // ---- staging: metadata, kind constants, compartment state of batch b
 __device__ void mcg_batch_enter(const McgDev& D, const McgBatchArgs& A, int32_t b) {
   const McgBatchSm B = mcg_batch_sm(A);
@@ -964,12 +971,34 @@ __device__ void mcg_batch_enter(const McgDev& D, const McgBatchArgs& A, int32_t 
     }
   }
   __syncthreads();
+  // a kind block already holding the same kind (an earlier batch of this
+  // launch, same offset) is not staged again
+  int slot = 0;
   for (int k = 0; k < nc; ++k) {
     if (B.cs[k].kb < 0) continue;
     bool first = true;
     for (int q = 0; q < k; ++q)
       if (B.cs[q].kb == B.cs[k].kb) first = false;
-    if (first) mcg_kind_stage(D, B.kc[k], B.ksm + B.cs[k].kb);
+    if (!first) continue;
+    const bool have = slot < MCG_KSLOTS && mcg_kslot_off[slot] == B.cs[k].kb &&
+                      mcg_kslot_arr[slot] == B.kc[k].arr;
+    if (!have) mcg_kind_stage(D, B.kc[k], B.ksm + B.cs[k].kb);
+    ++slot;
+  }
+  __syncthreads();
+  if (tid == 0) {  // record what the kind blocks now hold
+    int sl = 0;
+    for (int k = 0; k < nc && sl < MCG_KSLOTS; ++k) {
+      if (B.cs[k].kb < 0) continue;
+      bool first = true;
+      for (int q = 0; q < k; ++q)
+        if (B.cs[q].kb == B.cs[k].kb) first = false;
+      if (!first) continue;
+      mcg_kslot_off[sl] = B.cs[k].kb;
+      mcg_kslot_arr[sl] = B.kc[k].arr;
+      ++sl;
+    }
+    for (; sl < MCG_KSLOTS; ++sl) mcg_kslot_off[sl] = -1;
   }
   // STC instance locator: slot f -> (cell, group)
   for (int k = 0; k < nc; ++k) {
@@ -1084,7 +1113,8 @@ __device__ __noinline__ void mcg_ph_solve(const McgDev& D, const McgBatchArgs& A
   // (cell, system, chain) on threads [0, split), beside the other systems
   // (thread per (cell, system)) on [split, T)
   const int nch = (A.ch_stride > 0) ? ((2 * S1 * nc + 31) & ~31) : 0;
-  const int split = nch > 0 ? min(256, T / 2) : 0;
+  // LIF-only launches (A.lean): the other systems are point cells, one warp suffices
+  const int split = nch > 0 ? (A.lean ? min(nch, T - 32) : min(256, T / 2)) : 0;
   if (tid < split) {
     for (int t = tid; t < nch; t += split) {
       McgChainLane L{};
@@ -1776,10 +1806,10 @@ __global__ void __launch_bounds__(MCG_BATCH_THREADS, 1) k_batch(const __grid_con
     for (int i = 0; i < MCG_NPHASE; ++i) mcg_ph_acc[i] = 0;
     mcg_ph_acc[MCG_NPHASE] = clock64();
   }
-  if (A.n_specs_sm > 0) {
+  if (threadIdx.x < MCG_KSLOTS) mcg_kslot_off[threadIdx.x] = -1;
+  if (A.n_specs_sm > 0)
     for (int i = threadIdx.x; i < A.n_specs_sm; i += blockDim.x) B.spec[i] = D.specs[i];
-    __syncthreads();
-  }
+  __syncthreads();
   // resident: every batch has its own CTA for the whole launch
   const bool resident = A.n_batches <= int(gridDim.x);
   const bool mine = int(blockIdx.x) < A.n_batches;

@@ -177,6 +177,7 @@ struct Engine {
   int32_t bc_ev_cap = 0, bc_fmask_words = 0;
   int32_t bc_stride = 0;  // doubles per staged cell's compartment block
   int32_t bc_nch_max = 0;  // chain-sweep lane descriptors per batch
+  int32_t bc_lean = 0;
   int32_t bc_kind_doubles = 0, bc_specs_sm = 0, bc_stc_sm = 0;
   size_t bc_smem = 0;
   DBuf<int4> d_chunks;
@@ -275,6 +276,7 @@ struct Engine {
       }
     }
     bc_stride = lean ? (2 + sp_max) * smem_n : smem_stride;
+    bc_lean = lean ? 1 : 0;
     // per cell: compartment block, noise draws, kind and cell records, STC
     // segments, and (upper bound) its STC slots in the fold/locator tables
     // chain-sweep scratch: (1 + sp_max) systems x P_max positions per cell
@@ -803,6 +805,7 @@ struct Engine {
     A.ch_pmax = bc_ch_pmax;
     A.ev_cap = bc_ev_cap;
     A.nch_max = bc_nch_max;
+    A.lean = bc_lean;
     A.fmask_words = bc_fmask_words;
     if (phase_timing) {
       if (!d_phase.p) {

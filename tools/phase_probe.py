@@ -31,11 +31,14 @@ os.environ["MCG_PHASE_TIMING"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2411_16445_b200 import network as N, Engine, EngineOptions
 n = int(os.environ.get("PROBE_N", "2000"))
-c = N.ConsolidationConfig(n_cells=n, n_exc=n * 4 // 5, seed=1, multi_compartment=True)
+ne = n * 4 // 5
+dend = N.DendriteSize.large_dendrites if os.environ.get("PROBE_DEND") == "large" else N.DendriteSize.small_dendrites
+c = N.ConsolidationConfig(n_cells=n, n_exc=ne, p_conn=min(0.1, 0.1 * 1600 / ne), seed=1,
+                          multi_compartment=True, dend_size=dend)
 b = N.build_consolidation_network(c, True)
 e = Engine(b.recipe, EngineOptions(0.5, 1))
 ctas = e.stats().get("batch_grid", 143)
-for t1 in (1000.0, 3000.0, 10000.0, 12000.0):
+for t1 in [float(x) for x in os.environ.get("PROBE_T", "1000,3000,10000,12000").split(",")]:
     s0 = e.stats()["steps"]
     a = time.time(); e.advance_to(t1); w = time.time() - a
     st = e.stats()["steps"] - s0

@@ -140,6 +140,54 @@ __global__ void bench_chain(int reps, long long* cyc, const double* g_init) {
   if (threadIdx.x == 0) cyc[10] = (t1 - t0) / reps;
 }
 
+
+// the kernel's lane layout: 5 cells x 3 systems x 2 sides on lanes 0..29
+// (chain constants shared per system, r2c and x per cell at the kernel strides)
+__global__ void bench_chain30(int reps, long long* cyc, const double* g_init, int cell_stride,
+                              int ch_stride) {
+  double* S = mcg_smem;
+  int32_t* PI = reinterpret_cast<int32_t*>(S);
+  const int n = 31, lp = 20, P = 2 * lp + 1;
+  const int idx = 0;                   // int32 units
+  const int fc0 = 64;                  // 3 systems x 6 P
+  const int r2c0 = fc0 + 3 * 6 * P + 8;
+  const int x0 = r2c0 + 5 * ch_stride + 8;
+  if (threadIdx.x == 0) {
+    for (int p = 0; p < P; ++p) PI[idx + p] = -1;
+    int k = 0;
+    for (int i = 1; i <= 6; ++i) PI[idx + lp - 1 - k++] = i;
+    for (int i = 13; i <= 25; ++i) PI[idx + lp - 1 - k++] = i;
+    k = 0;
+    for (int i = 7; i <= 12; ++i) PI[idx + 2 * lp - 1 - k++] = i;
+    for (int i = 26; i <= 30; ++i) PI[idx + 2 * lp - 1 - k++] = i;
+    PI[idx + 2 * lp] = 0;
+    for (int sy = 0; sy < 3; ++sy)
+      for (int p = 0; p < P; ++p) {
+        const int i = PI[idx + p];
+        double* q = S + fc0 + sy * 6 * P;
+        q[p] = i < 0 ? -0.0 : g_init[i];
+        q[P + p] = i < 0 ? 0.0 : g_init[2 * n + i];
+        q[2 * P + p] = i < 0 ? 1.0 : g_init[n + i];
+        q[3 * P + p] = i < 0 ? 1.0 : 1.0 / g_init[n + i];
+        q[4 * P + p] = i < 0 ? 0.0 : g_init[3 * n + i];
+        q[5 * P + p] = i < 0 ? 0.0 : 0.25;
+      }
+    for (int c = 0; c < 5; ++c)
+      for (int i = 0; i < 3 * n; ++i) S[x0 + c * cell_stride + i] = -65.0 + i;
+  }
+  __syncthreads();
+  const int t = threadIdx.x, c = t / 6, sy = (t % 6) / 2, side = t & 1;
+  McgChainLane L{t < 30, side, lp, r2c0 + c * ch_stride + sy * P, fc0 + sy * 6 * P, idx,
+                 x0 + c * cell_stride + (sy == 0 ? 0 : n + (sy - 1) * n), 0, sy == 0, -1, -1, 0.0};
+  long long t0 = clock64();
+  for (int r = 0; r < reps; ++r) {
+    mcg_chain_lane(L);
+    __syncwarp();
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[11] = (t1 - t0) / reps;
+}
+
 int main() {
   const int n = 31;
   std::vector<double> h(4 * n);
@@ -167,5 +215,14 @@ int main() {
   bench_chain<<<1, 32, 16 * 1024>>>(1000, cyc, g);
   cudaError_t e2 = cudaDeviceSynchronize();
   printf("chain lanes: %lld cycles per sweep (%s)\n", cyc[10], cudaGetErrorString(e2));
+  cudaFuncSetAttribute(bench_chain30, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+  for (int cs : {124, 128, 132, 125}) {
+    for (int chs : {123, 128, 129}) {
+      bench_chain30<<<1, 32, 64 * 1024>>>(100, cyc, g, cs, chs);
+      bench_chain30<<<1, 32, 64 * 1024>>>(1000, cyc, g, cs, chs);
+      cudaError_t e3 = cudaDeviceSynchronize();
+      printf("chain 30 lanes cell_stride %d ch_stride %d: %lld cycles (%s)\n", cs, chs, cyc[11], cudaGetErrorString(e3));
+    }
+  }
   return 0;
 }
