@@ -1353,9 +1353,15 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
               ++g.f_tail;
             }
             ++X.iseq;
-            if (!refractory) {
-              const int sl = X.stc_off + g.start + int(inst);
-              const double tw = B.stc[sl] + g.h0 * B.stc[S4 + sl];
+            if (!refractory) {  // stc_total_weight: h + h0 * z
+              double tw;
+              if (A.stc_sm) {
+                const int sl = X.stc_off + g.start + int(inst);
+                tw = B.stc[sl] + g.h0 * B.stc[S4 + sl];
+              } else {
+                const int64_t j = g.inst + inst;
+                tw = D.i_stc_h[j] + g.h0 * D.i_stc_z[j];
+              }
               V[g.comp] += tw * E.w * g.cf;
             }
           }
@@ -1367,7 +1373,8 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
         while (q < X.in_end && int(B.evb[q].so) == int(so)) {
           const McgEvSm E = B.evb[q];
           const McgSegSm& g = B.seg[tid * A.n_stc_max + X.gseg[E.group]];
-          B.stc[2 * S4 + X.stc_off + g.start + int(E.inst)] += g.cpre_s;
+          if (A.stc_sm) B.stc[2 * S4 + X.stc_off + g.start + int(E.inst)] += g.cpre_s;
+          else D.i_stc_c[g.inst + E.inst] += g.cpre_s;
           ++q;
         }
         X.in_cur = q;

@@ -303,6 +303,8 @@ struct Engine {
            fixed + size_t(c_max + 1) * per_cell + std::min<size_t>(c_max + 1, nkinds) * kb_max * 8 <= budget)
       ++c_max;
     bc_cells = std::clamp((nl + dev_sms - 1) / std::max(dev_sms, 1), 1, std::min(c_max, 0xffff));
+    // test hook: cap the batch size (forces per-epoch batch staging on small nets)
+    if (const char* cap = std::getenv("MCG_MAX_CELLS_PER_CTA")) bc_cells = std::max(1, std::min(bc_cells, std::atoi(cap)));
     bc_batches = std::max(1, (nl + bc_cells - 1) / bc_cells);
     // STC slots of the fullest batch
     bc_stc_max = 1;
@@ -332,7 +334,7 @@ struct Engine {
     // staged delivery: the epoch's due events of the resident batch in shared
     // memory (mcg_stage_events), in whatever the opt-in limit leaves
     bc_ev_cap = 0;
-    if (bc_stc_sm && !std::getenv("MCG_NO_STAGED_EVENTS")) {
+    if (!std::getenv("MCG_NO_STAGED_EVENTS")) {
       const size_t lim = size_t(smem_optin) - 4096;  // static shared memory of the kernel
       const size_t left = lim > bc_smem + 32 ? lim - bc_smem - 32 : 0;
       bc_ev_cap = static_cast<int32_t>(std::min<size_t>(left / sizeof(McgEvSm), 4096));
