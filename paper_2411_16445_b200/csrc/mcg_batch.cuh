@@ -949,7 +949,9 @@ __device__ void mcg_batch_enter(const McgDev& D, const McgBatchArgs& A, int32_t 
   }
   __syncthreads();
   if (tid == 0) {
-    int acc = 0, hacc = 0, kacc = 0;
+    int acc = 0, hacc = 0, kacc = 0, nk = 0;
+    long long karr[MCG_KSLOTS];
+    int kbs[MCG_KSLOTS];
     for (int k = 0; k < nc; ++k) {
       B.cs[k].stc_off = acc;
       acc += B.cs[k].stc_n;
@@ -958,13 +960,17 @@ __device__ void mcg_batch_enter(const McgDev& D, const McgBatchArgs& A, int32_t 
       // one staged copy per distinct kind of the batch
       B.cs[k].kb = -1;
       if (B.cs[k].n <= m) {
-        for (int q = 0; q < k; ++q)
-          if (B.kc[q].arr == B.kc[k].arr && B.cs[q].kb >= 0) {
-            B.cs[k].kb = B.cs[q].kb;
+        for (int q = 0; q < nk; ++q)  // the batch's distinct kinds so far
+          if (karr[q] == B.kc[k].arr) {
+            B.cs[k].kb = kbs[q];
             break;
           }
         if (B.cs[k].kb < 0) {
           B.cs[k].kb = kacc;
+          if (nk < MCG_KSLOTS) {
+            karr[nk] = B.kc[k].arr;
+            kbs[nk++] = kacc;
+          }
           kacc += mcg_kind_block_doubles(B.kc[k].n, B.kc[k].n_species, B.kc[k].ch_lp);
         }
       }
@@ -1000,12 +1006,12 @@ __device__ void mcg_batch_enter(const McgDev& D, const McgBatchArgs& A, int32_t 
     }
     for (; sl < MCG_KSLOTS; ++sl) mcg_kslot_off[sl] = -1;
   }
-  // STC instance locator: slot f -> (cell, group)
-  for (int k = 0; k < nc; ++k) {
+  // STC instance locator: slot f -> (cell, group), warp per cell
+  for (int k = tid >> 5; k < nc; k += T >> 5) {
     const McgCellSm& X = B.cs[k];
     for (int q = 0; q < X.n_stc_seg; ++q) {
       const McgSegSm& g = B.seg[k * A.n_stc_max + q];
-      for (int i = tid; i < g.size; i += T)
+      for (int i = tid & 31; i < g.size; i += 32)
         B.floc[X.stc_off + g.start + i] = (uint32_t(k) << 16) | uint32_t(q);
     }
   }
@@ -1024,23 +1030,29 @@ __device__ void mcg_batch_enter(const McgDev& D, const McgBatchArgs& A, int32_t 
       B.stc[3 * S4 + f] = D.i_sps_abs[j];
     }
   }
-  // compartment state (cells that fit; the rest use global memory)
-  for (int k = 0; k < nc; ++k) {
-    const int c = c0 + k;
-    const McgKind& K = B.kc[k];
-    if (K.n > m) continue;
-    double* base = mcg_comp_block(A, B, k);
-    const int n = K.n;
-    const int64_t co = D.comp_off[c];
-    for (int i = tid; i < n; i += T) base[i] = D.v[co + i];
-    const double* gs = D.species + D.sp_off[c];
-    for (int i = tid; i < K.n_species * n; i += T) base[m + i] = gs[i];
-    if (K.dyn == MCG_DYN_HH)
-      for (int i = tid; i < n; i += T) {
-        base[(2 + D.sp_max) * m + i] = D.hh_m[co + i];
-        base[(3 + D.sp_max) * m + i] = D.hh_h[co + i];
-        base[(4 + D.sp_max) * m + i] = D.hh_n[co + i];
+  // compartment state (cells that fit; the rest use global memory), one flat
+  // loop over (cell, V | species | HH slot) so all loads are in flight together
+  {
+    const int per = (1 + D.sp_max + 3) * m;
+    for (int idx = tid; idx < nc * per; idx += T) {
+      const int k = idx / per, r = idx - k * per;
+      const McgKind& K = B.kc[k];
+      const int n = K.n;
+      if (n > m) continue;
+      const int a = r / m, i = r - a * m;  // array a, compartment i
+      if (i >= n) continue;
+      double* base = mcg_comp_block(A, B, k);
+      const int c = c0 + k;
+      if (a == 0) {
+        base[i] = D.v[D.comp_off[c] + i];
+      } else if (a <= D.sp_max) {
+        if (a - 1 < K.n_species) base[m + (a - 1) * n + i] = D.species[D.sp_off[c] + (a - 1) * n + i];
+      } else if (K.dyn == MCG_DYN_HH) {
+        const int h = a - 1 - D.sp_max;  // 0: m, 1: h, 2: n
+        const double* src = h == 0 ? D.hh_m : (h == 1 ? D.hh_h : D.hh_n);
+        base[(2 + D.sp_max + h) * m + i] = src[D.comp_off[c] + i];
       }
+    }
   }
   if (A.nch_max > 0) mcg_lanes_init(D, A, B, nc);
   __syncthreads();
