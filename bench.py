@@ -232,6 +232,20 @@ def other_configs():
                      "setup_s": setup}
         e.close()
         del b
+    # config 2: one MC neuron, 1000 Poisson inputs (5 Hz) onto STC + STDP synapses, dt 0.1 ms
+    rec = N.build_single_neuron_plastic(n_inputs=1000, rate_hz=5.0, duration_ms=3000.0, dt_ms=0.1)
+    e = Engine(rec.flatten(), EngineOptions(0.1, SEED))
+    e.set_timing(True)
+    e.advance_to(500.0)
+    s0 = e.stats()
+    e.advance_to(2500.0)
+    s1 = e.stats()
+    sec = (s1["advance_ms"] - s0["advance_ms"]) * 1e-3
+    steps = s1["steps"] - s0["steps"]
+    out["config2_single_neuron_1000"] = {"inputs": 1000, "dt_ms": 0.1, "bio_ms": 2000.0,
+                                         "sim_s_per_wall_s": 2.0 / sec,
+                                         "us_per_fine_step": 1e6 * sec / steps}
+    e.close()
     p = PR.GbParams()
     deltas = [-100.0, -50.0, -30.0, -20.0, -10.0, -5.0, 0.0, 5.0, 10.0, 20.0, 30.0, 50.0, 100.0]
     proto = PR.GbPairingProtocol(dt_ms=0.05, trials=4000, seed=999)

@@ -249,7 +249,7 @@ class ConnectionTable:
         n = len(src)
         self.from_source = np.ascontiguousarray(np.broadcast_to(from_source, n), dtype=np.uint8)
         self.src = np.ascontiguousarray(src, dtype=np.uint32)
-        self.dst = np.ascontiguousarray(dst, dtype=np.uint32)
+        self.dst = np.ascontiguousarray(np.broadcast_to(dst, n), dtype=np.uint32)
         self.labels = list(labels)
         self.label_idx = np.ascontiguousarray(np.broadcast_to(label_idx, n), dtype=np.int32)
         self.policy = np.ascontiguousarray(np.broadcast_to(policy, n), dtype=np.uint8)

@@ -72,3 +72,16 @@ def test_grid_layout_matches_reference_discretize():
     assert g.compartment_at(cell.apical_seg, 1.0) == 25
     assert g.compartment_at(cell.basal_seg, 1.0) == 30
     assert g.compartment_at(cell.soma_center_seg, 0.5) == 0
+
+
+def test_single_neuron_plastic_recipe():
+    """Config 2's recipe: per source one STC then one STDP connection,
+    all onto cell 0 (a scalar dst broadcasts)."""
+    from paper_2411_16445_b200 import network as N
+    r = N.build_single_neuron_plastic(n_inputs=50, duration_ms=100.0, dt_ms=0.1)
+    c = r.connections
+    assert len(c) == 100
+    assert list(c.src[:6]) == [0, 0, 1, 1, 2, 2]
+    assert [c.labels[i] for i in c.label_idx[:4]] == ["rec", "stdp", "rec", "stdp"]
+    assert set(c.dst.tolist()) == {0}
+    assert r.flatten().view.n_connections == 100
