@@ -1487,7 +1487,9 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
       // changed slots set their flag bit (fmask, cleared in phase A) and leave
       // their SPS delta at their own slot of dbuf
       const int S4 = A.stc_max;
-      for (int k = warp; k < nc; k += nwarps) {
+      // few cells (a single neuron with many synapses): parts of each cell's
+      // instances go to different warps (part p takes instances p*32 + lane, step 32 P)
+      auto stc_cell = [&](int k, int i0, int istep) {
         const McgCellSm& X = cs[k];
         const int c = c0 + k;
         for (int q = 0; q < X.n_stc_seg; ++q) {
@@ -1505,7 +1507,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
             }
           }
           const int fb = X.stc_off + g.start;
-          for (int i = lane; i < g.size; i += 32) {
+          for (int i = i0; i < g.size; i += istep) {
             const int f = fb + i;
             const double h = B.stc[f], cc = B.stc[2 * S4 + f], a = B.stc[3 * S4 + f];
             if (mcg_stc_at_rest(R, late, prp, h, cc, a)) {
@@ -1525,6 +1527,15 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
               atomicOr(&B.fmask[f >> 5], 1u << (f & 31));
             }
           }
+        }
+      };
+      const int parts = max(1, nwarps / nc);
+      if (parts == 1) {
+        for (int k = warp; k < nc; k += nwarps) stc_cell(k, lane, 32);
+      } else {
+        for (int it = warp; it < nc * parts; it += nwarps) {
+          const int k = it / parts, part = it - k * parts;
+          stc_cell(k, part * 32 + lane, 32 * parts);
         }
       }
     } else

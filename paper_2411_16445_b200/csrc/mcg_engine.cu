@@ -349,7 +349,9 @@ struct Engine {
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_batch, kBatchThreads, bc_smem));
     if (occ < 1) throw Error(MCG_ERR_CUDA, "batch kernel does not fit on an SM");
-    bc_grid = std::min(bc_batches, occ * dev_sms);
+    // at least one CTA per SM: the CTAs without a batch still expand source
+    // events and spikes (a single neuron with 1000 Poisson inputs)
+    bc_grid = std::min(bc_batches < dev_sms / 2 ? dev_sms : bc_batches, occ * dev_sms);
     if (bc_stc_sm && bc_grid < bc_batches) throw Error(MCG_ERR_CUDA, "batch kernel: not resident");
     d_chunks.alloc(size_t(kBatch) * bc_batches + 1);
     d_chunk_n.alloc(1);

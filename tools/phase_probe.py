@@ -24,7 +24,7 @@ if "--child" not in sys.argv:
         print(wins[w].split()[1] if w < len(wins) else "", cta[4 * w])
         for l in cta[4 * w + 1:4 * w + 4]:
             head, rest = l.split(":", 1)
-            vals = [x.split(":") for x in rest.split()]
+            vals = [x.split(":") for x in rest.split() if x.count(":") == 1]
             print("   ", head.strip(), " ".join(f"{i}:{float(x) / steps / 1965:.2f}" for i, x in vals if float(x) > 0))
     sys.exit(0)
 os.environ["MCG_PHASE_TIMING"] = "1"
@@ -35,8 +35,12 @@ ne = n * 4 // 5
 dend = N.DendriteSize.large_dendrites if os.environ.get("PROBE_DEND") == "large" else N.DendriteSize.small_dendrites
 c = N.ConsolidationConfig(n_cells=n, n_exc=ne, p_conn=min(0.1, 0.1 * 1600 / ne), seed=1,
                           multi_compartment=True, dend_size=dend)
-b = N.build_consolidation_network(c, True)
-e = Engine(b.recipe, EngineOptions(0.5, 1))
+if os.environ.get("PROBE_CFG") == "config2":
+    rec = N.build_single_neuron_plastic(n_inputs=1000, rate_hz=5.0, duration_ms=3000.0, dt_ms=0.1)
+    e = Engine(rec.flatten(), EngineOptions(0.1, 1))
+else:
+    b = N.build_consolidation_network(c, True)
+    e = Engine(b.recipe, EngineOptions(0.5, 1))
 ctas = e.stats().get("batch_grid", 143)
 for t1 in [float(x) for x in os.environ.get("PROBE_T", "1000,3000,10000,12000").split(",")]:
     s0 = e.stats()["steps"]
