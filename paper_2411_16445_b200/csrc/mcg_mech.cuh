@@ -13,6 +13,11 @@ __device__ __forceinline__ bool mcg_decay_active(const McgDev& D, McgCellGroup* 
   const int na = G->active_n;
   const int64_t base = G->inst;
   int out = 0;
+  // the reference's in-order fold acc[comp] += kv (and acc2[comp] += kv * erev),
+  // run by every lane on shuffled values with the running sums in registers
+  // while consecutive kernels share a compartment (they usually all do)
+  int rc = -1;
+  double r1 = 0.0, r2 = 0.0;
   for (int a0 = 0; a0 < na; a0 += 32) {
     const int a = a0 + lane;
     int i = 0, comp = 0;
@@ -32,16 +37,46 @@ __device__ __forceinline__ bool mcg_decay_active(const McgDev& D, McgCellGroup* 
     if (keep) D.i_active[base + out + __popc(m & mcg_lanemask_lt())] = i;
     unsigned mm = m;
     while (mm) {
-      const int l = __ffs(mm) - 1;
-      mm &= mm - 1;
-      const double kl = __shfl_sync(MCG_FULL, kv, l);
-      const int cl = __shfl_sync(MCG_FULL, comp, l);
-      if (lane == 0) {
-        acc[cl] += kl;
-        if (cond) acc2[cl] += kl * erev;
+      // up to four kept kernels per batch of shuffles, folded in order
+      int l[4];
+      int cnt = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        l[u] = mm ? __ffs(mm) - 1 : 0;
+        if (mm) {
+          mm &= mm - 1;
+          cnt = u + 1;
+        }
+      }
+      double kl[4];
+      int cl[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        kl[u] = __shfl_sync(MCG_FULL, kv, l[u]);
+        cl[u] = __shfl_sync(MCG_FULL, comp, l[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (u >= cnt) break;
+        if (cl[u] != rc) {
+          if (rc >= 0 && lane == 0) {
+            acc[rc] = r1;
+            if (cond) acc2[rc] = r2;
+          }
+          __syncwarp();
+          rc = cl[u];
+          r1 = acc[rc];
+          if (cond) r2 = acc2[rc];
+        }
+        r1 += kl[u];
+        if (cond) r2 += kl[u] * erev;
       }
     }
     out += __popc(m);
+  }
+  if (rc >= 0 && lane == 0) {
+    acc[rc] = r1;
+    if (cond) acc2[rc] = r2;
   }
   __syncwarp();
   if (lane == 0) G->active_n = out;
