@@ -6,6 +6,9 @@
 #include "mcg_build.h"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <map>
 #include <numbers>
@@ -242,7 +245,22 @@ void partition(const mcg_recipe& r, int world, std::vector<uint32_t>& bounds) {
   while (w < world) bounds[w++] = static_cast<uint32_t>(n);
 }
 
+namespace {
+// MCG_PROFILE_BUILD=1: host build stage times on stderr
+struct StageTimer {
+  bool on = std::getenv("MCG_PROFILE_BUILD") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "build %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+}  // namespace
+
 void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
+  StageTimer tm;
   const double dt = opt.dt_ms;
   m.dt = dt;
   m.seed = opt.seed;
@@ -471,6 +489,7 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
     }
   }
 
+  tm.mark("kinds");
   // ---- local cells (engine.cpp:317-348) ----
   const uint32_t g0 = m.gid_begin, g1 = m.gid_end;
   for (uint32_t gid = 0; gid < static_cast<uint32_t>(r.n_cells); ++gid)
@@ -531,6 +550,7 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
         m.species[m.sp_off[c] + static_cast<int64_t>(s) * K.n + i] = spec.species[s].init;
   }
 
+  tm.mark("cells");
   // ---- synapse instances: pre-placed then per connection ----
   // gather per (local cell, group) instance lists in creation order
   std::vector<std::vector<int32_t>> inst_comp(cgs);
@@ -557,6 +577,7 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
   std::vector<Edge> edges;
   std::map<std::pair<uint32_t, int32_t>, int> cursors;
   const int64_t nconn = r.n_connections;
+  edges.reserve(static_cast<size_t>(nconn));
   for (int64_t ci = 0; ci < nconn; ++ci) {
     const uint32_t dst = r.conn_dst[ci];
     if (dst >= static_cast<uint32_t>(r.n_cells)) engine_error("connection dst out of range");
@@ -599,11 +620,22 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
     }
     if (local) edges.push_back(e);
   }
+  tm.mark("connections");
   // rank order: (src_key, seq) — EventOrder (engine.cpp:25-31)
-  std::stable_sort(edges.begin(), edges.end(), [](const Edge& a, const Edge& b) {
-    if (a.src_key != b.src_key) return a.src_key < b.src_key;
-    return a.seq < b.seq;
-  });
+  // edges were generated in seq order, so a stable bucket sort by src_key
+  // (sources, key 0xFFFFFFFF, last) is the (src_key, seq) order in O(n)
+  {
+    const size_t nk = static_cast<size_t>(r.n_cells) + 1;
+    std::vector<int64_t> cnt(nk + 1, 0);
+    auto key = [&](const Edge& e) {
+      return e.src_key == 0xFFFFFFFFu ? nk - 1 : static_cast<size_t>(e.src_key);
+    };
+    for (const Edge& e : edges) ++cnt[key(e) + 1];
+    for (size_t k = 0; k < nk; ++k) cnt[k + 1] += cnt[k];
+    std::vector<Edge> sorted(edges.size());
+    for (const Edge& e : edges) sorted[cnt[key(e)]++] = e;
+    edges.swap(sorted);
+  }
   const int64_t ne = static_cast<int64_t>(edges.size());
   m.e_dst.resize(ne);
   m.e_group.resize(ne);
@@ -638,6 +670,7 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
     for (int64_t x : src_lists[s]) m.src_edges.push_back(x);
   }
 
+  tm.mark("edge sort + CSR");
   // flatten instances
   m.cgs.resize(cgs);
   int64_t ninst = 0;
@@ -654,6 +687,7 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
   m.i_stc_z.assign(ninst, 0.0);
   m.i_stc_c.assign(ninst, 0.0);
   m.i_sps_abs.assign(ninst, 0.0);
+  tm.mark("instances");
   // number of connections per (cg) for fifo sizing
   std::vector<int64_t> cg_conns(cgs, 0);
   for (const Edge& e : edges) cg_conns[m.cg_off[e.dst_local] + e.group] += 1;
@@ -698,6 +732,7 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
     }
   }
 
+  tm.mark("fifos");
   // ---- sources (generate_source_events, engine.cpp:831-873) ----
   m.sources.resize(r.n_sources);
   for (int s = 0; s < r.n_sources; ++s) {
@@ -736,6 +771,7 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
     P.out = 0;
   }
 
+  tm.mark("sources + probes");
   // ---- totals ----
   for (int c = 0; c < nl; ++c) {
     const McgKind& K = m.kinds[m.cell_kind[c]];
@@ -745,6 +781,7 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
       for (int i = 0; i < K.n; ++i)
         if (m.k_g_na[K.arr + i] != 0.0) ++m.hh_comps;
   }
+  tm.mark("totals");
   // static-charge edges: the instance's compartment and w * cf[comp] (the
   // product apply_event forms, engine.cpp:455-459), so staged delivery reads
   // one edge record instead of chasing group -> instance -> compartment
@@ -762,6 +799,7 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
       m.e_wcf[r] = m.e_weight[r] * m.k_cf[K.arr + comp];
     }
   }
+  tm.mark("edge payloads");
 }
 
 }  // namespace mcg

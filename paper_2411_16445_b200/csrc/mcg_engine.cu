@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -46,14 +47,26 @@ struct DBuf {
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  ~DBuf() {
-    if (p) cudaFree(p);
+  ~DBuf() { release(); }
+  // allocations from the device's memory pool, which keeps freed memory (its
+  // release threshold is raised at engine creation): constructing an engine
+  // does not map fresh memory.  Complete before use on any stream; freed
+  // only when the device is idle.
+  void release() {
+    if (p) {
+      cudaDeviceSynchronize();
+      cudaFreeAsync(p, 0);
+      cudaStreamSynchronize(0);
+    }
+    p = nullptr;
   }
   void alloc(size_t count) {
-    if (p) cudaFree(p);
-    p = nullptr;
+    release();
     n = count;
-    if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+    if (count) {
+      CK(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), 0));
+      CK(cudaStreamSynchronize(0));
+    }
   }
   void upload(const std::vector<T>& v, cudaStream_t st) {
     alloc(std::max<size_t>(v.size(), 1));
@@ -365,7 +378,16 @@ struct Engine {
   void init(const mcg_recipe& r, const mcg_options& opt) {
     device = opt.device;
     CK(cudaSetDevice(device));
+    {  // keep freed device memory in the pool (DBuf allocations)
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+    }
+    const auto t0 = std::chrono::steady_clock::now();
     build_model(r, opt, m);
+    const auto t1 = std::chrono::steady_clock::now();
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     CK(cudaMallocHost(&h_ctr, C_N * sizeof(unsigned long long)));
     CK(cudaMallocHost(&h_err, sizeof(int32_t)));
@@ -552,8 +574,15 @@ struct Engine {
     stats.stc_synapses = m.stc_syn;
     stats.hh_comps = m.hh_comps;
     stats.species_comps = m.species_comps;
+    const auto t2 = std::chrono::steady_clock::now();
     setup_batch_kernel();
     refresh_dev();
+    if (std::getenv("MCG_PROFILE_BUILD")) {
+      const auto t3 = std::chrono::steady_clock::now();
+      auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+      std::fprintf(stderr, "engine: build_model %.2f ms, uploads %.2f ms, batch setup %.2f ms\n",
+                   ms(t0, t1), ms(t1, t2), ms(t2, t3));
+    }
   }
 
   void alloc_inboxes() {
