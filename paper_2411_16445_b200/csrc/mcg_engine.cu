@@ -938,6 +938,7 @@ struct Engine {
   // one min-delay epoch towards t_ms (sharded epoch loop, engine.cpp:913-942):
   // expands the imported spikes, steps the epoch, exports this rank's spikes
   void run_epoch(double t_ms) {
+    invalidate_mirror();
     if (x_send == nullptr) throw Error(MCG_ERR_ENGINE, "sharded engine: exchange buffers not set");
     const int64_t target = ceil_steps(t_ms, m.dt);
     if (step >= target) return;
@@ -956,6 +957,7 @@ struct Engine {
   }
 
   void advance_to(double t_ms) {
+    invalidate_mirror();
     if (m.world > 1)
       throw Error(MCG_ERR_ENGINE, "sharded engine: drive it with mcg_shard_run_epoch + an exchange");
     const int64_t target = ceil_steps(t_ms, m.dt);
@@ -976,6 +978,7 @@ struct Engine {
   }
 
   void fast_forward_to(double t_ms, double coarse_dt_ms) {
+    invalidate_mirror();
     const double dt = m.dt;
     const int64_t per = static_cast<int64_t>(std::llround(coarse_dt_ms / dt));
     if (per < 1 || std::fabs(double(per) * dt - coarse_dt_ms) > 1e-9 * coarse_dt_ms)
@@ -1057,6 +1060,36 @@ struct Engine {
     return static_cast<int>(gid - m.gid_begin);
   }
 
+  // host mirror of the state arrays cell(gid) reads: the first
+  // read of a field after the device state changed downloads the whole array
+  // once; later reads (the other cells) are host copies.  Writes go through
+  // to the device and keep a valid mirror current.
+  std::vector<std::vector<unsigned char>> mirror = std::vector<std::vector<unsigned char>>(32);
+  std::vector<char> mirror_ok = std::vector<char>(32, 0);
+  void invalidate_mirror() { std::fill(mirror_ok.begin(), mirror_ok.end(), 0); }
+
+  template <class T>
+  void mirrored_field(int field, void* out, const DBuf<T>& b, int64_t off, int64_t count,
+                      bool write, const void* in) {
+    if (count <= 0) return;
+    if (field < 0 || field >= 32) return copy_field(out, b.p, off, count, write, in);
+    std::vector<unsigned char>& h = mirror[field];
+    if (write) {
+      copy_field(out, b.p, off, count, true, in);
+      if (mirror_ok[field]) std::memcpy(h.data() + off * sizeof(T), in, count * sizeof(T));
+      return;
+    }
+    if (!mirror_ok[field]) {
+      h.resize(b.n * sizeof(T));
+      if (b.n) {
+        CK(cudaMemcpyAsync(h.data(), b.p, b.n * sizeof(T), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+      }
+      mirror_ok[field] = 1;
+    }
+    std::memcpy(out, h.data() + off * sizeof(T), count * sizeof(T));
+  }
+
   template <class T>
   void copy_field(void* out, const T* base, int64_t off, int64_t count, bool write,
                   const void* in) {
@@ -1078,16 +1111,16 @@ struct Engine {
       if (off < 0 || count < 0 || off + count > lim) throw Error(MCG_ERR_ARGUMENT, "range out of bounds");
     };
     switch (field) {
-      case MCG_FIELD_V: comp_range(K.n); return copy_field(out, d_v.p, co + off, count, write, in);
-      case MCG_FIELD_HH_M: comp_range(K.n); return copy_field(out, d_hh_m.p, co + off, count, write, in);
-      case MCG_FIELD_HH_H: comp_range(K.n); return copy_field(out, d_hh_h.p, co + off, count, write, in);
-      case MCG_FIELD_HH_N: comp_range(K.n); return copy_field(out, d_hh_n.p, co + off, count, write, in);
+      case MCG_FIELD_V: comp_range(K.n); return mirrored_field(field, out, d_v, co + off, count, write, in);
+      case MCG_FIELD_HH_M: comp_range(K.n); return mirrored_field(field, out, d_hh_m, co + off, count, write, in);
+      case MCG_FIELD_HH_H: comp_range(K.n); return mirrored_field(field, out, d_hh_h, co + off, count, write, in);
+      case MCG_FIELD_HH_N: comp_range(K.n); return mirrored_field(field, out, d_hh_n, co + off, count, write, in);
       case MCG_FIELD_SPECIES:
         if (index < 0 || index >= K.n_species) throw Error(MCG_ERR_ARGUMENT, "species index");
         comp_range(K.n);
-        return copy_field(out, d_species.p, m.sp_off[c] + int64_t(index) * K.n + off, count, write, in);
-      case MCG_FIELD_DETECTOR_PREV_V: return copy_field(out, d_det_prev.p, c, 1, write, in);
-      case MCG_FIELD_REFRACTORY_UNTIL: return copy_field(out, d_refr.p, c, 1, write, in);
+        return mirrored_field(field, out, d_species, m.sp_off[c] + int64_t(index) * K.n + off, count, write, in);
+      case MCG_FIELD_DETECTOR_PREV_V: return mirrored_field(field, out, d_det_prev, c, 1, write, in);
+      case MCG_FIELD_REFRACTORY_UNTIL: return mirrored_field(field, out, d_refr, c, 1, write, in);
       case MCG_FIELD_DETECTOR_ARMED: {
         int32_t a = 0;
         if (write) {
@@ -1115,18 +1148,18 @@ struct Engine {
     comp_range(G.size);
     const int64_t j = G.inst + off;
     switch (field) {
-      case MCG_FIELD_SYN_COMP: return copy_field(out, d_i_comp.p, j, count, write, in);
-      case MCG_FIELD_SYN_WEIGHT: return copy_field(out, d_i_weight.p, j, count, write, in);
-      case MCG_FIELD_SYN_KERNEL: return copy_field(out, d_i_kernel.p, j, count, write, in);
-      case MCG_FIELD_STDP_A_PRE: return copy_field(out, d_i_stdp_pre.p, j, count, write, in);
-      case MCG_FIELD_STDP_A_POST: return copy_field(out, d_i_stdp_post.p, j, count, write, in);
-      case MCG_FIELD_STDP_W: return copy_field(out, d_i_stdp_w.p, j, count, write, in);
-      case MCG_FIELD_STDP_LAST: return copy_field(out, d_i_stdp_last.p, j, count, write, in);
-      case MCG_FIELD_HOMEO_W: return copy_field(out, d_i_homeo_w.p, j, count, write, in);
-      case MCG_FIELD_STC_H: return copy_field(out, d_i_stc_h.p, j, count, write, in);
-      case MCG_FIELD_STC_Z: return copy_field(out, d_i_stc_z.p, j, count, write, in);
-      case MCG_FIELD_STC_C: return copy_field(out, d_i_stc_c.p, j, count, write, in);
-      case MCG_FIELD_STC_SPS_ABS: return copy_field(out, d_i_sps_abs.p, j, count, write, in);
+      case MCG_FIELD_SYN_COMP: return mirrored_field(field, out, d_i_comp, j, count, write, in);
+      case MCG_FIELD_SYN_WEIGHT: return mirrored_field(field, out, d_i_weight, j, count, write, in);
+      case MCG_FIELD_SYN_KERNEL: return mirrored_field(field, out, d_i_kernel, j, count, write, in);
+      case MCG_FIELD_STDP_A_PRE: return mirrored_field(field, out, d_i_stdp_pre, j, count, write, in);
+      case MCG_FIELD_STDP_A_POST: return mirrored_field(field, out, d_i_stdp_post, j, count, write, in);
+      case MCG_FIELD_STDP_W: return mirrored_field(field, out, d_i_stdp_w, j, count, write, in);
+      case MCG_FIELD_STDP_LAST: return mirrored_field(field, out, d_i_stdp_last, j, count, write, in);
+      case MCG_FIELD_HOMEO_W: return mirrored_field(field, out, d_i_homeo_w, j, count, write, in);
+      case MCG_FIELD_STC_H: return mirrored_field(field, out, d_i_stc_h, j, count, write, in);
+      case MCG_FIELD_STC_Z: return mirrored_field(field, out, d_i_stc_z, j, count, write, in);
+      case MCG_FIELD_STC_C: return mirrored_field(field, out, d_i_stc_c, j, count, write, in);
+      case MCG_FIELD_STC_SPS_ABS: return mirrored_field(field, out, d_i_sps_abs, j, count, write, in);
       default: throw Error(MCG_ERR_ARGUMENT, "unknown field");
     }
   }
@@ -1262,6 +1295,7 @@ struct Engine {
 
   // Checkpoint::deserialize + Engine::restore (engine.cpp:1095-1140, 1235-1325)
   void restore(const uint8_t* bytes, size_t size) {
+    invalidate_mirror();
     if (m.world > 1) throw Error(MCG_ERR_ENGINE, "checkpoint: not supported for a sharded engine");
     const Ckpt ck = ck_deserialize(bytes, size);
     auto getf = [&](const std::string& n) -> const std::vector<double>& {
