@@ -669,19 +669,35 @@ __device__ __forceinline__ void mcg_unstage(const McgDev& D, const McgBatchArgs&
 // merged over the cell's STC groups in (step, seq) order (InternalOrder).
 // Returns false (cell delivered from global memory this epoch) if the event
 // buffer is full.
+// ascending bitonic sort of one key per lane (~0 pads), by shuffles
+__device__ __forceinline__ uint64_t mcg_warp_sort_reg(uint64_t v, int lane, int n) {
+  // stages up to the smallest power of two >= n (the pads are the largest keys)
+  for (int k = 2; k < 2 * n && k <= 32; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const uint64_t p = __shfl_xor_sync(MCG_FULL, v, j);
+      const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+      v = (lower == up) ? (v < p ? v : p) : (v < p ? p : v);
+    }
+  return v;
+}
+
+// regs: the pending list is exactly this epoch's sorted inbox, held one key
+// per lane (rkey), its first rnd keys due (the merge loop's common case)
 __device__ bool mcg_stage_events(const McgDev& D, const McgBatchArgs& A, const McgBatchSm& B,
-                                 int k, int c, int64_t s0, int64_t s1, int lane, int* ev_top) {
+                                 int k, int c, int64_t s0, int64_t s1, int lane, int* ev_top,
+                                 bool regs = false, uint64_t rkey = 0, int rnd = 0) {
   McgCellSm& X = B.cs[k];
   const McgKind& K = B.kc[k];
   const uint64_t* pend = D.pend + (int64_t(c) * 2 + X.sel) * D.pend_cap;
   const uint64_t lim = uint64_t(s1) << D.rank_bits;
-  int nd = 0;
-  for (int base = X.cur; base < X.end; base += 32) {
-    const int i = base + lane;
-    const unsigned bal = __ballot_sync(MCG_FULL, i < X.end && pend[i] < lim);
-    nd += __popc(bal);
-    if (bal != MCG_FULL) break;
-  }
+  int nd = rnd;
+  if (!regs)
+    for (int base = X.cur; base < X.end; base += 32) {
+      const int i = base + lane;
+      const unsigned bal = __ballot_sync(MCG_FULL, i < X.end && pend[i] < lim);
+      nd += __popc(bal);
+      if (bal != MCG_FULL) break;
+    }
   if (!X.staged) {  // take the queue metadata over from global memory
     __syncwarp();
     if (lane == 0) {
@@ -727,7 +743,7 @@ __device__ bool mcg_stage_events(const McgDev& D, const McgBatchArgs& A, const M
   }
   const uint64_t rank_mask = (1ull << D.rank_bits) - 1;
   for (int t = lane; t < nd; t += 32) {
-    const uint64_t key = pend[X.cur + t];
+    const uint64_t key = regs ? rkey : pend[X.cur + t];
     const int64_t r = int64_t(key & rank_mask);
     const int grp = D.e_group[r];
     const uint32_t inst = D.e_inst[r];
@@ -1265,6 +1281,30 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
     const int c = c0 + k;
     const int nin = D.inc_n[c];
     McgCellSm& X = cs[k];
+    if (X.fast && X.cur >= X.end && nin <= 32) {
+      // common case: nothing pending from earlier epochs and a small inbox,
+      // sorted in registers and staged from them (pend gets the same keys)
+      uint64_t key = ~0ull;
+      int nd = 0;
+      if (nin > 0) {
+        const uint64_t* in = D.inc + int64_t(c) * D.inc_cap;
+        key = mcg_warp_sort_reg(lane < nin ? in[lane] : ~0ull, lane, nin);
+        const uint64_t lim = uint64_t(s1) << D.rank_bits;
+        nd = __popc(__ballot_sync(MCG_FULL, lane < nin && key < lim));
+        uint64_t* out = D.pend + (int64_t(c) * 2 + (1 - X.sel)) * D.pend_cap;
+        if (lane < nin) out[lane] = key;
+        __syncwarp();
+        if (lane == 0) {
+          X.end = nin;
+          X.cur = 0;
+          X.sel = 1 - X.sel;
+        }
+        __syncwarp();
+      }
+      mcg_stage_events(D, A, B, k, c, s0, s1, lane, &s_ev_top, true, key, nd);
+      if (lane == 0) X.nsp = 0;
+      continue;
+    }
     if (nin > 0) {
       uint64_t* in = D.inc + int64_t(c) * D.inc_cap;
       if (nin > 1) mcg_warp_sort(in, nin, lane);
