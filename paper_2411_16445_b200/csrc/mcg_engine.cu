@@ -191,6 +191,7 @@ struct Engine {
   int32_t bc_stride = 0;  // doubles per staged cell's compartment block
   int32_t bc_nch_max = 0;  // chain-sweep lane descriptors per batch
   int32_t bc_lean = 0;
+  int bc_carve = 100;  // shared-memory carveout (percent) this engine's batch kernel needs
   int32_t bc_kind_doubles = 0, bc_specs_sm = 0, bc_stc_sm = 0;
   size_t bc_smem = 0;
   DBuf<int4> d_chunks;
@@ -357,7 +358,8 @@ struct Engine {
     CK(cudaFuncSetAttribute(k_batch, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(bc_smem)));
     // leave the rest of the unified L1/shared array to L1 (STC state streams through it)
-    const int carve = std::min(100, static_cast<int>((bc_smem * 100 + 228 * 1024 - 1) / (228 * 1024)) + 5);
+    bc_carve = std::min(100, static_cast<int>((bc_smem * 100 + 228 * 1024 - 1) / (228 * 1024)) + 5);
+    const int carve = bc_carve;
     CK(cudaFuncSetAttribute(k_batch, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_batch, kBatchThreads, bc_smem));
@@ -856,6 +858,11 @@ struct Engine {
     int64_t max_len = L;
     void* args[] = {&Dv, &A, &max_len};
     CK(cudaEventRecord(evk0, st));
+    // the kernel attributes are process-global and another engine in this
+    // process (a shard, a second network) may have set its own: restate ours
+    CK(cudaFuncSetAttribute(k_batch, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(bc_smem)));
+    CK(cudaFuncSetAttribute(k_batch, cudaFuncAttributePreferredSharedMemoryCarveout, bc_carve));
     CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_batch), bc_grid, kBatchThreads, args,
                                    bc_smem, st));
     CK(cudaEventRecord(evk1, st));
@@ -1036,6 +1043,8 @@ struct Engine {
     if (nl > 0) {
       McgDev dff = dev;
       dff.kinds = d_kinds_ff.p;
+      CK(cudaFuncSetAttribute(k_ff, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(smem_bytes)));
       k_ff<<<(nl * 32 + kBlock - 1) / kBlock, kBlock, smem_bytes, st>>>(
           dff, d_fh.p, d_cap_ff.p, d_f_ff.p, d_d_ff.p, dtc, n_coarse);
       stats.kernel_launches += 1;

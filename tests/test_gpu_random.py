@@ -158,3 +158,25 @@ def test_random_recipe_bitwise(gpu, seed):
         a, b = r.trace_arrays(p), g.trace_arrays(p)
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]), f"probe {p}"
     assert g.make_checkpoint().data == r.make_checkpoint()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_recipe_sharded(gpu, seed):
+    """The same random recipes cut into 2 or 3 shards (the allgather done in
+    process): merged spikes and every cell's voltage equal the single engine's."""
+    from paper_2411_16445_b200 import shard
+    rec = _recipe(seed)
+    dt = [0.5, 0.25, 0.1, 0.5][seed % 4]
+    flat = rec.flatten()
+    opt = EngineOptions(dt, 100 + seed)
+    single = Engine(flat, opt)
+    single.advance_to(120.0)
+    t1, g1 = single.spike_arrays()
+    world = 2 + seed % 2
+    t2, g2, engines = shard.run_shards_in_process(flat.view, opt, world, 120.0)
+    np.testing.assert_array_equal(g1, g2)
+    np.testing.assert_array_equal(t1.view(np.int64), t2.view(np.int64))
+    b = shard.partition(flat.view, world)
+    for r, e in enumerate(engines):
+        for gid in range(int(b[r]), int(b[r + 1])):
+            np.testing.assert_array_equal(single.cell(gid).v_mV, e.cell(gid).v_mV)
