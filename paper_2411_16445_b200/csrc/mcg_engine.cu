@@ -89,15 +89,24 @@ enum { C_EP_SPK = 0, C_LOG = 1, C_DELIVERED = 2, C_N = 4 };
 
 // anything still undelivered: queued keys, unexpanded spikes with local
 // fan-out, or delayed calcium (the fast-forward guard, engine.cpp:958-960)
+// fast-forward guard (engine.cpp:958-960): which cells hold undelivered
+// events -- pending or incoming inbox entries, queued delayed calcium, or
+// events the last epoch's spikes will deliver (expanded at the next epoch's
+// entry here, already in the targets' inboxes in the reference)
 __global__ void k_pending(McgDev D, const int64_t* out_begin, const int64_t* out_end,
-                          int32_t n_fifos, int32_t* flag) {
+                          const int32_t* e_dst, int32_t* cell_flag) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < D.n_cells && (D.pend_n[i] > D.pend_off[i] || D.inc_n[i] > 0)) atomicOr(flag, 1);
-  if (i < n_fifos && D.fifos[i].head < D.fifos[i].tail) atomicOr(flag, 1);
-  // spikes of the last epoch are expanded at the next epoch's entry
-  if (i < D.n_cells && D.sp_count[i] > 0) {
+  if (i >= D.n_cells) return;
+  bool p = D.pend_n[i] > D.pend_off[i] || D.inc_n[i] > 0;
+  const McgKind& K = D.kinds[D.cell_kind[i]];
+  for (int gi = 0; gi < K.n_groups; ++gi) {
+    const int32_t f = D.cgs[D.cg_off[i] + gi].fifo;
+    if (f >= 0 && D.fifos[f].head < D.fifos[f].tail) p = true;
+  }
+  if (p) cell_flag[i] = 1;
+  if (D.sp_count[i] > 0) {
     const uint32_t g = D.gid0 + uint32_t(i);
-    if (out_end[g] > out_begin[g]) atomicOr(flag, 1);
+    for (int64_t r = out_begin[g]; r < out_end[g]; ++r) cell_flag[e_dst[r]] = 1;
   }
 }
 
@@ -996,20 +1005,33 @@ struct Engine {
     const int nl = n_local();
     const int nf = static_cast<int>(m.fifos.size());
     refresh_dev();
+    (void)nf;
     DBuf<int32_t> flag;
-    flag.alloc(1);
+    flag.alloc(std::max(nl, 1));
     flag.zero(st);
-    const int64_t span = std::max<int64_t>({int64_t(nl), int64_t(nf), int64_t(nl) * sp_cap, 1});
-    k_pending<<<static_cast<unsigned>((span + 255) / 256), 256, 0, st>>>(
-        dev, d_out_begin.p, d_out_end.p, nf, flag.p);
-    int32_t pending = 0;
-    CK(cudaMemcpyAsync(&pending, flag.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    if (nl > 0)
+      k_pending<<<static_cast<unsigned>((nl + 255) / 256), 256, 0, st>>>(
+          dev, d_out_begin.p, d_out_end.p, d_e_dst.p, flag.p);
+    std::vector<int32_t> hflag(std::max(nl, 1), 0);
+    CK(cudaMemcpyAsync(hflag.data(), flag.p, hflag.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (pending) throw Error(MCG_ERR_ENGINE, "fast-forward: pending undelivered spikes");
-    const int64_t ncg = static_cast<int64_t>(m.cgs.size());
+    int first = nl;
+    for (int c = 0; c < nl; ++c)
+      if (hflag[c]) {
+        first = c;
+        break;
+      }
+    // the reference resets each cell's calcium, STDP traces and kernels as it
+    // walks the cells and throws at the first one with undelivered events:
+    // the cells before it are reset (engine.cpp:958-969)
+    const int64_t ncg = first < nl ? m.cg_off[first] : static_cast<int64_t>(m.cgs.size());
     if (ncg > 0) {
       k_ff_reset<<<static_cast<unsigned>((ncg + 127) / 128), 128, 0, st>>>(dev, ncg);
       stats.kernel_launches += 1;
+    }
+    if (first < nl) {
+      CK(cudaStreamSynchronize(st));
+      throw Error(MCG_ERR_ENGINE, "fast-forward: pending undelivered spikes");
     }
     const int64_t n_coarse = (target - step) / per;
     if (n_coarse <= 0) return;

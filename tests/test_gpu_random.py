@@ -180,3 +180,40 @@ def test_random_recipe_sharded(gpu, seed):
     for r, e in enumerate(engines):
         for gid in range(int(b[r]), int(b[r + 1])):
             np.testing.assert_array_equal(single.cell(gid).v_mV, e.cell(gid).v_mV)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_recipe_fast_forward(gpu, seed):
+    """fast_forward_to on the random recipes (engine.cpp:947-1034): both engines
+    either fast-forward to identical state or reject the span with the same
+    message (pending deliveries, spans that are not multiples of coarse dt)."""
+    rec = _recipe(seed)
+    dt = [0.5, 0.25, 0.1, 0.5][seed % 4]
+    flat = rec.flatten()
+    r = ref.RefEngine(flat.view, dt, 100 + seed, 1)
+    g = Engine(flat, EngineOptions(dt, 100 + seed))
+    for e in (r, g):
+        e.advance_to(200.0)
+    for t_ff, coarse in ((200.0 + 600 * 50.0, 50.0), (200.0 + 7.3, 5.0)):
+        er = eg = None
+        try:
+            r.fast_forward_to(t_ff, coarse)
+        except Exception as e:  # noqa: BLE001
+            er = str(e)
+        try:
+            g.fast_forward_to(t_ff, coarse)
+        except Exception as e:  # noqa: BLE001
+            eg = str(e)
+        assert er == eg
+    for gid in range(len(rec.cell_kind)):
+        np.testing.assert_array_equal(r.read("v", gid), g.cell(gid).v_mV)
+        for gi in range(r.ngroups(gid)):
+            if r.group_size(gid, gi) == 0:
+                continue
+            for f in ("stc_h", "stc_z", "stc_c"):
+                try:
+                    a = r.read(f, gid, gi)
+                except Exception:  # noqa: BLE001
+                    continue
+                np.testing.assert_array_equal(a, g.cell(gid).groups[gi]._read(f, np.float64))
+    assert g.make_checkpoint().data == r.make_checkpoint()
