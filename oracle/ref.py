@@ -102,6 +102,7 @@ def lib():
             "ref_stdp_window": (C.c_double, [P(A.mcg_stdp_params), C.c_double, C.c_int,
                                              C.c_double]),
             "ref_make_checkpoint": (C.c_int, [vp, vp, C.c_int64, P(C.c_int64)]),
+            "ref_write_v": (C.c_int, [vp, C.c_uint32, vp, C.c_int64]),
             "ref_restore": (C.c_int, [vp, vp, C.c_int64]),
         }
         for name, (res, args) in sig.items():
@@ -212,6 +213,10 @@ class RefEngine:
 
     def clear_spikes(self):
         lib().ref_clear_spikes(self._h)
+
+    def write_v(self, gid, values):
+        a = np.ascontiguousarray(values, np.float64)
+        _chk(lib().ref_write_v(self._h, gid, a.ctypes.data, a.size))
 
     def make_checkpoint(self) -> bytes:
         n = C.c_int64()

@@ -742,4 +742,13 @@ int ref_restore(ref_engine* e, const uint8_t* buf, int64_t size) {
   });
 }
 
+// direct writes of cell(gid).v_mV (the tests mutate the reference's CellRT)
+int ref_write_v(ref_engine* e, uint32_t gid, const double* v, int64_t n) {
+  return guard([&] {
+    auto& c = e->eng->cell(gid);
+    if (static_cast<int64_t>(c.v_mV.size()) != n) throw EngineError("write_v: size mismatch");
+    for (int64_t i = 0; i < n; ++i) c.v_mV[i] = v[i];
+  });
+}
+
 }  // extern "C"

@@ -217,3 +217,40 @@ def test_random_recipe_fast_forward(gpu, seed):
                     continue
                 np.testing.assert_array_equal(a, g.cell(gid).groups[gi]._read(f, np.float64))
     assert g.make_checkpoint().data == r.make_checkpoint()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_recipe_writes_and_restore(gpu, seed):
+    """Mid-run writes of cell(gid).v_mV through the API, then a checkpoint of the
+    B200 engine restored into a fresh one: both continuations equal the
+    reference's."""
+    rec = _recipe(seed)
+    dt = [0.5, 0.25, 0.1, 0.5][seed % 4]
+    flat = rec.flatten()
+    r = ref.RefEngine(flat.view, dt, 100 + seed, 1)
+    g = Engine(flat, EngineOptions(dt, 100 + seed))
+    for e in (r, g):
+        e.advance_to(60.0)
+    rng = np.random.default_rng(seed)
+    for gid in rng.integers(0, len(rec.cell_kind), 3):
+        v = r.read("v", int(gid))
+        if v.size == 0:
+            continue
+        v = v + rng.uniform(-3, 8, v.size)
+        r.write_v(int(gid), v)
+        g.cell(int(gid)).set_v(v)
+    ck = g.make_checkpoint()
+    assert ck.data == r.make_checkpoint()
+    g2 = Engine(flat, EngineOptions(dt, 100 + seed))
+    g2.restore(ck)
+    for e in (r, g, g2):
+        e.advance_to(150.0)
+    rt, rg = r.spike_arrays()
+    for e in (g, g2):
+        t, i = e.spike_arrays()
+        tail = rt > 60.0 if e is g2 else np.ones(len(rt), bool)
+        assert np.array_equal(t, rt[tail]) and np.array_equal(i, rg[tail])
+    for gid in range(len(rec.cell_kind)):
+        np.testing.assert_array_equal(r.read("v", gid), g.cell(gid).v_mV)
+        np.testing.assert_array_equal(r.read("v", gid), g2.cell(gid).v_mV)
+    assert g2.make_checkpoint().data == r.make_checkpoint()
