@@ -59,11 +59,11 @@ def _kind(rng, which):
     return k
 
 
-def _recipe(seed):
+def _recipe(seed, n=None):
     rng = np.random.default_rng(seed)
     which = ["exact", "cable", "hh"]
     kinds = [_kind(rng, w) for w in rng.choice(which, size=int(rng.integers(1, 4)))]
-    n = int(rng.integers(6, 20))
+    n = int(rng.integers(6, 20)) if n is None else n
     cell_kind = [int(x) for x in rng.integers(0, len(kinds), n)]
     srcs = [PoissonSource([PoissonWindow(0.0, 150.0, float(rng.uniform(20, 200)))]),
             RegularSource(float(rng.uniform(0, 5)), float(rng.uniform(3, 9)), 20),
@@ -254,3 +254,25 @@ def test_random_recipe_writes_and_restore(gpu, seed):
         np.testing.assert_array_equal(r.read("v", gid), g.cell(gid).v_mV)
         np.testing.assert_array_equal(r.read("v", gid), g2.cell(gid).v_mV)
     assert g2.make_checkpoint().data == r.make_checkpoint()
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_recipe_large_mixed(gpu, monkeypatch, seed):
+    """Larger random networks (several mixed-kind cells per CTA); odd seeds in
+    the non-resident batch mode (MCG_MAX_CELLS_PER_CTA)."""
+    rec = _recipe(1000 + seed, n=260)
+    dt = [0.5, 0.25][seed % 2]
+    flat = rec.flatten()
+    r = ref.RefEngine(flat.view, dt, 7 + seed, 1)
+    if seed % 2:
+        monkeypatch.setenv("MCG_MAX_CELLS_PER_CTA", "1")
+    g = Engine(flat, EngineOptions(dt, 7 + seed))
+    monkeypatch.delenv("MCG_MAX_CELLS_PER_CTA", raising=False)
+    for t in (55.0, 130.0):
+        r.advance_to(t)
+        g.advance_to(t)
+    rt, rg = r.spike_arrays()
+    gt, gg = g.spike_arrays()
+    assert len(rt) > 0
+    assert np.array_equal(rt, gt) and np.array_equal(rg, gg)
+    assert g.make_checkpoint().data == r.make_checkpoint()
