@@ -32,7 +32,8 @@ def test_library_loads_and_exports_every_declared_symbol():
 def test_struct_layouts(tmp_path):
     structs = ["mcg_lif", "mcg_hh", "mcg_species", "mcg_stdp_params", "mcg_homeo_params",
                "mcg_stc_params", "mcg_syn_spec", "mcg_placement", "mcg_kind", "mcg_source",
-               "mcg_recipe", "mcg_options", "mcg_stats"]
+               "mcg_recipe", "mcg_options", "mcg_stats", "mcg_gb_params", "mcg_gb_protocol",
+               "mcg_gb_point"]
     prog = tmp_path / "sz.c"
     prog.write_text('#include <stdio.h>\n#include "mcg.h"\nint main(){\n' + "".join(
         f'printf("%zu\\n", sizeof({s}));\n' for s in structs) + "}\n")
