@@ -59,3 +59,20 @@ def test_busyring_default(gpu):
     r, g = _run(rr.view, 0.025, 0, [("advance", 200.0)])
     n = assert_spikes_equal(r, g)
     assert n == 9984
+
+
+def test_config3_8h_protocol(gpu):
+    """The flagship experiment at full size (N=2000 MC, seed 1): learning at
+    10 s, detailed to 13 s, fast-forward across 8 h in coarse steps, recall
+    (network.cpp:600-639). Spike trains through recall, every excitatory
+    cell's STC state and probes of V are bitwise the reference's."""
+    c = N.ConsolidationConfig(n_cells=2000, n_exc=1600, seed=1, multi_compartment=True)
+    rr = ref.RefRecipe.consolidation(ref_cfg(c), True)
+    t_recall = c.t_learn_ms + 8 * 3600e3
+    t_ff0 = c.t_learn_ms + 3000.0
+    t_ff1 = t_ff0 + np.floor((t_recall - 1000.0 - t_ff0) / c.coarse_dt_ms) * c.coarse_dt_ms
+    sched = [("advance", t_ff0), ("ff", t_ff1, c.coarse_dt_ms), ("advance", t_recall + 500.0)]
+    r, g = _run(rr.view, c.dt_ms, 1, sched)
+    assert assert_spikes_equal(r, g) > 0
+    assert_cells_equal(r, g, range(0, 1600), fields=(), group_fields=STC)
+    assert_cells_equal(r, g, range(0, 2000, 11), fields=("v",))
