@@ -1040,7 +1040,8 @@ struct Engine {
     for (size_t i = 0; i < m.specs.size(); ++i) fh[i] = std::exp(-0.1 * dtc / m.specs[i].tau_h);
     // species systems at the coarse step: cap = vol/dtc (engine.cpp:1019-1025),
     // eliminated once with solve_tree's operation order
-    std::vector<double> cap_ff(m.k_sp_cap_dt.size()), f_ff(cap_ff.size()), d_ff(cap_ff.size());
+    std::vector<double> cap_ff(m.k_sp_cap_dt.size()), f_ff(cap_ff.size()), d_ff(cap_ff.size()),
+        r_ff(cap_ff.size(), 0.0);
     std::vector<McgKind> kinds_ff = m.kinds;
     for (size_t k = 0; k < m.kinds.size(); ++k) {
       McgKind& K = kinds_ff[k];
@@ -1051,24 +1052,34 @@ struct Engine {
                                            m.k_sp_gs.data() + o, m.k_sp_coupling.data() + o,
                                            f_ff.data() + o, d_ff.data() + o))
           K.sp_const = 0;
+        for (int i = 0; i < K.n; ++i) r_ff[o + i] = mcg_recip(d_ff[o + i]);
       }
     }
-    DBuf<double> d_fh, d_cap_ff, d_f_ff, d_d_ff;
+    DBuf<double> d_fh, d_cap_ff, d_f_ff, d_d_ff, d_r_ff;
     DBuf<McgKind> d_kinds_ff;
     d_fh.upload(fh, st);
     d_cap_ff.upload(cap_ff, st);
     d_f_ff.upload(f_ff, st);
     d_d_ff.upload(d_ff, st);
+    d_r_ff.upload(r_ff, st);
     d_kinds_ff.upload(kinds_ff, st);
     probes_begin(step, target, true, n_coarse);
     refresh_dev();
     if (nl > 0) {
       McgDev dff = dev;
       dff.kinds = d_kinds_ff.p;
+      // register-resident cells, then the rest (mcg_ff_fast_of splits them)
+      const size_t ff_smem = (smem_bytes / (kBlock / 32) + sizeof(double) * MCG_FF_SCR) *
+                             (MCG_FF_BLOCK / 32);
+      CK(cudaFuncSetAttribute(k_ff_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(ff_smem)));
+      k_ff_fast<<<(nl * 32 + MCG_FF_BLOCK - 1) / MCG_FF_BLOCK, MCG_FF_BLOCK, ff_smem, st>>>(
+          dff, d_fh.p, d_cap_ff.p, d_f_ff.p, d_d_ff.p, d_r_ff.p, dtc, n_coarse);
       CK(cudaFuncSetAttribute(k_ff, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               static_cast<int>(smem_bytes)));
       k_ff<<<(nl * 32 + kBlock - 1) / kBlock, kBlock, smem_bytes, st>>>(
-          dff, d_fh.p, d_cap_ff.p, d_f_ff.p, d_d_ff.p, dtc, n_coarse);
+          dff, d_fh.p, d_cap_ff.p, d_f_ff.p, d_d_ff.p, d_r_ff.p, dtc, n_coarse);
+      stats.kernel_launches += 1;
       stats.kernel_launches += 1;
     }
     const int64_t a = step;
