@@ -374,40 +374,51 @@ __device__ __forceinline__ void mcg_ff_solve_lanes(const McgKind& K, const McgFf
 #pragma unroll
     for (int sp = 0; sp < MCG_FF_SPMAX; ++sp) pr[sp] = L.f[sp] * r[sp];
     const bool gather = L.depth == l - 1;
+    // pull k happens only where a parent has more than k children (more[k-1]),
+    // which implies every earlier pull: one branch per level in the common case
 #pragma unroll
     for (int k = 0; k < MCG_FF_MAXCH; ++k) {
-      if (k == 0 || ((L.more[k > 0 ? k - 1 : 0] >> l) & 1u)) {
-        const bool take = gather && k < L.nch;
+      if (k > 0 && !((L.more[k > 0 ? k - 1 : 0] >> l) & 1u)) break;
+      const bool take = gather && k < L.nch;
 #pragma unroll
-        for (int sp = 0; sp < MCG_FF_SPMAX; ++sp) {
-          const double v = __shfl_sync(MCG_FULL, pr[sp], L.ch[k]);
-          const double t = r[sp] + v;
-          r[sp] = take ? t : r[sp];
-        }
+      for (int sp = 0; sp < MCG_FF_SPMAX; ++sp) {
+        const double v = __shfl_sync(MCG_FULL, pr[sp], L.ch[k]);
+        const double t = r[sp] + v;
+        r[sp] = take ? t : r[sp];
       }
     }
   }
-  // substitution, root down
+  // substitution, root down; operands outside the reciprocal division's proven
+  // range (never seen in practice) send the whole sweep through mcg_div again
+  bool bad = false;
 #pragma unroll
-  for (int sp = 0; sp < MCG_FF_SPMAX; ++sp)
-    if (lane == 0) x[sp] = mcg_div(r[sp], L.d[sp], L.rd[sp]);
+  for (int sp = 0; sp < MCG_FF_SPMAX; ++sp) {
+    bool b;
+    const double q = mcg_div_nb(r[sp], L.d[sp], L.rd[sp], b);
+    if (lane == 0) x[sp] = q;
+    bad |= lane == 0 && b;
+  }
   for (int l = 1; l <= max_depth; ++l) {
     const bool sel = L.depth == l;
-    double t[MCG_FF_SPMAX];
-    bool bad = false;
 #pragma unroll
     for (int sp = 0; sp < MCG_FF_SPMAX; ++sp) {
       const double xp = __shfl_sync(MCG_FULL, x[sp], L.par);
-      t[sp] = r[sp] + L.coup[sp] * xp;
       bool b;
-      const double q = mcg_div_nb(t[sp], L.d[sp], L.rd[sp], b);
+      const double q = mcg_div_nb(r[sp] + L.coup[sp] * xp, L.d[sp], L.rd[sp], b);
       x[sp] = sel ? q : x[sp];
-      bad |= b;
+      bad |= sel && b;
     }
-    if (__any_sync(MCG_FULL, sel && bad)) {
-      if (sel)
+  }
+  if (__any_sync(MCG_FULL, bad)) {
 #pragma unroll
-        for (int sp = 0; sp < MCG_FF_SPMAX; ++sp) x[sp] = mcg_div(t[sp], L.d[sp], L.rd[sp]);
+    for (int sp = 0; sp < MCG_FF_SPMAX; ++sp)
+      if (lane == 0) x[sp] = mcg_div(r[sp], L.d[sp], L.rd[sp]);
+    for (int l = 1; l <= max_depth; ++l) {
+#pragma unroll
+      for (int sp = 0; sp < MCG_FF_SPMAX; ++sp) {
+        const double xp = __shfl_sync(MCG_FULL, x[sp], L.par);
+        if (L.depth == l) x[sp] = mcg_div(r[sp] + L.coup[sp] * xp, L.d[sp], L.rd[sp]);
+      }
     }
   }
 #pragma unroll
