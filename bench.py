@@ -246,6 +246,30 @@ def other_configs():
                                          "sim_s_per_wall_s": 2.0 / sec,
                                          "us_per_fine_step": 1e6 * sec / steps}
     e.close()
+    # the whole 8 h experiment on config 3 (network.cpp:600-639): detailed to 13 s,
+    # fast-forward across 8 h in 1 s coarse steps, recall; wall clock per phase
+    c = N.ConsolidationConfig(n_cells=2000, n_exc=1600, seed=SEED, multi_compartment=True,
+                              dt_ms=DT_MS)
+    b = N.build_consolidation_network(c, True)
+    e = Engine(b.recipe, EngineOptions(DT_MS, SEED))
+    t_recall = c.t_learn_ms + 8 * 3600e3
+    t_ff0 = c.t_learn_ms + 3000.0
+    t_ff1 = t_ff0 + math.floor((t_recall - 1000.0 - t_ff0) / c.coarse_dt_ms) * c.coarse_dt_ms
+    ts = [_t.perf_counter()]
+    e.advance_to(t_ff0)
+    ts.append(_t.perf_counter())
+    e.fast_forward_to(t_ff1, c.coarse_dt_ms)
+    ts.append(_t.perf_counter())
+    e.advance_to(t_recall + 500.0)
+    ts.append(_t.perf_counter())
+    n_coarse = int(round((t_ff1 - t_ff0) / c.coarse_dt_ms))
+    out["config3_8h_protocol"] = {"detailed_0_13s_s": ts[1] - ts[0], "fast_forward_s": ts[2] - ts[1],
+                                  "recall_s": ts[3] - ts[2], "total_s": ts[3] - ts[0],
+                                  "coarse_steps": n_coarse,
+                                  "us_per_coarse_step": 1e6 * (ts[2] - ts[1]) / n_coarse,
+                                  "spikes": int(len(e.spike_arrays()[0]))}
+    e.close()
+    del b
     p = PR.GbParams()
     deltas = [-100.0, -50.0, -30.0, -20.0, -10.0, -5.0, 0.0, 5.0, 10.0, 20.0, 30.0, 50.0, 100.0]
     proto = PR.GbPairingProtocol(dt_ms=0.05, trials=4000, seed=999)
