@@ -373,9 +373,13 @@ struct Engine {
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_batch, kBatchThreads, bc_smem));
     if (occ < 1) throw Error(MCG_ERR_CUDA, "batch kernel does not fit on an SM");
-    // at least one CTA per SM: the CTAs without a batch still expand source
-    // events and spikes (a single neuron with 1000 Poisson inputs)
-    bc_grid = std::min(bc_batches < dev_sms / 2 ? dev_sms : bc_batches, occ * dev_sms);
+    // few batches but many sources: widen towards one CTA per SM, since the
+    // CTAs without a batch still expand source events (a single neuron with
+    // 1000 Poisson inputs); with few sources every extra CTA only adds to the
+    // grid barriers (one synapse on one neuron: config 1)
+    const int64_t want = std::min<int64_t>(dev_sms, (static_cast<int64_t>(m.sources.size()) + 3) / 4);
+    bc_grid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(bc_batches, want),
+                                                 int64_t(occ) * dev_sms));
     if (bc_stc_sm && bc_grid < bc_batches) throw Error(MCG_ERR_CUDA, "batch kernel: not resident");
     d_chunks.alloc(size_t(kBatch) * bc_batches + 1);
     d_chunk_n.alloc(1);

@@ -35,7 +35,12 @@ ne = n * 4 // 5
 dend = N.DendriteSize.large_dendrites if os.environ.get("PROBE_DEND") == "large" else N.DendriteSize.small_dendrites
 c = N.ConsolidationConfig(n_cells=n, n_exc=ne, p_conn=min(0.1, 0.1 * 1600 / ne), seed=1,
                           multi_compartment=True, dend_size=dend)
-if os.environ.get("PROBE_CFG") == "config2":
+if os.environ.get("PROBE_CFG") == "config1":
+    cfg = N.StcSingleConfig()
+    times = N.stc_protocol_times(N.StcProtocol.stet, cfg.t_onset_ms)
+    rec = N.build_stc_single(cfg, times)
+    e = Engine(rec.flatten() if hasattr(rec, "flatten") else rec, EngineOptions(cfg.dt_ms, 1))
+elif os.environ.get("PROBE_CFG") == "config2":
     rec = N.build_single_neuron_plastic(n_inputs=1000, rate_hz=5.0, duration_ms=3000.0, dt_ms=0.1)
     e = Engine(rec.flatten(), EngineOptions(0.1, 1))
 else:
