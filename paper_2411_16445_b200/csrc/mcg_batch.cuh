@@ -76,9 +76,17 @@ __device__ void mcg_expand(const McgEv& E, const McgDev& D, int32_t j, int64_t s
   const int64_t gw = int64_t(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
   const int64_t ntask = int64_t(E.n_tasks) * max_len;
   for (int64_t t = gw; t < ntask; t += nw) {
-    const int64_t off = t % max_len;
+    int64_t q, off;
+    if (((static_cast<uint64_t>(t) | static_cast<uint64_t>(max_len)) >> 32) == 0) {
+      const uint32_t q32 = static_cast<uint32_t>(t) / static_cast<uint32_t>(max_len);
+      q = q32;
+      off = static_cast<uint32_t>(t) - q32 * static_cast<uint32_t>(max_len);
+    } else {
+      q = t / max_len;
+      off = t - q * max_len;
+    }
     if (off >= len) continue;
-    const McgSrcTask T = E.tasks[t / max_len];
+    const McgSrcTask T = E.tasks[q];
     const int64_t e0 = E.src_edge_off[T.source], e1 = E.src_edge_off[T.source + 1];
     if (e1 == e0) continue;
     if (T.type == MCG_SRC_POISSON) {
@@ -520,7 +528,7 @@ __device__ __forceinline__ int64_t mcg_fifo_next(const McgDev& D, const McgKind&
     if (G.fifo < 0) continue;
     const McgFifo& F = D.fifos[G.fifo];
     if (F.head < F.tail) {
-      const int64_t st = D.fifo_step[F.base + (F.head % F.cap)];
+      const int64_t st = D.fifo_step[F.base + mcg_mod(F.head, F.cap)];
       if (st < nx) nx = st;
     }
   }
@@ -719,7 +727,7 @@ __device__ bool mcg_stage_events(const McgDev& D, const McgBatchArgs& A, const M
     int nq = 0;
     for (int64_t base = g.f_head; base < g.f_tail; base += 32) {
       const int64_t i = base + lane;
-      const bool due = i < g.f_tail && D.fifo_step[g.f_base + (i % g.f_cap)] < s1;
+      const bool due = i < g.f_tail && D.fifo_step[g.f_base + mcg_mod(i, g.f_cap)] < s1;
       const unsigned bal = __ballot_sync(MCG_FULL, due);
       nq += __popc(bal);
       if (bal != MCG_FULL) break;
@@ -771,7 +779,7 @@ __device__ bool mcg_stage_events(const McgDev& D, const McgBatchArgs& A, const M
       int nq = 0;
       for (int64_t base = g.f_head; base < g.f_tail; base += 32) {
         const int64_t i = base + lane;
-        const int64_t slot = g.f_base + (i % g.f_cap);
+        const int64_t slot = g.f_base + mcg_mod(i, g.f_cap);
         const bool due = i < g.f_tail && D.fifo_step[slot] < s1;
         const unsigned bal = __ballot_sync(MCG_FULL, due);
         if (due) {
@@ -802,7 +810,7 @@ __device__ bool mcg_stage_events(const McgDev& D, const McgBatchArgs& A, const M
       for (int q = 0; q < X.n_stc_seg; ++q) {
         const McgSegSm& g = B.seg[k * A.n_stc_max + q];
         if (g.fifo < 0 || g.f_head >= g.f_tail) continue;
-        const int64_t slot = g.f_base + (g.f_head % g.f_cap);
+        const int64_t slot = g.f_base + mcg_mod(g.f_head, g.f_cap);
         const int64_t st = D.fifo_step[slot];
         if (st >= s1) continue;
         const uint64_t seq = D.fifo_si[slot] >> 32;
@@ -814,7 +822,7 @@ __device__ bool mcg_stage_events(const McgDev& D, const McgBatchArgs& A, const M
       }
       if (best < 0) break;
       McgSegSm& g = B.seg[k * A.n_stc_max + best];
-      const int64_t slot = g.f_base + (g.f_head % g.f_cap);
+      const int64_t slot = g.f_base + mcg_mod(g.f_head, g.f_cap);
       McgEvSm e;
       e.w = 0.0;
       e.inst = uint32_t(D.fifo_si[slot] & 0xffffffffu);
@@ -1397,7 +1405,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
             if (g.f_tail - g.f_head >= g.f_cap) {
               atomicOr(D.err, MCG_ERR_FLAG_FIFO);
             } else {
-              const int64_t slot = g.f_base + (g.f_tail % g.f_cap);
+              const int64_t slot = g.f_base + mcg_mod(g.f_tail, g.f_cap);
               D.fifo_step[slot] = s + g.ca_delay;
               D.fifo_si[slot] = (uint64_t(X.iseq) << 32) | uint64_t(inst);
               D.fifo_src[slot] = E.src;
@@ -1458,7 +1466,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
               if (G.fifo < 0) continue;
               const McgFifo& F = D.fifos[G.fifo];
               if (F.head < F.tail) {
-                const int64_t slot = F.base + (F.head % F.cap);
+                const int64_t slot = F.base + mcg_mod(F.head, F.cap);
                 if (D.fifo_step[slot] <= s) {
                   const uint64_t seq = D.fifo_si[slot] >> 32;
                   if (seq < bseq) {
@@ -1470,7 +1478,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
             }
             if (best < 0) break;
             McgFifo& F = D.fifos[D.cgs[cg0 + best].fifo];
-            const uint64_t si = D.fifo_si[F.base + (F.head % F.cap)];
+            const uint64_t si = D.fifo_si[F.base + mcg_mod(F.head, F.cap)];
             ++F.head;
             mcg_apply_event(D, K, c, cg0, V, best, uint32_t(si & 0xffffffffu), 0.0, 1,
                             refractory, s, mcg_stc_ref(A, B, tid, best));
@@ -1805,7 +1813,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
       for (int q = X.p0; q < X.p1; ++q) {
         const int p = D.probe_idx[q];
         const McgProbe& Pr = D.probes[p];
-        if ((s + 1) % Pr.every != 0) continue;
+        if (mcg_mod(s + 1, Pr.every) != 0) continue;
         const int64_t m0 = (D.ctl[3] + Pr.every) / Pr.every;
         const double* SP = in_sm ? V + m : D.species + D.sp_off[c];
         D.trace_buf[D.trace_base[p] + ((s + 1) / Pr.every - m0)] =

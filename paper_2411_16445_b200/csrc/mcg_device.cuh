@@ -127,6 +127,15 @@ __device__ __forceinline__ double mcg_div(double x, double d, double y) {
   return res;
 }
 
+// a % b for a >= 0, b > 0: the 32-bit unsigned remainder when both fit (a
+// short sequence instead of the 64-bit division routine; the queue counters
+// and step numbers of any realistic run stay below 2^32)
+__device__ __forceinline__ int64_t mcg_mod(int64_t a, int64_t b) {
+  if (((static_cast<uint64_t>(a) | static_cast<uint64_t>(b)) >> 32) == 0)
+    return static_cast<uint32_t>(a) % static_cast<uint32_t>(b);
+  return a % b;
+}
+
 __device__ __forceinline__ unsigned mcg_lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -217,7 +226,7 @@ __device__ void mcg_apply_event(const McgDev& D, const McgKind& K, int c, int64_
         if (F.tail - F.head >= F.cap) {
           atomicOr(D.err, MCG_ERR_FLAG_FIFO);
         } else {
-          const int64_t slot = F.base + (F.tail % F.cap);
+          const int64_t slot = F.base + mcg_mod(F.tail, F.cap);
           D.fifo_step[slot] = s + S.ca_delay;
           D.fifo_si[slot] = (uint64_t(D.internal_seq[c]) << 32) | uint64_t(inst);
           D.fifo_src[slot] = src;
