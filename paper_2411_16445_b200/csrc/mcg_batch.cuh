@@ -1565,7 +1565,8 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
             McgStcVal v{h, B.stc[S4 + f], cc, a};
             double delta = 0.0;
             const bool changed = mcg_stc_step(S, D.dt, D.seed, D.gid0 + uint32_t(c), g.gi, i, s,
-                                              late, prp, g.vol, g.rvol, v, delta);
+                                              late, prp, g.vol, g.rvol, v, delta,
+                                              D.stc_nz + g.inst + i);
             B.stc[f] = v.h;
             B.stc[S4 + f] = v.z;
             B.stc[2 * S4 + f] = v.c;
@@ -1628,7 +1629,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
             double delta = 0.0;
             const int li = f - cs[k].stc_off - g.start;
             changed = mcg_stc_step(S, D.dt, D.seed, D.gid0 + uint32_t(c), g.gi, li, s, late, prp,
-                                   g.vol, g.rvol, v[u], delta);
+                                   g.vol, g.rvol, v[u], delta, D.stc_nz + jj[u]);
             dlt[u] = delta;
             D.i_stc_h[jj[u]] = v[u].h;
             D.i_stc_z[jj[u]] = v[u].z;

@@ -26,6 +26,12 @@
 #define MCG_ERR_FLAG_ACTIVE 4
 #define MCG_ERR_FLAG_SPIKES 8
 
+// memo of one STC instance's noise pair (mcg_stc_noise); tag -1: empty
+struct __align__(16) McgNzCache {
+  long long tag;
+  double z;
+};
+
 struct McgDev {
   double dt;
   uint64_t seed;
@@ -67,6 +73,7 @@ struct McgDev {
   int64_t* i_stdp_last;
   double* i_homeo_w;
   double *i_stc_h, *i_stc_z, *i_stc_c, *i_sps_abs;
+  McgNzCache* stc_nz;  // per STC instance: z1 of the last even step's noise pair
   // per-cell inboxes (mcg_events.cuh): incoming keys of this epoch (unsorted)
   // and the sorted pending list, double buffered; key = step << rank_bits | rank
   uint64_t* inc;
@@ -311,11 +318,28 @@ struct McgStcVal {
   double h, z, c, a;
 };
 
-// plasticity noise draw of one STC instance (rare: calcium above a threshold)
-__device__ __noinline__ double mcg_stc_noise(uint64_t seed, uint32_t gid, int gi, int i,
-                                             int64_t s) {
+// plasticity noise draw of one STC instance (calcium above a threshold):
+// normal_for(key, s) with the instance's key. Steps 2p and 2p + 1 draw the two
+// normals of one Box-Muller pair, so the even step leaves z1 in the instance's
+// McgNzCache entry for the odd one (a memo of a pure function of the key and
+// the step: valid across restores and fast-forwards)
+__device__ __noinline__ double mcg_stc_noise(McgNzCache* e, uint64_t seed, uint32_t gid, int gi,
+                                             int i, int64_t s) {
+  const uint64_t n = static_cast<uint64_t>(s);
+  const long long pr = static_cast<long long>(n >> 1);
+  if (n & 1u) {
+    const McgNzCache c = *e;
+    if (c.tag == pr) return c.z;
+  }
   const mcg_key key = mcg_make_key(seed, gid, (2ull << 32) | uint64_t(gi), uint64_t(i));
-  return mcg_normal_for(&key, static_cast<uint64_t>(s));
+  double z0, z1;
+  mcg_normal_pair_for(&key, n, &z0, &z1);
+  if (n & 1u) return z1;
+  McgNzCache c;
+  c.tag = pr;
+  c.z = z1;
+  *e = c;
+  return z0;
 }
 
 // A synapse at rest — h exactly at its baseline, calcium above neither
@@ -351,11 +375,11 @@ __device__ __forceinline__ bool mcg_stc_at_rest(const McgStcRest& R, bool late, 
 __device__ __forceinline__ bool mcg_stc_step(const McgSpec& S, double dt, uint64_t seed,
                                              uint32_t gid, int gi, int i, int64_t s, bool late,
                                              double prp, double vol, double rvol, McgStcVal& v,
-                                             double& delta) {
+                                             double& delta, McgNzCache* nz) {
   double h = v.h;
   const bool up = v.c > S.theta_p, dn = v.c > S.theta_d;
   double nrm = 0.0;
-  if (S.sigma != 0.0 && (up || dn)) nrm = mcg_stc_noise(seed, gid, gi, i, s);
+  if (S.sigma != 0.0 && (up || dn)) nrm = mcg_stc_noise(nz, seed, gid, gi, i, s);
   // stc_early_step
   const int crossings = int(up) + int(dn);
   double d = 0.1 * (S.h0 - h);

@@ -146,6 +146,7 @@ struct Engine {
   DBuf<int32_t> d_i_comp, d_i_active;
   DBuf<double> d_i_weight, d_i_kernel, d_i_stdp_pre, d_i_stdp_post, d_i_stdp_w, d_i_homeo_w,
       d_i_stc_h, d_i_stc_z, d_i_stc_c, d_i_sps_abs;
+  DBuf<McgNzCache> d_stc_nz;
   DBuf<int64_t> d_i_stdp_last;
   // edges
   DBuf<int32_t> d_e_dst, d_e_group;
@@ -496,6 +497,9 @@ struct Engine {
     d_i_stc_z.upload(m.i_stc_z, st);
     d_i_stc_c.upload(m.i_stc_c, st);
     d_i_sps_abs.upload(m.i_sps_abs, st);
+    d_stc_nz.alloc(std::max<size_t>(m.i_stc_h.size(), 1));
+    if (d_stc_nz.p)
+      CK(cudaMemsetAsync(d_stc_nz.p, 0xff, d_stc_nz.n * sizeof(McgNzCache), st));  // tag -1
     d_e_dst.upload(m.e_dst, st);
     d_e_group.upload(m.e_group, st);
     d_e_inst.upload(m.e_inst, st);
@@ -699,6 +703,7 @@ struct Engine {
     D.i_stdp_last = d_i_stdp_last.p;
     D.i_homeo_w = d_i_homeo_w.p;
     D.i_stc_h = d_i_stc_h.p;
+    D.stc_nz = d_stc_nz.p;
     D.i_stc_z = d_i_stc_z.p;
     D.i_stc_c = d_i_stc_c.p;
     D.i_sps_abs = d_i_sps_abs.p;

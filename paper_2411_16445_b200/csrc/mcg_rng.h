@@ -101,6 +101,17 @@ MCG_HD void mcg_normal_pair(double u1, double u2, double* z0, double* z1) {
 }
 
 // normal_for (rng.cpp:67-78)
+// both normals of the Box-Muller pair that normal_for(key, n) draws from
+// (counters 2p and 2p + 1 share it: z0 for the even one, z1 for the odd one)
+MCG_HD void mcg_normal_pair_for(const mcg_key* key, uint64_t n, double* z0, double* z1) {
+  uint64_t x[4];
+  mcg_threefry(key, n >> 2, x);
+  const unsigned pair = (unsigned)((n >> 1) & 1u);
+  const double u1 = ((double)(x[2 * pair] >> 11) + 1.0) * MCG_2POW_M53;
+  const double u2 = (double)(x[2 * pair + 1] >> 11) * MCG_2POW_M53;
+  mcg_normal_pair(u1, u2, z0, z1);
+}
+
 MCG_HD double mcg_normal_for(const mcg_key* key, uint64_t n) {
   uint64_t x[4];
   mcg_threefry(key, n >> 2, x);
