@@ -301,6 +301,18 @@ enum { MCG_MATH_EXP = 0, MCG_MATH_LOG = 1, MCG_MATH_SIN = 2, MCG_MATH_COS = 3,
 mcg_status mcg_device_math(int32_t device, int32_t func, const double* in, int64_t n,
                            const uint64_t key[4], uint64_t n0, double* out);
 
+/* ---- host libm pin (bitwise parity precondition) ----------------------- */
+
+/* Checks that the libm.so.6 mapped into this process is the glibc build the
+ * device ports were written against (build-id 0d9969fe…, glibc 2.39-0ubuntu8.5),
+ * that the CPU has FMA + AVX2 (glibc's ifunc then selects the FMA variants the
+ * ports follow), and that the host build of the ports agrees bit for bit with
+ * the live exp/log/sincos on `samples` pseudo-random arguments per range
+ * (<= 0: 20000).  The reference's libm calls (engine.cpp:44-54, :582-719,
+ * rng.cpp:62-64) produce the engine's results only when this returns MCG_OK.
+ * A one-line report is written to report[0..cap). */
+mcg_status mcg_libm_check(int64_t samples, char* report, int64_t cap);
+
 /* ---- recipe materialization on the device --------- */
 
 /* Directed Erdos-Renyi sample of er_connected (network.cpp:34-39):

@@ -54,9 +54,34 @@ static int compare(A& ref, B& gpu, const mcsim::Recipe& r, double t_ms) {
     std::printf("FAIL checkpoints differ (%zu vs %zu bytes)\n", b0.size(), b1.size());
     return 1;
   }
+  // restore over a diverged state that has a live cell() mirror: the mirror
+  // must be dropped, not written back over the restored state
+  gpu.advance_to(t_ms + 100.0);
+  (void)gpu.cell(0);
   gpu.restore(mcsim::Checkpoint::deserialize(b0));
-  std::printf("OK %zu spikes identical, checkpoints identical (%zu bytes), t = %.1f ms\n",
-              s0.size(), b0.size(), t_ms);
+  if (gpu.cell(0).v_mV != ref.cell(0).v_mV) {
+    std::printf("FAIL cell 0 after restore returns the pre-restore mirror\n");
+    return 1;
+  }
+  ref.clear_spikes();
+  gpu.clear_spikes();
+  const double t2 = t_ms + 200.0;
+  ref.advance_to(t2);
+  gpu.advance_to(t2);
+  const auto& r0 = ref.spikes();
+  const auto& r1 = gpu.spikes();
+  bool same = r0.size() == r1.size();
+  for (std::size_t i = 0; same && i < r0.size(); ++i)
+    same = r0[i].gid == r1[i].gid && std::memcmp(&r0[i].t_ms, &r1[i].t_ms, 8) == 0;
+  for (uint32_t gid = 0; same && gid < n; gid += (n > 16 ? n / 16 : 1))
+    same = ref.cell(gid).v_mV == gpu.cell(gid).v_mV && ref.cell(gid).species == gpu.cell(gid).species;
+  if (!same) {
+    std::printf("FAIL continuation after restore differs (%zu vs %zu spikes)\n", r0.size(), r1.size());
+    return 1;
+  }
+  std::printf("OK %zu spikes identical, checkpoints identical (%zu bytes), t = %.1f ms; "
+              "restore + %zu spikes to %.1f ms identical\n",
+              s0.size(), b0.size(), t_ms, r0.size(), t2);
   return 0;
 }
 

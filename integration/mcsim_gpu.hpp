@@ -13,7 +13,8 @@
 //     reference's observers expect: test_engine.cpp:106, 178-180, 213-226);
 //   * failures rethrow the reference's exception types with its messages
 //     (EngineError, NumericError, TargetingError, MorphologyError).
-// make_checkpoint / restore are not provided yet.
+// make_checkpoint / restore exchange MCSCKPT1 bytes through the reference's
+// own Checkpoint type; either engine restores the other's.
 #pragma once
 
 #include <cstring>
@@ -286,6 +287,9 @@ class Engine {
   }
   void restore(const mcsim::Checkpoint& c) {
     const std::vector<std::uint8_t> b = c.serialize();
+    // mirrors taken before the restore describe the state being replaced:
+    // drop them unwritten, or the next flush would overwrite the restored state
+    cells_.clear();
     check(mcg_restore(eng_, b.data(), static_cast<int64_t>(b.size())));
     invalidate();
   }

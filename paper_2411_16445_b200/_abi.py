@@ -143,7 +143,8 @@ EXPORTS = ("mcg_create", "mcg_destroy", "mcg_last_error", "mcg_abi_version", "mc
            "mcg_get_stats", "mcg_set_timing", "mcg_device_math",
            "mcg_er_connect", "mcg_shard_spike_cap", "mcg_shard_gid_begin", "mcg_shard_gid_end",
            "mcg_shard_set_buffers", "mcg_shard_run_epoch", "mcg_partition",
-           "mcg_gb_trials", "mcg_gb_dp_curve", "mcg_stdp_window", "mcg_checkpoint", "mcg_restore")
+           "mcg_gb_trials", "mcg_gb_dp_curve", "mcg_stdp_window", "mcg_checkpoint", "mcg_restore",
+           "mcg_libm_check")
 
 _lib = None
 
@@ -191,6 +192,7 @@ def _declare(L):
         "mcg_partition": (C.c_int32, [P(mcg_recipe), C.c_int32, C.c_void_p]),
         "mcg_checkpoint": (C.c_int32, [eng, C.c_void_p, C.c_int64, P(C.c_int64)]),
         "mcg_restore": (C.c_int32, [eng, C.c_void_p, C.c_int64]),
+        "mcg_libm_check": (C.c_int32, [C.c_int64, C.c_char_p, C.c_int64]),
         "mcg_gb_trials": (C.c_int32, [C.c_int32, P(mcg_gb_params), C.c_void_p, C.c_int32,
                                       P(mcg_gb_protocol), C.c_void_p, C.c_void_p]),
         "mcg_gb_dp_curve": (C.c_int32, [C.c_int32, P(mcg_gb_params), C.c_void_p, C.c_int32,
@@ -216,3 +218,12 @@ def lib():
         _declare(L)
         _lib = L
     return _lib
+
+
+def libm_check(samples: int = 20000):
+    """(ok, report): is this host's libm the glibc build the device ports
+    follow (mcg_libm_check in include/mcg.h)?  Bitwise parity with a reference
+    running on this host needs ok."""
+    buf = C.create_string_buffer(512)
+    st = lib().mcg_libm_check(samples, buf, len(buf))
+    return st == 0, buf.value.decode()

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libmcg.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["mcg_engine.cu", "mcg_build.cpp"]
+SOURCES = ["mcg_engine.cu", "mcg_build.cpp", "mcg_hostcheck.cpp"]
 HEADERS = ["mcg_build.h", "mcg_device.cuh", "mcg_events.cuh", "mcg_mech.cuh", "mcg_epoch.cuh", "mcg_batch.cuh",
            "mcg_sweep.cuh", "mcg_protocols.cuh", "mcg_checkpoint.h",
            "mcg_libm.h",
@@ -39,7 +39,7 @@ def build_engine(force=False, verbose=False):
     if not force and not _stale(LIB, deps):
         return LIB
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++20",
-           "-Xcompiler", "-fPIC,-ffp-contract=off", "-shared",
+           "-Xcompiler", "-fPIC,-ffp-contract=off", "-shared", "-ldl",
            *[os.path.join(CSRC, f) for f in SOURCES], "-o", LIB + ".tmp"]
     if verbose:
         print(" ".join(cmd), flush=True)

@@ -1004,6 +1004,11 @@ struct Engine {
 
   void fast_forward_to(double t_ms, double coarse_dt_ms) {
     invalidate_mirror();
+    // a shard cannot decide the reference's pending-spike guard alone: the
+    // other ranks' spikes of the last epoch (x_recv) are not expanded yet, and
+    // the guard's reset-before-throw order runs over the global gid range
+    if (m.world > 1)
+      throw Error(MCG_ERR_ENGINE, "fast-forward: not supported for a sharded engine");
     const double dt = m.dt;
     const int64_t per = static_cast<int64_t>(std::llround(coarse_dt_ms / dt));
     if (per < 1 || std::fabs(double(per) * dt - coarse_dt_ms) > 1e-9 * coarse_dt_ms)

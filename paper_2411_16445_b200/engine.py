@@ -90,10 +90,11 @@ class Checkpoint:
             if count > (len(d) - pos) // 8:
                 raise EngineError("checkpoint: corrupted length header")
             raw = take(8 * count)
+            # a repeated name keeps its first record (the reference emplaces)
             if typ == 0:
-                f64[name] = np.frombuffer(raw, "<f8").copy()
+                f64.setdefault(name, np.frombuffer(raw, "<f8").copy())
             elif typ == 1:
-                u64[name] = np.frombuffer(raw, "<u8").copy()
+                u64.setdefault(name, np.frombuffer(raw, "<u8").copy())
             else:
                 raise EngineError("checkpoint: unknown record type")
         return f64, u64

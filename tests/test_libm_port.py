@@ -24,3 +24,12 @@ def test_port_matches_glibc(checker, seed):
     r = subprocess.run([checker, "1000000", str(seed)], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr[-2000:] + r.stdout
     assert "0 mismatches" in r.stdout
+
+
+def test_runtime_libm_pin():
+    """libmcg's load-time pin: this host's libm build-id, its FMA ifunc
+    variant and a differential run all agree with the device ports' tables."""
+    from paper_2411_16445_b200 import _abi
+    ok, rep = _abi.libm_check(50000)
+    assert ok, rep
+    assert "matches the tables" in rep and "0/" in rep
