@@ -41,6 +41,11 @@ DT_MS = 0.5
 SEED = 1
 N_CELLS, N_EXC = 2000, 1600
 METRIC = "simulated s per wall s (consolidation network, fine steps)"
+# both arms run the reference's build_consolidation_network recipe (seed 1); the
+# GPU arm builds it with this repo's port (network.py), pinned equal to the
+# reference builder's recipe at N = 300, 2000 and 4000 (tests/test_gpu_builders.py,
+# tests/test_gpu_configs.py), the reference arm with the reference's own builder
+DATA_NOTE = "synthetic: build_consolidation_network(config 3, seed 1) recipe"
 UNIT = "sim-s/wall-s"
 
 
@@ -50,12 +55,43 @@ def workload_config():
                                  dt_ms=DT_MS)
 
 
-def config_block(n_gpus, l2_note):
+L2_NOTE = ("GPU arm: a 256 MB buffer is written between timed steps (flushes the 126 MB L2); "
+           "reference arm: host CPU, no device cache")
+
+
+def config_block(n_gpus):
+    """Identical in both arms (the driver compares them)."""
     return {"workload": "config3: consolidation network N=2000 (1600 MC exc x 31 comps + 400 point inh), "
                         "p=0.1, STC synapses, seed 1, dt 0.5 ms, 8h protocol, step = 500 ms bio",
             "n_cells": N_CELLS, "compartments": 50000, "dt_ms": DT_MS, "step_bio_ms": STEP_MS,
             "parallelism": f"cells sharded over {n_gpus} GPU(s)" if n_gpus > 1 else "single GPU",
-            "l2": l2_note}
+            "l2": L2_NOTE}
+
+
+def host_facts():
+    """CPU model and glibc of the host the CPU figures were taken on."""
+    model = "?"
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((l.split(":", 1)[1].strip() for l in f if l.startswith("model name")), "?")
+    except OSError:
+        pass
+    try:
+        libc = os.confstr("CS_GNU_LIBC_VERSION")
+    except (ValueError, OSError):
+        libc = "?"
+    return {"cpu_model": model, "glibc": libc, "host_threads": os.cpu_count() or 1}
+
+
+def ref_workload_recipe():
+    """The workload's recipe from the REFERENCE's own builder
+    (build_consolidation_network, network.cpp:426-598, in oracle/_ref): the
+    reference arm never maps this repo's library."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import ref
+    cfg = ref.default_consolidation(n_cells=N_CELLS, n_exc=N_EXC, seed=SEED, multi_compartment=1,
+                                    dt_ms=DT_MS)
+    return ref.RefRecipe.consolidation(cfg, True)
 
 
 class ClockSampler:
@@ -143,8 +179,9 @@ def flush_l2():
     del buf
 
 
-def cpu_baseline(recipe_view, sample_ms):
-    """Reference engine (oracle/_ref) on the host cores, bounded sample."""
+def cpu_baseline(recipe_view, sample_ms, sample_ms_1w):
+    """Reference engine (oracle/_ref) on the host cores, bounded samples: all
+    host threads (the headline CPU figure) and one worker."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import ref
     cores = os.cpu_count() or 1
@@ -152,21 +189,27 @@ def cpu_baseline(recipe_view, sample_ms):
     t0 = time.perf_counter()
     e.advance_to(sample_ms)
     w = time.perf_counter() - t0
+    del e
+    e1 = ref.RefEngine(recipe_view, DT_MS, SEED, 1)
+    t0 = time.perf_counter()
+    e1.advance_to(sample_ms_1w)
+    w1 = time.perf_counter() - t0
+    del e1
     return {"value": (sample_ms * 1e-3) / w, "unit": UNIT, "cores": cores, "kind": "reference",
-            "sample": f"config3 recipe, advance 0 -> {sample_ms:.0f} ms bio, workers={cores}"}
+            "sample": f"config3 recipe, advance 0 -> {sample_ms:.0f} ms bio, workers={cores}",
+            "one_worker": {"value": (sample_ms_1w * 1e-3) / w1, "unit": UNIT, "cores": 1,
+                           "sample": f"advance 0 -> {sample_ms_1w:.0f} ms bio, workers=1"},
+            **host_facts()}
 
 
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from paper_2411_16445_b200 import network as N
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    rr = ref_workload_recipe()
     import ref
-    b = N.build_consolidation_network(workload_config(), True)
-    flat = b.recipe.flatten()
     cores = os.cpu_count() or 1
-    e = ref.RefEngine(flat.view, DT_MS, SEED, cores)
+    e = ref.RefEngine(rr.view, DT_MS, SEED, cores)
     t = 0.0
     for _ in range(args.warmup):
         t += STEP_MS
@@ -180,10 +223,11 @@ def run_reference_arm(args):
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_block(args.gpus, "n/a (CPU)"),
+            "vs_baseline": None, "dtype": "f64", "data": DATA_NOTE,
+            "config": config_block(args.gpus),
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "reference",
-                             "sample": f"steps {args.warmup}..{args.warmup + args.steps} of 500 ms bio"},
+                             "sample": f"steps {args.warmup}..{args.warmup + args.steps} of 500 ms bio, "
+                                       f"workers={cores}", **host_facts()},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -370,7 +414,7 @@ def run_gpu_arm(args):
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(flat.view, args.cpu_sample_ms)
+        cpu = cpu_baseline(flat.view, args.cpu_sample_ms, args.cpu_sample_ms_1w)
 
     other = None if args.no_other else other_configs()
 
@@ -378,8 +422,8 @@ def run_gpu_arm(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference's own recipe builder, seed 1)",
-        "config": config_block(world, "256 MB buffer written between timed steps (flushes L2)"),
+        "data": DATA_NOTE,
+        "config": config_block(world),
         "compartment_updates_per_s": 50000 * fine_steps / total,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic_per_launch(steps_per_launch),
@@ -487,8 +531,8 @@ def run_gpu_arm_sharded(args, world, rank):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (reference's own recipe builder, seed 1)",
-            "config": config_block(world, "256 MB buffer written after warm-up (flushes L2)"),
+            "data": DATA_NOTE,
+            "config": config_block(world),
             "compartment_updates_per_s": 50000 * fine_steps / total,
             "exchange": backend,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -515,6 +559,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-sample-ms", type=float, default=2000.0)
+    ap.add_argument("--cpu-sample-ms-1w", type=float, default=1000.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-other", action="store_true", help="skip the secondary configurations")
     args = ap.parse_args()
