@@ -314,6 +314,7 @@ def other_configs():
                                   "spikes": int(len(e.spike_arrays()[0]))}
     e.close()
     del b
+    out["busyring"] = busyring_configs()
     p = PR.GbParams()
     deltas = [-100.0, -50.0, -30.0, -20.0, -10.0, -5.0, 0.0, 5.0, 10.0, 20.0, 30.0, 50.0, 100.0]
     proto = PR.GbPairingProtocol(dt_ms=0.05, trials=4000, seed=999)
@@ -327,6 +328,62 @@ def other_configs():
                                       "wall_s": wall,
                                       "trial_steps_per_s": len(deltas) * proto.trials * n_steps / wall,
                                       "mean_change": [pt.mean_change for pt in curve]}
+    return out
+
+
+BUSYRING_W = 0.050515121785495443  # SURVEY §8(c) golden: calibrated ring weight (bench.cpp:105-132)
+
+
+def busyring_configs():
+    """The HH + STDP workload (bench.cpp:134-194, run_bench_once): 1024 HH
+    cells with depth-2 dendritic trees, rings of 4, 1000 zero-weight random
+    synapses per cell, dt 0.025 ms, 200 ms; without and with STDP on the
+    random synapses.  Both engines run the reference builder's recipe
+    (oracle/_ref); setup and propagation are timed separately as run_bench
+    does: device time (CUDA events) and wall for this library, wall for the
+    reference with all host threads.  Spike counts of the two engines are
+    reported side by side (the parity tests check the trains bitwise)."""
+    import time as _t
+    from paper_2411_16445_b200 import Engine, EngineOptions
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import ref
+    cores = os.cpu_count() or 1
+    out = {}
+    for name, stdp in (("busyring_1024_d2", 0), ("busyring_1024_d2_stdp", 1)):
+        rr = ref.RefRecipe.busyring(ref.default_busyring(ring_weight_uS=BUSYRING_W, stdp_on_random=stdp))
+        view = rr.view
+        t0 = _t.perf_counter()
+        e = Engine(view, EngineOptions(0.025, 0), device=0)
+        setup = _t.perf_counter() - t0
+        e.set_timing(True)
+        s0 = e.stats()
+        t1 = _t.perf_counter()
+        e.advance_to(200.0)
+        prop_wall = _t.perf_counter() - t1
+        s1 = e.stats()
+        dev_s = (s1["advance_ms"] - s0["advance_ms"]) * 1e-3
+        steps = s1["steps"] - s0["steps"]
+        nsp = int(len(e.spike_arrays()[0]))
+        comps = s1["total_comps"]
+        e.close()
+        t0 = _t.perf_counter()
+        r = ref.RefEngine(view, 0.025, 0, cores)
+        r_setup = _t.perf_counter() - t0
+        t1 = _t.perf_counter()
+        r.advance_to(200.0)
+        r_prop = _t.perf_counter() - t1
+        r_nsp = int(len(r.spike_arrays()[0]))
+        del r
+        out[name] = {"cells": 1024, "compartments": comps, "synapses": s1["total_synapses"],
+                     "hh_comps": s1["hh_comps"], "bio_ms": 200.0, "dt_ms": 0.025, "steps": steps,
+                     "prop_device_s": dev_s, "prop_wall_s": prop_wall, "setup_s": setup,
+                     "us_per_fine_step": 1e6 * dev_s / max(steps, 1),
+                     "compartment_updates_per_s": comps * steps / dev_s,
+                     "spikes": nsp,
+                     "reference": {"prop_wall_s": r_prop, "setup_s": r_setup, "workers": cores,
+                                   "spikes": r_nsp, "kind": "reference (oracle/_ref)"},
+                     "prop_speedup_vs_reference": r_prop / prop_wall}
+        del rr
     return out
 
 
@@ -565,6 +622,13 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus != world:
+        # one process per GPU: N > 1 runs under torchrun, which sets WORLD_SIZE
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} ranks (WORLD_SIZE={world}); launch with "
+              f"python -m torch.distributed.run --nproc-per-node {args.gpus} --master-addr 127.0.0.1 "
+              f"bench.py --gpus {args.gpus}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_gpu_arm(args)

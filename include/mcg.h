@@ -160,6 +160,12 @@ typedef struct { /* Recipe, recipe.hpp:183-189, connections/probes as SoA */
   const int32_t* probe_group;     /* label resolved; -1 when the label is empty */
   const int32_t* probe_instance;
   const int32_t* probe_every;
+  /* optional (0 / NULL allowed): the label text of each connection, so an
+     unresolved label (conn_group -1) is reported with the reference's message
+     "connection label '<label>' not found" (engine.cpp:367-369) */
+  int32_t n_labels;
+  const char* const* labels;
+  const int32_t* conn_label;      /* index into labels per connection */
 } mcg_recipe;
 
 typedef struct { /* EngineOptions, engine.hpp:37-41, plus placement */

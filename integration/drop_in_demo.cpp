@@ -85,10 +85,42 @@ static int compare(A& ref, B& gpu, const mcsim::Recipe& r, double t_ms) {
   return 0;
 }
 
+// a malformed recipe through both engines: the same exception type and text
+template <class E>
+static std::string build_error(const mcsim::Recipe& r, const mcsim::EngineOptions& opt) {
+  try {
+    E e(r, opt);
+  } catch (const mcsim::EngineError& x) {
+    return std::string("EngineError: ") + x.what();
+  } catch (const std::exception& x) {
+    return std::string("other: ") + x.what();
+  }
+  return "no error";
+}
+
+static int errors() {
+  mcsim::ConsolidationConfig cfg;
+  cfg.n_cells = 20;
+  cfg.n_exc = 16;
+  cfg.pattern = 4;
+  mcsim::ConsolidationBuild b = mcsim::build_consolidation_network(cfg, false);
+  const mcsim::EngineOptions opt{cfg.dt_ms, cfg.seed, 1};
+  b.recipe.connections.at(3).label = "no_such_label";
+  const std::string e0 = build_error<mcsim::Engine>(b.recipe, opt);
+  const std::string e1 = build_error<mcsim_gpu::Engine>(b.recipe, opt);
+  if (e0 != e1 || e0.find("no_such_label") == std::string::npos) {
+    std::printf("FAIL build errors differ: '%s' vs '%s'\n", e0.c_str(), e1.c_str());
+    return 1;
+  }
+  std::printf("OK both engines: %s\n", e0.c_str());
+  return 0;
+}
+
 int main(int argc, char** argv) {
   const std::string which = argc > 1 ? argv[1] : "consolidation";
   const double t_ms = argc > 2 ? std::atof(argv[2]) : 2000.0;
   try {
+    if (which == "errors") return errors();
     if (which == "busyring") {
       mcsim::BusyringSpec spec = mcsim::default_busyring();
       spec.n_cells = 256;

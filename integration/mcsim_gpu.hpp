@@ -70,6 +70,11 @@ class FlatRecipe {
       c_src_.push_back(c.src);
       c_dst_.push_back(c.dst);
       c_group_.push_back(label_index(r, c.dst, c.label));
+      if (c_group_.back() < 0) {  // unresolved: keep the text for the build's message
+        c_label_.resize(c_group_.size(), -1);
+        c_label_.back() = static_cast<int32_t>(miss_text_.size());
+        miss_text_.push_back(c.label);
+      }
       c_policy_.push_back(static_cast<uint8_t>(c.policy));
       c_w_.push_back(c.weight);
       c_d_.push_back(c.delay_ms);
@@ -95,6 +100,13 @@ class FlatRecipe {
     view_.conn_src = c_src_.data();
     view_.conn_dst = c_dst_.data();
     view_.conn_group = c_group_.data();
+    if (!miss_text_.empty()) {
+      c_label_.resize(c_group_.size(), -1);
+      for (const auto& t : miss_text_) miss_ptr_.push_back(t.c_str());
+      view_.n_labels = static_cast<int32_t>(miss_ptr_.size());
+      view_.labels = miss_ptr_.data();
+      view_.conn_label = c_label_.data();
+    }
     view_.conn_policy = c_policy_.data();
     view_.conn_weight = c_w_.data();
     view_.conn_delay_ms = c_d_.data();
@@ -221,6 +233,9 @@ class FlatRecipe {
   std::vector<uint32_t> c_src_, c_dst_, p_gid_, cell_kind_;
   std::vector<int32_t> c_group_, p_comp_, p_species_, p_group_, p_instance_, p_every_;
   std::vector<double> c_w_, c_d_;
+  std::vector<int32_t> c_label_;        // per connection: index into miss_text_ (-1: resolved)
+  std::vector<std::string> miss_text_;  // unresolved connection labels, for error messages
+  std::vector<const char*> miss_ptr_;
   mcg_recipe view_{};
 };
 

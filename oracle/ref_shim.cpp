@@ -50,7 +50,9 @@ int guard(F&& f) {
   }
 }
 
-std::string glabel(int i) { return "g" + std::to_string(i); }
+// placement labels of a flat recipe: a prefix no user label carries, so an
+// unresolved label passed through by text never matches one
+std::string glabel(int i) { return "\x1fg" + std::to_string(i); }
 std::string slabel(int i) { return "s" + std::to_string(i); }
 
 StcParams to_stc(const mcg_stc_params& p) {
@@ -154,7 +156,9 @@ Recipe to_recipe(const mcg_recipe& f) {
     c.from_source = f.conn_from_source[i] != 0;
     c.src = f.conn_src[i];
     c.dst = f.conn_dst[i];
-    c.label = f.conn_group[i] >= 0 ? glabel(f.conn_group[i]) : "__missing__";
+    c.label = f.conn_group[i] >= 0 ? glabel(f.conn_group[i])
+              : (f.labels && f.conn_label && f.conn_label[i] >= 0 && f.conn_label[i] < f.n_labels)
+                  ? std::string(f.labels[f.conn_label[i]]) : "__missing__";
     c.policy = static_cast<SelectionPolicy>(f.conn_policy[i]);
     c.weight = f.conn_weight[i];
     c.delay_ms = f.conn_delay_ms[i];

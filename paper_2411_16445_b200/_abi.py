@@ -95,7 +95,9 @@ class mcg_recipe(C.Structure):
                 ("n_probes", C.c_int32), ("probe_gid", C.POINTER(C.c_uint32)),
                 ("probe_what", C.POINTER(C.c_uint8)), ("probe_comp", C.POINTER(C.c_int32)),
                 ("probe_species", C.POINTER(C.c_int32)), ("probe_group", C.POINTER(C.c_int32)),
-                ("probe_instance", C.POINTER(C.c_int32)), ("probe_every", C.POINTER(C.c_int32))]
+                ("probe_instance", C.POINTER(C.c_int32)), ("probe_every", C.POINTER(C.c_int32)),
+                ("n_labels", C.c_int32), ("labels", C.POINTER(C.c_char_p)),
+                ("conn_label", C.POINTER(C.c_int32))]
 
 
 class mcg_options(C.Structure):

@@ -583,8 +583,13 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
     if (dst >= static_cast<uint32_t>(r.n_cells)) engine_error("connection dst out of range");
     const int32_t gi = r.conn_group[ci];
     const mcg_kind& dspec = r.kinds[r.cell_kind[dst]];
-    if (gi < 0 || gi >= dspec.n_placements)
-      engine_error("connection label '#" + std::to_string(gi) + "' not found");
+    if (gi < 0 || gi >= dspec.n_placements) {
+      const int32_t li = (r.labels && r.conn_label) ? r.conn_label[ci] : -1;
+      engine_error("connection label '" +
+                   ((li >= 0 && li < r.n_labels && r.labels[li]) ? std::string(r.labels[li])
+                                                                  : "#" + std::to_string(gi)) +
+                   "' not found");
+    }
     const bool local = dst >= g0 && dst < g1;
     uint32_t instance = 0;
     const mcg_placement& pl = dspec.placements[gi];

@@ -443,20 +443,20 @@ class FlatRecipe:
         for k, ks in enumerate(r.kinds):
             for li, lab in enumerate(t.labels):
                 lut[k, li] = ks.find_group(lab)
+        # unresolved labels and out-of-range destinations or kinds pass through
+        # as -1: the engine's build reports them in the reference's order
+        # (engine.cpp:317-391), naming the label from the table below
         group = np.full(len(t), -1, np.int32)
         if len(t):
             ok = t.dst < n_cells
-            dk = np.zeros(len(t), np.int64)
+            dk = np.full(len(t), -1, np.int64)
             dk[ok] = cell_kind[t.dst[ok]]
+            ok &= (dk >= 0) & (dk < nk)
             group[ok] = lut[dk[ok], t.label_idx[ok]]
-            bad = np.nonzero(ok & (group < 0))[0]
-            bad_dst = np.nonzero(~ok)[0]
-            first_bad = min(bad[0] if len(bad) else len(t), bad_dst[0] if len(bad_dst) else len(t))
-            if first_bad < len(t):
-                if not ok[first_bad]:
-                    raise EngineError("connection dst out of range")
-                raise EngineError(f"connection label '{t.labels[t.label_idx[first_bad]]}' not found")
-        for a in (t.from_source, t.src, t.dst, group, t.policy, t.weight, t.delay_ms):
+        label_idx = np.ascontiguousarray(t.label_idx, dtype=np.int32)
+        label_txt = (C.c_char_p * max(len(t.labels), 1))(*[s.encode() for s in t.labels])
+        for a in (t.from_source, t.src, t.dst, group, t.policy, t.weight, t.delay_ms, label_idx,
+                  label_txt):
             keep(a)
 
         npb = len(r.probes)
@@ -501,6 +501,9 @@ class FlatRecipe:
         v.probe_group = _arr(p_grp, C.c_int32)
         v.probe_instance = _arr(p_inst, C.c_int32)
         v.probe_every = _arr(p_every, C.c_int32)
+        v.n_labels = len(t.labels)
+        v.labels = C.cast(label_txt, C.POINTER(C.c_char_p))
+        v.conn_label = _arr(label_idx, C.c_int32)
         self.view = v
         self.n_cells = n_cells
         self.recipe = r

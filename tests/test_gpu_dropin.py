@@ -12,7 +12,7 @@ DEMO = os.path.join(ROOT, "integration", "_build", "drop_in_demo")
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("which,t_ms", [("consolidation", "2000"), ("busyring", "100")])
+@pytest.mark.parametrize("which,t_ms", [("consolidation", "2000"), ("busyring", "100"), ("errors", "0")])
 def test_drop_in_engine_matches_reference(gpu, which, t_ms):
     if not os.path.exists(DEMO):
         pytest.skip("drop_in_demo not built (needs the reference headers at build time)")

@@ -276,3 +276,16 @@ def test_random_recipe_large_mixed(gpu, monkeypatch, seed):
     assert len(rt) > 0
     assert np.array_equal(rt, gt) and np.array_equal(rg, gg)
     assert g.make_checkpoint().data == r.make_checkpoint()
+
+
+def test_build_errors_match_reference(gpu):
+    """Both engines raise the reference's message for each malformed recipe
+    (error order of Impl::build, engine.cpp:317-391; the label by name)."""
+    from test_recipe_host import _error_recipes
+    from paper_2411_16445_b200.recipe import EngineError
+    for r, msg in _error_recipes():
+        flat = r.flatten()
+        with pytest.raises(ref.RefError, match=msg):
+            ref.RefEngine(flat.view, 0.5, 1, 1)
+        with pytest.raises(EngineError, match=msg):
+            Engine(flat, EngineOptions(0.5, 1))

@@ -39,17 +39,46 @@ def test_flatten_roundtrip_through_reference():
     assert_recipes_equal(flat.view, back.view)
 
 
-def test_label_errors_match_reference_messages():
+def _error_recipes():
+    """Recipes with build errors, each paired with the reference's message
+    (Impl::build, engine.cpp:317-391: kinds first, then per connection dst,
+    label, source/src and delay, in connection order)."""
     kind = CellKindSpec(membrane=LifMembrane(exact=True),
                         placements=[PlacementSpec("in", SynSpec(kind=SynKind.static_charge))])
     kind.segments = N.build_consolidation_cell(N.ConsolidationCellParams()).segments
+    out = []
     r = Recipe(kinds=[kind], cell_kind=[0, 0], sources=[ScriptedSource([1.0])],
                connections=[ConnectionSpec(False, 0, 1, "nope", 0, 1.0, 5.0)])
-    with pytest.raises(EngineError, match="connection label 'nope' not found"):
-        r.flatten()
-    r.connections = [ConnectionSpec(False, 0, 7, "in", 0, 1.0, 5.0)]
-    with pytest.raises(EngineError, match="connection dst out of range"):
-        r.flatten()
+    out.append((r, "connection label 'nope' not found"))
+    out.append((Recipe(kinds=[kind], cell_kind=[0, 0], sources=[],
+                       connections=[ConnectionSpec(False, 0, 7, "in", 0, 1.0, 5.0)]),
+                "connection dst out of range"))
+    # an earlier error wins: the kind check precedes every connection check
+    out.append((Recipe(kinds=[kind], cell_kind=[0, 3], sources=[],
+                       connections=[ConnectionSpec(False, 0, 1, "nope", 0, 1.0, 5.0)]),
+                "cell kind out of range"))
+    # connection order: a bad src on connection 0 before a bad label on connection 1
+    out.append((Recipe(kinds=[kind], cell_kind=[0, 0], sources=[],
+                       connections=[ConnectionSpec(False, 9, 1, "in", 0, 1.0, 5.0),
+                                    ConnectionSpec(False, 0, 1, "gone", 0, 1.0, 5.0)]),
+                "connection src out of range"))
+    # a label resolving on no kind at an out-of-range destination: dst first
+    out.append((Recipe(kinds=[kind], cell_kind=[0, 0], sources=[],
+                       connections=[ConnectionSpec(False, 0, 1, "in", 0, 1.0, 5.0),
+                                    ConnectionSpec(False, 0, 5, "gone", 0, 1.0, 5.0)]),
+                "connection dst out of range"))
+    return out
+
+
+def test_build_errors_match_reference_messages():
+    """flatten() passes unresolved labels and out-of-range indices through;
+    the reference engine built from the flat recipe reports them in its own
+    order, naming the label (tests/test_gpu_random.py checks the GPU engine
+    raises the same)."""
+    for r, msg in _error_recipes():
+        flat = r.flatten()
+        with pytest.raises(ref.RefError, match=msg):
+            ref.RefEngine(flat.view, 0.5, 1, 1)
 
 
 def test_grid_layout_matches_reference_discretize():
