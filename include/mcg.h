@@ -273,6 +273,24 @@ uint32_t mcg_shard_gid_end(const mcg_engine* eng);
 mcg_status mcg_shard_set_buffers(mcg_engine* eng, int64_t* send, int64_t* recv, int64_t block_cap,
                                  int32_t world);
 mcg_status mcg_shard_run_epoch(mcg_engine* eng, double t_ms);
+/* The same loop with the exchange inside the library: mcg_shard_init_nccl
+ * creates an NCCL communicator of mcg_options.world ranks (this engine is
+ * mcg_options.rank) from an id made by mcg_nccl_unique_id on one rank and
+ * shared by the caller (any transport), and allocates the blocks on the
+ * engine's device.  mcg_shard_advance_to then runs every epoch up to t_ms as
+ * one stepping launch + ncclAllGather on the engine's stream, with one host
+ * wait per 32 epochs (inboxes are sized so that no epoch can overflow them;
+ * MCG_SHARD_SYNC=1 waits every epoch).  Every rank keeps the global spike
+ * list (all ranks' spikes, the reference's (epoch, gid, step) order);
+ * mcg_num_spikes / mcg_get_spikes keep returning this rank's own spikes.
+ * libnccl.so.2 is loaded at run time (dlopen).  Replaces the worker pool's
+ * barrier + Impl::exchange (engine.cpp:926-942, 875-889). */
+mcg_status mcg_nccl_unique_id(uint8_t id[128]);
+mcg_status mcg_shard_init_nccl(mcg_engine* eng, const uint8_t id[128]);
+mcg_status mcg_shard_advance_to(mcg_engine* eng, double t_ms);
+int64_t mcg_shard_num_global_spikes(const mcg_engine* eng);
+mcg_status mcg_shard_get_global_spikes(mcg_engine* eng, int64_t first, int64_t count, double* t_ms,
+                                       uint32_t* gid);
 /* the shard bounds mcg_create uses for (recipe, world): rank r owns gids
  * [bounds[r], bounds[r+1]); bounds has world + 1 entries.  Host only (no GPU). */
 mcg_status mcg_partition(const mcg_recipe* recipe, int32_t world, uint32_t* bounds);

@@ -146,7 +146,8 @@ EXPORTS = ("mcg_create", "mcg_destroy", "mcg_last_error", "mcg_abi_version", "mc
            "mcg_er_connect", "mcg_shard_spike_cap", "mcg_shard_gid_begin", "mcg_shard_gid_end",
            "mcg_shard_set_buffers", "mcg_shard_run_epoch", "mcg_partition",
            "mcg_gb_trials", "mcg_gb_dp_curve", "mcg_stdp_window", "mcg_checkpoint", "mcg_restore",
-           "mcg_libm_check")
+           "mcg_libm_check", "mcg_nccl_unique_id", "mcg_shard_init_nccl", "mcg_shard_advance_to",
+           "mcg_shard_num_global_spikes", "mcg_shard_get_global_spikes")
 
 _lib = None
 
@@ -192,6 +193,11 @@ def _declare(L):
         "mcg_shard_set_buffers": (C.c_int32, [eng, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32]),
         "mcg_shard_run_epoch": (C.c_int32, [eng, C.c_double]),
         "mcg_partition": (C.c_int32, [P(mcg_recipe), C.c_int32, C.c_void_p]),
+        "mcg_nccl_unique_id": (C.c_int32, [C.c_void_p]),
+        "mcg_shard_init_nccl": (C.c_int32, [eng, C.c_void_p]),
+        "mcg_shard_advance_to": (C.c_int32, [eng, C.c_double]),
+        "mcg_shard_num_global_spikes": (C.c_int64, [eng]),
+        "mcg_shard_get_global_spikes": (C.c_int32, [eng, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]),
         "mcg_checkpoint": (C.c_int32, [eng, C.c_void_p, C.c_int64, P(C.c_int64)]),
         "mcg_restore": (C.c_int32, [eng, C.c_void_p, C.c_int64]),
         "mcg_libm_check": (C.c_int32, [C.c_int64, C.c_char_p, C.c_int64]),

@@ -20,7 +20,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = ["mcg_engine.cu", "mcg_build.cpp", "mcg_hostcheck.cpp"]
 HEADERS = ["mcg_build.h", "mcg_device.cuh", "mcg_events.cuh", "mcg_mech.cuh", "mcg_epoch.cuh", "mcg_batch.cuh",
-           "mcg_sweep.cuh", "mcg_protocols.cuh", "mcg_checkpoint.h",
+           "mcg_sweep.cuh", "mcg_warp.cuh", "mcg_protocols.cuh", "mcg_checkpoint.h",
            "mcg_libm.h",
            "mcg_model.h",
            "mcg_rng.h", "glibc_tables.h"]

@@ -60,6 +60,8 @@ struct McgBatchArgs {
   unsigned long long* chunk_n;
   int64_t* x_send;         // sharded: this rank's spikes of the epoch [count, (gid, step, t) x cap]
   int64_t x_cap;
+  int32_t dbg;             // development trace (MCG_WARP_DBG: (cell + 1) << 8)
+  int64_t dbg_s;
 };
 
 // phase 1: sources of [s0, s1) + previous epoch's spikes (from the per-cell slots)
@@ -1391,12 +1393,17 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
       X.refractory = refractory;
       double* V = (K.n <= m) ? mcg_comp_block(A, B, tid) : D.v + D.comp_off[c];
       const int64_t cg0 = D.cg_off[c];
+      const bool trace = (A.dbg >> 8) == c + 1 && s >= A.dbg_s && s <= A.dbg_s + 5;
+      if (trace)
+        printf("[k_batch] cell %d s %lld staged %d ev [%d,%d) in [%d,%d) V0 %.17g\n", c, (long long)s, X.staged,
+               X.ev_cur, X.ev_end, X.in_cur, X.in_end, V[0]);
       if (X.staged) {
         // staged delivery (mcg_stage_events): network events, then delayed calcium
         const int S4 = A.stc_max;
         int e = X.ev_cur;
         while (e < X.ev_end && int(B.evb[e].so) == int(so)) {
           const McgEvSm E = B.evb[e];
+          if (trace) printf("[k_batch]   ev so %d grp %d inst %u w %.17g\n", int(E.so), E.group, E.inst & 0x7fffffffu, E.w);
           const uint32_t inst = E.inst & 0x7fffffffu;
           if (X.gk[E.group] == MCG_SYN_STATIC_CHARGE) {
             if (!refractory && (E.inst >> 31)) V[E.comp] += E.w;  // w * cf[comp]

@@ -11,6 +11,8 @@
 // asked (the lazily-synced mirror of engine.hpp).
 #include <cub/cub.cuh>  // mcg_er_connect's scan
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the library is dlopen'ed (NcclApi)
 
 #include <algorithm>
 #include <chrono>
@@ -24,6 +26,7 @@
 #include <unordered_map>
 
 #include "mcg_batch.cuh"
+#include "mcg_warp.cuh"
 #include "mcg_protocols.cuh"
 #include "mcg_checkpoint.h"
 #include "mcg_build.h"
@@ -111,6 +114,66 @@ __global__ void k_pending(McgDev D, const int64_t* out_begin, const int64_t* out
 }
 
 }  // namespace
+
+// NCCL, loaded at run time by the first engine that shards through it (a
+// single-GPU build never needs libnccl; with torch in the process its
+// bundled libnccl.so.2 is the one found)
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+  void load() {
+    if (h) return;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names)
+      if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL)) != nullptr) break;
+    if (!h) throw Error(MCG_ERR_CUDA, std::string("nccl: cannot load libnccl.so.2: ") + dlerror());
+    auto sym = [&](const char* n) {
+      void* f = dlsym(h, n);
+      if (!f) throw Error(MCG_ERR_CUDA, std::string("nccl: missing symbol ") + n);
+      return f;
+    };
+    get_unique_id = reinterpret_cast<decltype(get_unique_id)>(sym("ncclGetUniqueId"));
+    comm_init_rank = reinterpret_cast<decltype(comm_init_rank)>(sym("ncclCommInitRank"));
+    all_gather = reinterpret_cast<decltype(all_gather)>(sym("ncclAllGather"));
+    comm_destroy = reinterpret_cast<decltype(comm_destroy)>(sym("ncclCommDestroy"));
+    error_string = reinterpret_cast<decltype(error_string)>(sym("ncclGetErrorString"));
+  }
+  void check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) throw Error(MCG_ERR_CUDA, std::string("nccl: ") + what + ": " + error_string(r));
+  }
+};
+NcclApi& nccl_api() {
+  static NcclApi api;
+  api.load();
+  return api;
+}
+
+// the epoch's gathered spikes (every rank's send block) appended to the
+// global spike log as (s0, gid, step, t bits); the host orders each epoch by
+// (gid, step), Impl::exchange's order (engine.cpp:877-888)
+__global__ void k_collect_recv(const int64_t* recv, int32_t world, int64_t block, const int64_t* ctl,
+                               int64_t* glog, unsigned long long* glog_n, int64_t cap, int32_t* err) {
+  const int64_t s0 = ctl[0];
+  for (int r = 0; r < world; ++r) {
+    const int64_t* b = recv + r * block;
+    const int64_t n = b[0];
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const unsigned long long pos = atomicAdd(glog_n, 1ull);
+      if (static_cast<int64_t>(pos) >= cap) {
+        atomicOr(err, MCG_ERR_FLAG_SPIKES);
+        continue;
+      }
+      glog[4 * pos] = s0;
+      glog[4 * pos + 1] = b[1 + 3 * i];
+      glog[4 * pos + 2] = b[2 + 3 * i];
+      glog[4 * pos + 3] = b[3 + 3 * i];
+    }
+  }
+}
 
 struct Engine {
   HostModel m;
@@ -206,14 +269,39 @@ struct Engine {
   size_t bc_smem = 0;
   DBuf<int4> d_chunks;
   DBuf<unsigned long long> d_chunk_n;
+  // warp-group kernel (mcg_warp.cuh) for LIF networks with charge-type synapses
+  bool use_warp = false;
+  int32_t wg_G = 1, wg_groups = 1, wg_warps = 1, wg_grid = 1, wg_resident = 0, wg_P = 0, wg_MW = 1;
+  int32_t wg_ev_cap = 0, wg_warp_doubles = 0, wg_kind_doubles = 0, wg_specs_sm = 0, wg_lazy = 0;
+  size_t wg_smem = 0;
+  DBuf<int32_t> d_kb_off;
+  DBuf<uint32_t> d_stc_mask;
+  DBuf<int64_t> d_stc_t;
+  bool lazy_valid = false;  // active masks and calcium stamps match the state
+  bool lazy_dirty = false;  // resting synapses' calcium lags `step` (k_warp ran since the last flush)
   cudaEvent_t evk0 = nullptr, evk1 = nullptr;
   // MCG_PHASE_TIMING=1: per-phase cycle totals of the batch kernel, printed
   // to stderr after every advance_to (development instrumentation)
   bool phase_timing = std::getenv("MCG_PHASE_TIMING") != nullptr;
   DBuf<unsigned long long> d_phase;
 
-  void print_phases() {
+  void print_phases(int64_t call_steps = 0) {
     if (!phase_timing || !d_phase.p) return;
+    if (use_warp) {
+      unsigned long long ph[2 * MCG_WPH_N];
+      CK(cudaMemcpy(ph, d_phase.p, sizeof(ph), cudaMemcpyDeviceToHost));
+      const double warps = std::min<double>(wg_groups, double(wg_grid) * wg_warps);
+      std::fprintf(stderr, "k_warp phase us/step/warp (mean | max warp), steps=%lld warps=%.0f:",
+                   (long long)call_steps, warps);
+      static const char* nm[MCG_WPH_N] = {"epoch_in", "noise", "deliver", "stc", "trigger", "solve",
+                                          "detect_post", "probes", "epoch_out", "groups", "expand", "gsync"};
+      for (int i = 0; i < MCG_WPH_N; ++i)
+        std::fprintf(stderr, " %s %.3f|%.3f", nm[i], ph[i] / warps / 1965.0 / std::max<int64_t>(call_steps, 1),
+                     ph[MCG_WPH_N + i] / 1965.0 / std::max<int64_t>(call_steps, 1));
+      std::fprintf(stderr, "\n");
+      d_phase.zero(st);
+      return;
+    }
     unsigned long long ph[2 * MCG_NPHASE];
     CK(cudaMemcpy(ph, d_phase.p, sizeof(ph), cudaMemcpyDeviceToHost));
     std::fprintf(stderr, "phase cycles (sum over CTAs):");
@@ -250,6 +338,8 @@ struct Engine {
   McgDev dev{};
 
   ~Engine() {
+    if (nccl_comm) nccl_api().comm_destroy(static_cast<ncclComm_t>(nccl_comm));
+    if (h_ctl_ring) cudaFreeHost(h_ctl_ring);
     if (h_ctr) cudaFreeHost(h_ctr);
     if (h_err) cudaFreeHost(h_err);
     if (h_abort) cudaFreeHost(h_abort);
@@ -390,6 +480,178 @@ struct Engine {
   }
 
   int32_t n_local() const { return static_cast<int32_t>(m.cell_kind.size()); }
+
+  // k_warp (mcg_warp.cuh) runs networks whose every kind is a LIF cell small
+  // enough for shared memory, cable kinds with constant, chain-scheduled V and
+  // species systems, and at most one STC placement plus static-charge ones:
+  // every consolidation network.  Everything else runs on k_batch.
+  bool warp_eligible(std::string* why) const {
+    auto no = [&](const char* w) {
+      if (why) *why = w;
+      return false;
+    };
+    if (std::getenv("MCG_NO_WARP")) return no("MCG_NO_WARP");
+    const int nl = n_local();
+    if (nl == 0) return no("no local cells");
+    if (sp_max > 15) return no("more than 15 species");
+    std::vector<char> used(m.kinds.size(), 0);
+    for (int c = 0; c < nl; ++c) used[m.cell_kind[c]] = 1;
+    for (size_t ki = 0; ki < m.kinds.size(); ++ki) {
+      if (!used[ki]) continue;
+      const McgKind& K = m.kinds[ki];
+      if (K.n > smem_n || K.n > 0xffff) return no("kind too large for shared memory");
+      if (K.dyn == MCG_DYN_LIF_EXACT) {
+        if (K.n != 1) return no("exact LIF with several compartments");
+      } else if (K.dyn == MCG_DYN_LIF) {
+        if (!K.v_const) return no("LIF cable without a constant V system");
+        if (K.n > 1 && (K.ch_lp == 0 || (K.n_species > 0 && !K.sp_const)))
+          return no("cable kind without a chain schedule");
+      } else {
+        return no("membrane is not LIF");
+      }
+      if (K.n_groups > 8) return no("more than 8 placements");
+      int n_stc = 0;
+      for (int gi = 0; gi < K.n_groups; ++gi) {
+        const int kd = m.specs[K.spec0 + gi].kind;
+        if (kd == MCG_SYN_STC_CHARGE) ++n_stc;
+        else if (kd != MCG_SYN_STATIC_CHARGE) return no("synapse kind other than charge / STC");
+      }
+      if (n_stc > 1) return no("more than one STC placement");
+    }
+    for (int c = 0; c < nl; ++c) {
+      const McgKind& K = m.kinds[m.cell_kind[c]];
+      for (int gi = 0; gi < K.n_groups; ++gi) {
+        const McgCellGroup& G = m.cgs[m.cg_off[c] + gi];
+        if (m.specs[G.spec].kind != MCG_SYN_STC_CHARGE) continue;
+        if (G.size > 32 * MCG_MW_MAX) return no("more than 1024 STC synapses on a cell");
+        if (G.fifo < 0) return no("STC group without a delayed-calcium queue");
+      }
+    }
+    return true;
+  }
+
+  void setup_warp_kernel() {
+    use_warp = false;
+    std::string why;
+    if (!warp_eligible(&why)) {
+      if (std::getenv("MCG_VERBOSE")) std::fprintf(stderr, "engine: k_batch (%s)\n", why.c_str());
+      return;
+    }
+    const int nl = n_local();
+    int dev_sms = 148, smem_optin = 0;
+    CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    // kind blocks (mcg_kind_block_doubles), one per kind
+    std::vector<int32_t> kb(m.kinds.size(), -1);
+    int kd = 0, pmax = 0;
+    for (size_t ki = 0; ki < m.kinds.size(); ++ki) {
+      const McgKind& K = m.kinds[ki];
+      if (K.n > smem_n) continue;
+      kb[ki] = kd;
+      kd += mcg_kind_block_doubles(K.n, K.n_species, K.ch_lp);
+      if (K.ch_lp > 0) pmax = std::max(pmax, 2 * K.ch_lp + 1);
+    }
+    int stc_max = 0;
+    bool lazy = !std::getenv("MCG_NO_LAZY");
+    for (int c = 0; c < nl; ++c) {
+      const McgKind& K = m.kinds[m.cell_kind[c]];
+      for (int gi = 0; gi < K.n_groups; ++gi) {
+        const McgCellGroup& G = m.cgs[m.cg_off[c] + gi];
+        if (m.specs[G.spec].kind == MCG_SYN_STC_CHARGE) stc_max = std::max(stc_max, G.size);
+      }
+    }
+    // lazy calcium needs a resting calcium to stay below the thresholds and a
+    // late step that is a no-op at rest (mcg_warp.cuh)
+    for (const McgSpec& S : m.specs) {
+      if (S.kind != MCG_SYN_STC_CHARGE) continue;
+      if (!(S.theta_p >= 0.0 && S.theta_d >= 0.0 && S.cf >= 0.0 && S.cf <= 1.0 && S.theta_tag >= 0.0 &&
+            std::fabs(S.f_int) <= 1.7976931348623157e308))
+        lazy = false;
+    }
+    wg_lazy = lazy ? 1 : 0;
+    wg_kind_doubles = kd;
+    wg_P = pmax;
+    wg_MW = std::max(1, (stc_max + 31) / 32);
+    const int S = sp_max;
+    // every cell of a group has 2 (1 + S) system lanes (mcg_wg_epoch phase D)
+    const int g_max = std::max(1, std::min(MCG_WG_MAX, 32 / (2 * (1 + S))));
+    wg_G = g_max;
+    if (const char* gv = std::getenv("MCG_WARP_G")) wg_G = std::clamp(std::atoi(gv), 1, g_max);
+    wg_groups = (nl + wg_G - 1) / wg_G;
+    wg_specs_sm = m.specs.size() * sizeof(McgSpec) <= 16 * 1024 ? static_cast<int32_t>(m.specs.size()) : 0;
+    wg_ev_cap = 128;
+    if (const char* ev = std::getenv("MCG_WARP_EVCAP")) wg_ev_cap = std::max(0, std::atoi(ev));
+    wg_warp_doubles = mcg_warp_region_doubles(wg_G, smem_n, S, wg_P, wg_MW, wg_ev_cap);
+    const size_t fixed = size_t(wg_kind_doubles) * 8 + ((m.kinds.size() * sizeof(McgKind) + 7) / 8) * 8 +
+                        ((size_t(wg_specs_sm) * sizeof(McgSpec) + 7) / 8) * 8;
+    const size_t lim = size_t(smem_optin) - 2048;
+    if (fixed + size_t(wg_warp_doubles) * 8 > lim) {
+      if (std::getenv("MCG_VERBOSE")) std::fprintf(stderr, "engine: k_batch (warp region too large)\n");
+      return;
+    }
+    const int max_warps = static_cast<int>(std::min<size_t>(8, (lim - fixed) / (size_t(wg_warp_doubles) * 8)));
+    // resident when every group has its own warp: spread over the SMs
+    if (wg_groups <= dev_sms * max_warps) {
+      wg_resident = 1;
+      wg_grid = std::min(dev_sms, wg_groups);
+      wg_warps = (wg_groups + wg_grid - 1) / wg_grid;
+    } else {
+      wg_resident = 0;
+      wg_grid = dev_sms;
+      wg_warps = max_warps;
+    }
+    // test hooks: fewer warps / CTAs (forces per-epoch group staging on small nets)
+    if (const char* wv = std::getenv("MCG_WARP_WARPS")) wg_warps = std::clamp(std::atoi(wv), 1, max_warps);
+    if (const char* gv = std::getenv("MCG_WARP_GRID")) wg_grid = std::clamp(std::atoi(gv), 1, dev_sms);
+    wg_resident = wg_groups <= wg_grid * wg_warps ? 1 : 0;
+    wg_smem = fixed + size_t(wg_warps) * wg_warp_doubles * 8 + 64;
+    CK(cudaFuncSetAttribute(k_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wg_smem)));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_warp, wg_warps * 32, wg_smem));
+    if (occ < 1) {
+      if (std::getenv("MCG_VERBOSE")) std::fprintf(stderr, "engine: k_batch (k_warp does not fit)\n");
+      return;
+    }
+    wg_grid = std::min(wg_grid, occ * dev_sms);
+    if (wg_resident && wg_groups > wg_grid * wg_warps) wg_resident = 0;
+    d_kb_off.upload(kb, st);
+    d_stc_mask.alloc(size_t(std::max(nl, 1)) * wg_MW);
+    d_stc_mask.zero(st);
+    d_stc_t.alloc(std::max<size_t>(m.i_stc_h.size(), 1));
+    d_chunks.alloc(size_t(kBatch) * std::max(bc_batches, wg_groups) + 1);
+    use_warp = true;
+    lazy_valid = false;
+    lazy_dirty = false;
+    if (std::getenv("MCG_VERBOSE"))
+      std::fprintf(stderr, "engine: k_warp G=%d groups=%d grid=%d warps=%d resident=%d P=%d MW=%d lazy=%d smem=%zu\n",
+                   wg_G, wg_groups, wg_grid, wg_warps, wg_resident, wg_P, wg_MW, wg_lazy, wg_smem);
+  }
+
+  // lazy calcium (mcg_warp.cuh): masks and stamps from the current state
+  void lazy_init() {
+    if (!use_warp || lazy_valid) return;
+    const int nl = n_local();
+    refresh_dev();
+    const int dbg = std::getenv("MCG_WARP_DBG") ? std::atoi(std::getenv("MCG_WARP_DBG")) : 0;
+    k_lazy_init<<<(nl * 32 + 255) / 256, 256, 0, st>>>(dev, d_stc_mask.p, d_stc_t.p, wg_MW,
+                                                        (wg_lazy && (dbg & 4)) ? 2 : wg_lazy, step);
+    CK(cudaGetLastError());
+    stats.kernel_launches += 1;
+    lazy_valid = true;
+    lazy_dirty = false;
+  }
+  // every resting synapse's calcium brought to `step` (before the host reads
+  // or rewrites STC state)
+  void ensure_flushed() {
+    if (!use_warp || !lazy_dirty) return;
+    const int nl = n_local();
+    refresh_dev();
+    k_lazy_flush<<<(nl * 32 + 255) / 256, 256, 0, st>>>(dev, d_stc_mask.p, d_stc_t.p, wg_MW, step);
+    CK(cudaGetLastError());
+    stats.kernel_launches += 1;
+    lazy_dirty = false;
+    lazy_valid = false;  // stamps are stale now; the next advance re-derives them
+  }
 
   void init(const mcg_recipe& r, const mcg_options& opt) {
     device = opt.device;
@@ -595,6 +857,7 @@ struct Engine {
     stats.species_comps = m.species_comps;
     const auto t2 = std::chrono::steady_clock::now();
     setup_batch_kernel();
+    setup_warp_kernel();
     refresh_dev();
     if (std::getenv("MCG_PROFILE_BUILD")) {
       const auto t3 = std::chrono::steady_clock::now();
@@ -809,11 +1072,32 @@ struct Engine {
     std::sort(ch.begin(), ch.end(), [](const int4& a, const int4& b) {
       return a.x != b.x ? a.x < b.x : a.y < b.y;
     });
-    for (const int4& q : ch)
-      for (int i = 0; i < q.w; ++i) {
-        spk_t.push_back(lt[q.z + i]);
-        spk_gid.push_back(lg[q.z + i]);
+    if (use_warp) {
+      // k_warp's groups hold strided gids: within an epoch, order by gid (a
+      // cell's spikes are contiguous and in step order, so a stable sort)
+      size_t a = 0;
+      std::vector<int64_t> idx;
+      while (a < ch.size()) {
+        size_t b = a;
+        idx.clear();
+        while (b < ch.size() && ch[b].x == ch[a].x) {
+          for (int i = 0; i < ch[b].w; ++i) idx.push_back(ch[b].z + i);
+          ++b;
+        }
+        std::stable_sort(idx.begin(), idx.end(), [&](int64_t u, int64_t v) { return lg[u] < lg[v]; });
+        for (int64_t q : idx) {
+          spk_t.push_back(lt[q]);
+          spk_gid.push_back(lg[q]);
+        }
+        a = b;
       }
+    } else {
+      for (const int4& q : ch)
+        for (int i = 0; i < q.w; ++i) {
+          spk_t.push_back(lt[q.z + i]);
+          spk_gid.push_back(lg[q.z + i]);
+        }
+    }
   }
 
   // one persistent launch: up to kBatch epochs from `step` towards `target`
@@ -825,15 +1109,175 @@ struct Engine {
 
   int64_t shard_spike_cap() const { return int64_t(std::max(n_local(), 1)) * sp_cap; }
 
-  void run_batch(int64_t target, int64_t call_first) {
-    h_ctl[0] = step;
-    h_ctl[1] = target;
-    h_ctl[2] = L;
-    h_ctl[3] = call_first;
-    CK(cudaMemcpyAsync(d_ctl.p, h_ctl, 4 * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  // ---- the exchange inside the library (mcg_shard_init_nccl) --------------
+  void* nccl_comm = nullptr;
+  DBuf<int64_t> d_xs, d_xr;          // this rank's send block, all ranks' blocks
+  DBuf<int64_t> d_ctl_ring;          // epoch control of each launch of a batch
+  int64_t* h_ctl_ring = nullptr;
+  DBuf<int64_t> d_glog;              // gathered spikes of a batch: (s0, gid, step, t bits)
+  DBuf<unsigned long long> d_glog_n;
+  std::vector<double> gspk_t;        // the global spike list (every rank's spikes)
+  std::vector<uint32_t> gspk_gid;
+  bool async_ok = false;             // inboxes sized so that no expansion can overflow
+
+  // inbox capacities that no epoch can exceed: per destination, every in-edge
+  // delivers at most sp_cap (cell edges) or L (source edges: one event per
+  // step) events per epoch, and an event waits at most ceil(delay / L) + 1
+  // epochs in the pending list; false (and nothing changed) above the budget
+  bool size_inboxes_for_worst_case(size_t budget_bytes) {
+    const int nl = n_local();
+    std::vector<int64_t> inc(std::max(nl, 1), 0), pend(std::max(nl, 1), 0);
+    for (size_t r = 0; r < m.e_dst.size(); ++r) {
+      const int c = m.e_dst[r];
+      if (c < 0) continue;
+      const int64_t per = (m.e_src[r] == 0xFFFFFFFFu) ? L : sp_cap;
+      const int64_t d = m.e_delay[r];
+      inc[c] += per;
+      pend[c] += per * ((d + L - 1) / L + 1);
+    }
+    const int64_t mi = *std::max_element(inc.begin(), inc.end());
+    const int64_t mp = *std::max_element(pend.begin(), pend.end());
+    int64_t ic = 32, pc = 64;
+    while (ic < mi + 1) ic <<= 1;
+    while (pc < mp + 1) pc <<= 1;
+    if (ic > (int64_t(1) << 24) || pc > (int64_t(1) << 24)) return false;
+    const size_t bytes = size_t(std::max(nl, 1)) * size_t(ic + 2 * pc) * 8;
+    if (bytes > budget_bytes) return false;
+    if (ic > inc_cap || pc > pend_cap) {
+      // move the pending keys into the larger buffers (as grow_inboxes)
+      while (pend_cap < pc || inc_cap < ic) {
+        if (inc_cap < ic && pend_cap < pc) grow_inboxes();
+        else if (inc_cap < ic) {
+          inc_cap *= 2;
+          d_inc.alloc(static_cast<size_t>(std::max(nl, 1)) * inc_cap);
+          d_inc_n.zero(st);
+        } else {
+          const int32_t keep = inc_cap;
+          grow_inboxes();
+          inc_cap = keep;
+          d_inc.alloc(static_cast<size_t>(std::max(nl, 1)) * inc_cap);
+          d_inc_n.zero(st);
+        }
+      }
+    }
+    return true;
+  }
+
+  void init_nccl(const uint8_t* id) {
+    if (m.world < 1) throw Error(MCG_ERR_ARGUMENT, "nccl: world < 1");
+    NcclApi& api = nccl_api();
+    CK(cudaSetDevice(device));
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    ncclComm_t comm = nullptr;
+    api.check(api.comm_init_rank(&comm, m.world, uid, m.rank), "ncclCommInitRank");
+    nccl_comm = comm;
+    // a common block capacity: every rank's shard_spike_cap is below
+    // n_cells_global * sp_cap, and sp_cap depends only on the kinds and L
+    const int64_t cap = int64_t(std::max(m.n_cells_global, 1)) * sp_cap;
+    const int64_t block = 1 + 3 * cap;
+    d_xs.alloc(size_t(block));
+    d_xs.zero(st);
+    d_xr.alloc(size_t(block) * m.world);
+    d_xr.zero(st);
+    x_send = d_xs.p;
+    x_recv = d_xr.p;
+    x_cap = cap;
+    x_world = m.world;
+    d_ctl_ring.alloc(4 * kBatch);
+    if (!h_ctl_ring) CK(cudaMallocHost(&h_ctl_ring, 4 * kBatch * sizeof(int64_t)));
+    d_glog.alloc(size_t(4) * kBatch * size_t(std::max(m.n_cells_global, 1)) * sp_cap);
+    d_glog_n.alloc(1);
+    d_glog_n.zero(st);
+    async_ok = size_inboxes_for_worst_case(size_t(16) << 30) && !std::getenv("MCG_SHARD_SYNC");
+    refresh_dev();
+    CK(cudaStreamSynchronize(st));
+  }
+
+  // the gathered spikes of the batch, epoch by epoch in (gid, step) order
+  void drain_glog() {
+    unsigned long long n = 0;
+    CK(cudaMemcpyAsync(&n, d_glog_n.p, sizeof(n), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (n == 0) return;
+    std::vector<int64_t> g(4 * n);
+    CK(cudaMemcpyAsync(g.data(), d_glog.p, g.size() * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemsetAsync(d_glog_n.p, 0, sizeof(unsigned long long), st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<int64_t> idx(n);
+    for (size_t i = 0; i < n; ++i) idx[i] = int64_t(i);
+    std::sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) {
+      for (int k = 0; k < 3; ++k)
+        if (g[4 * a + k] != g[4 * b + k]) return g[4 * a + k] < g[4 * b + k];
+      return false;
+    });
+    for (int64_t i : idx) {
+      double t;
+      std::memcpy(&t, &g[4 * i + 3], 8);
+      gspk_t.push_back(t);
+      gspk_gid.push_back(static_cast<uint32_t>(g[4 * i + 1]));
+    }
+  }
+
+  // sharded advance with the exchange on the engine's stream: per epoch one
+  // stepping launch, ncclAllGather of the spike blocks, the gathered spikes
+  // appended to the global log; the host waits once per batch of kBatch
+  // epochs (or per epoch when the inboxes could overflow)
+  void shard_advance(double t_ms) {
+    if (!nccl_comm) throw Error(MCG_ERR_ENGINE, "sharded engine: mcg_shard_init_nccl first");
+    invalidate_mirror();
+    const int64_t target = ceil_steps(t_ms, m.dt);
+    if (step >= target) return;
+    const int64_t a = step;
+    probes_begin(a, target, false, 0);
+    lazy_init();
+    refresh_dev();
+    NcclApi& api = nccl_api();
+    const int64_t block = 1 + 3 * x_cap;
+    CK(cudaEventRecord(eva, st));
+    while (step < target) {
+      const int64_t n_ep = async_ok ? std::min<int64_t>(kBatch, (target - step + L - 1) / L) : 1;
+      int64_t s = step;
+      for (int64_t e = 0; e < n_ep; ++e) {
+        int64_t* hc = h_ctl_ring + 4 * e;
+        hc[0] = s;
+        hc[1] = target;
+        hc[2] = L;
+        hc[3] = a;
+        s = std::min<int64_t>(s + L, target);
+      }
+      CK(cudaMemcpyAsync(d_ctl_ring.p, h_ctl_ring, 4 * n_ep * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+      for (int64_t e = 0; e < n_ep; ++e) {
+        launch_epoch_kernel(1, d_ctl_ring.p + 4 * e);
+        api.check(api.all_gather(x_send, x_recv, size_t(block), ncclInt64,
+                                 static_cast<ncclComm_t>(nccl_comm), st), "ncclAllGather");
+        k_collect_recv<<<1, 256, 0, st>>>(x_recv, x_world, block, d_ctl_ring.p + 4 * e, d_glog.p,
+                                          d_glog_n.p, int64_t(d_glog.n / 4), d_err.p);
+        stats.kernel_launches += 2;
+      }
+      sync_counters_raw();
+      if (*h_abort) throw Error(MCG_ERR_ENGINE, "sharded engine: inbox overflow");
+      stats.epochs += n_ep;
+      stats.epoch_kernel_launches += n_ep;
+      stats.steps += s - step;
+      drain_chunks();
+      drain_glog();
+      step = s;
+      check_err();
+    }
+    CK(cudaEventRecord(evb, st));
+    CK(cudaEventSynchronize(evb));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, eva, evb));
+    stats.advance_ms += ms;
+    stats.advance_calls += 1;
+    probes_end(a, target, false, 0, 1);
+  }
+
+  // one launch of the stepping kernel (k_warp or k_batch) over `planned`
+  // epochs described by the device control block `ctl`
+  void launch_epoch_kernel(int64_t planned, const int64_t* ctl) {
     const bool sharded = x_send != nullptr;
-    // sharded: one epoch per launch, the exchange happens between launches
-    const int64_t planned = sharded ? 1 : std::min<int64_t>(kBatch, (target - step + L - 1) / L);
     refresh_dev();
     McgBatchArgs A{};
     A.E = ev_dev();
@@ -846,6 +1290,55 @@ struct Engine {
       A.x_cap = x_cap;
     }
     A.n_epochs = static_cast<int32_t>(planned);
+    A.E.ctl = ctl;
+    McgDev Dv = dev;
+    Dv.ctl = ctl;
+    int64_t max_len = L;
+    if (use_warp) {
+      McgWarpArgs W{};
+      W.E = A.E;
+      W.n_epochs = A.n_epochs;
+      W.G = wg_G;
+      W.n_groups = wg_groups;
+      W.resident = wg_resident;
+      W.m = smem_n;
+      W.S = sp_max;
+      W.P = wg_P;
+      W.MW = wg_MW;
+      W.cell_doubles = (2 + sp_max) * smem_n;
+      W.ev_cap = wg_ev_cap;
+      W.warp_doubles = wg_warp_doubles;
+      W.kind_doubles = wg_kind_doubles;
+      W.n_kinds = static_cast<int32_t>(m.kinds.size());
+      W.n_specs_sm = wg_specs_sm;
+      W.lazy = wg_lazy;
+      W.cu_every = static_cast<int32_t>(std::max<int64_t>(1, 48 / std::max<int64_t>(L, 1)));
+      if (phase_timing) {
+        if (!d_phase.p) {
+          d_phase.alloc(size_t(2 + std::max(bc_grid, wg_grid)) * MCG_NPHASE);
+          d_phase.zero(st);
+        }
+        W.phase = d_phase.p;
+      }
+      W.dbg = std::getenv("MCG_WARP_DBG") ? std::atoi(std::getenv("MCG_WARP_DBG")) : 0;
+      W.dbg_s = std::getenv("MCG_WARP_DBG_S") ? std::atoll(std::getenv("MCG_WARP_DBG_S")) : 30;
+      W.kb_off = d_kb_off.p;
+      W.stc_mask = d_stc_mask.p;
+      W.stc_t = d_stc_t.p;
+      W.log_t = d_log_t.p;
+      W.log_gid = d_log_gid.p;
+      W.log_n = d_ctr.p + C_LOG;
+      W.chunks = d_chunks.p;
+      W.chunk_n = d_chunk_n.p;
+      W.x_send = A.x_send;
+      W.x_cap = A.x_cap;
+      void* wargs[] = {&Dv, &W, &max_len};
+      CK(cudaEventRecord(evk0, st));
+      CK(cudaFuncSetAttribute(k_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wg_smem)));
+      CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_warp), wg_grid, wg_warps * 32, wargs,
+                                     wg_smem, st));
+      if (wg_lazy) lazy_dirty = true;
+    } else {
     A.cells_per_cta = bc_cells;
     A.n_batches = bc_batches;
     A.comp_stride = bc_stride;
@@ -872,8 +1365,8 @@ struct Engine {
     A.log_n = d_ctr.p + C_LOG;
     A.chunks = d_chunks.p;
     A.chunk_n = d_chunk_n.p;
-    McgDev Dv = dev;
-    int64_t max_len = L;
+    A.dbg = std::getenv("MCG_WARP_DBG") ? std::atoi(std::getenv("MCG_WARP_DBG")) : 0;
+    A.dbg_s = std::getenv("MCG_WARP_DBG_S") ? std::atoll(std::getenv("MCG_WARP_DBG_S")) : 30;
     void* args[] = {&Dv, &A, &max_len};
     CK(cudaEventRecord(evk0, st));
     // the kernel attributes are process-global and another engine in this
@@ -883,6 +1376,19 @@ struct Engine {
     CK(cudaFuncSetAttribute(k_batch, cudaFuncAttributePreferredSharedMemoryCarveout, bc_carve));
     CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_batch), bc_grid, kBatchThreads, args,
                                    bc_smem, st));
+    }
+  }
+
+  void run_batch(int64_t target, int64_t call_first) {
+    h_ctl[0] = step;
+    h_ctl[1] = target;
+    h_ctl[2] = L;
+    h_ctl[3] = call_first;
+    CK(cudaMemcpyAsync(d_ctl.p, h_ctl, 4 * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    const bool sharded = x_send != nullptr;
+    // sharded: one epoch per launch, the exchange happens between launches
+    const int64_t planned = sharded ? 1 : std::min<int64_t>(kBatch, (target - step + L - 1) / L);
+    launch_epoch_kernel(planned, d_ctl.p);
     CK(cudaEventRecord(evk1, st));
     sync_counters_raw();
     const int32_t ab = *h_abort;
@@ -969,6 +1475,7 @@ struct Engine {
     if (step >= target) return;
     const int64_t a = step, b = std::min<int64_t>(target, step + L);
     probes_begin(a, b, false, 0);
+    lazy_init();
     refresh_dev();
     CK(cudaEventRecord(eva, st));
     while (step < b) run_batch(b, a);
@@ -989,6 +1496,7 @@ struct Engine {
     if (step >= target) return;
     const int64_t a = step;
     probes_begin(a, target, false, 0);
+    lazy_init();
     refresh_dev();
     CK(cudaEventRecord(eva, st));
     while (step < target) run_batch(target, a);
@@ -998,7 +1506,7 @@ struct Engine {
     CK(cudaEventElapsedTime(&ms, eva, evb));
     stats.advance_ms += ms;
     stats.advance_calls += 1;
-    print_phases();
+    print_phases(target - a);
     probes_end(a, target, false, 0, 1);
   }
 
@@ -1016,6 +1524,8 @@ struct Engine {
     const int64_t target = ceil_steps(t_ms, dt);
     if ((target - step) % per != 0)
       throw Error(MCG_ERR_ENGINE, "fast-forward: span must be a multiple of coarse dt");
+    ensure_flushed();
+    lazy_valid = false;
     const int nl = n_local();
     const int nf = static_cast<int>(m.fifos.size());
     refresh_dev();
@@ -1161,6 +1671,8 @@ struct Engine {
   void state_io(int field, uint32_t gid, int index, int64_t off, int64_t count, void* out,
                 const void* in, bool write) {
     const int c = local_of(gid);
+    ensure_flushed();
+    if (write) lazy_valid = false;
     const McgKind& K = m.kinds[m.cell_kind[c]];
     const int64_t co = m.comp_off[c];
     auto comp_range = [&](int64_t lim) {
@@ -1239,6 +1751,7 @@ struct Engine {
   // seq order), which this engine expands only at the next epoch's start.
   std::vector<uint8_t> make_checkpoint() {
     if (m.world > 1) throw Error(MCG_ERR_ENGINE, "checkpoint: not supported for a sharded engine");
+    ensure_flushed();
     const int nl = n_local();
     const size_t nv = m.v.size(), nsp = m.species.size(), ni = m.i_comp.size();
     const auto v = download(d_v, nv), hm = download(d_hh_m, nv), hh = download(d_hh_h, nv),
@@ -1351,6 +1864,8 @@ struct Engine {
 
   // Checkpoint::deserialize + Engine::restore (engine.cpp:1095-1140, 1235-1325)
   void restore(const uint8_t* bytes, size_t size) {
+    ensure_flushed();  // a rejected checkpoint leaves the current state whole
+    lazy_valid = false;
     invalidate_mirror();
     if (m.world > 1) throw Error(MCG_ERR_ENGINE, "checkpoint: not supported for a sharded engine");
     const Ckpt ck = ck_deserialize(bytes, size);
@@ -1738,6 +2253,44 @@ mcg_status mcg_partition(const mcg_recipe* recipe, int32_t world, uint32_t* boun
 
 mcg_status mcg_shard_run_epoch(mcg_engine* eng, double t_ms) {
   return guarded([&] { eng->e.run_epoch(t_ms); });
+}
+
+mcg_status mcg_nccl_unique_id(uint8_t* id) {
+  return guarded([&] {
+    if (!id) throw mcg::Error(MCG_ERR_ARGUMENT, "nccl: null id");
+    mcg::NcclApi& api = mcg::nccl_api();
+    ncclUniqueId uid;
+    api.check(api.get_unique_id(&uid), "ncclGetUniqueId");
+    std::memcpy(id, &uid, sizeof(uid));
+  });
+}
+
+mcg_status mcg_shard_init_nccl(mcg_engine* eng, const uint8_t* id) {
+  return guarded([&] {
+    if (!eng || !id) throw mcg::Error(MCG_ERR_ARGUMENT, "nccl: null pointer");
+    eng->e.init_nccl(id);
+  });
+}
+
+mcg_status mcg_shard_advance_to(mcg_engine* eng, double t_ms) {
+  return guarded([&] { eng->e.shard_advance(t_ms); });
+}
+
+int64_t mcg_shard_num_global_spikes(const mcg_engine* eng) {
+  return eng ? static_cast<int64_t>(eng->e.gspk_t.size()) : 0;
+}
+
+mcg_status mcg_shard_get_global_spikes(mcg_engine* eng, int64_t first, int64_t count, double* t_ms,
+                                       uint32_t* gid) {
+  return guarded([&] {
+    const mcg::Engine& E = eng->e;
+    if (first < 0 || count < 0 || first + count > static_cast<int64_t>(E.gspk_t.size()))
+      throw mcg::Error(MCG_ERR_ARGUMENT, "spike range out of bounds");
+    for (int64_t i = 0; i < count; ++i) {
+      if (t_ms) t_ms[i] = E.gspk_t[first + i];
+      if (gid) gid[i] = E.gspk_gid[first + i];
+    }
+  });
 }
 
 }  // extern "C"

@@ -74,7 +74,14 @@ __device__ __forceinline__ double mcg_chain_rinit(const McgChainLane& L, int nod
   return cap * x + rhs;
 }
 
-// all 32 lanes of the warp must call this (inactive lanes with on = 0)
+// all 32 lanes of the warp must call this (inactive lanes with on = 0).
+// Three passes over the lane's chain side, so that the two dependent chains
+// carry nothing but their own fp64 operations:
+//   1. r2 of every position, cap*x + rhs (independent: full ILP)
+//   2. elimination, leaf to top: r2[p] += f[c]*r2[c] along the chain
+//   3. the root, then substitution, top to leaf, with the reciprocal quotient
+// Each chain loop loads the next block's operands before the current block's
+// links, so the shared-memory latency stays off the chain.
 __device__ __forceinline__ void mcg_chain_lane(const McgChainLane& L) {
   double* S = mcg_smem;
   const int32_t* PI = reinterpret_cast<const int32_t*>(mcg_smem);
@@ -83,55 +90,76 @@ __device__ __forceinline__ void mcg_chain_lane(const McgChainLane& L) {
   const int p0 = L.side * L.lp;
   const int rb = L.r2c + p0, fb = L.fc + p0, cb = L.fc + P + p0, db = L.fc + 2 * P + p0,
             yb = L.fc + 3 * P + p0, ib = L.idx + p0;
-
-  // ---- elimination, leaf side first.  Block b's links run while block b + 4's
-  // r2 is formed from operands loaded one block ahead, whose node indices were
-  // loaded two blocks ahead
   const int capb = L.fc + 4 * P + p0, glb = L.fc + 5 * P + p0;
+  // the root's state, read before the root shuffle: side 0 stores the root's
+  // new value right after it, and the two lanes need not be converged there
+  const double x_root = L.on ? S[L.x] : 0.0;
+  const double rc_root = (L.on && L.rc >= 0) ? S[L.rc] : 0.0;
+
+  // ---- 1. r2 = cap*x + rhs (tree_solver.cpp:57); padding positions +0
+#pragma unroll 1
+  for (int b = 0; b < lp; b += 4) {
+    int nd[4];
+    double xv[4], rcv[4], cp[4], gl[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      nd[u] = PI[ib + b + u];
+      cp[u] = S[capb + b + u];
+      gl[u] = S[glb + b + u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = nd[u] >= 0 ? nd[u] : 0;  // padding reads node 0 and discards it
+      xv[u] = S[L.x + q];
+      rcv[u] = S[(L.rc >= 0 ? L.rc : L.x) + q];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double r = mcg_chain_rinit(L, nd[u], cp[u], gl[u], xv[u], rcv[u]);
+      S[rb + b + u] = nd[u] >= 0 ? r : 0.0;
+    }
+  }
+
+  // ---- 2. elimination, leaf side first: cur = final r2 of the last position,
+  // fp its f (the child's factor applied to its parent).  Two register blocks
+  // in turn: one is loaded while the other's links run.
   double cur = 0.0, fp = -0.0;
-  {
-    double r4[4], f4[4];
-    int i4[4];  // node indices of the block after the one r4 holds
-    auto load_idx = [&](int b, int* o) {
+  if (lp > 0) {
+    double rA[4], fA[4], rB[4], fB[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) o[u] = (b < lp) ? PI[ib + b + u] : -1;
-    };
-    auto form = [&](int b, const int* id, double* r, double* f) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int node = id[u];
-        const double x = node >= 0 ? S[L.x + node] : 0.0;
-        const double rc = (node >= 0 && L.rc >= 0) ? S[L.rc + node] : 0.0;
-        const double gl = L.v ? S[glb + b + u] : 0.0;
-        r[u] = mcg_chain_rinit(L, node, S[capb + b + u], gl, x, rc);
-        f[u] = S[fb + b + u];
-      }
-    };
-    if (lp > 0) {
-      int i0[4];
-      load_idx(0, i0);
-      load_idx(4, i4);
-      form(0, i0, r4, f4);
+    for (int u = 0; u < 4; ++u) {
+      rA[u] = S[rb + u];
+      fA[u] = S[fb + u];
     }
 #pragma unroll 1
-    for (int b = 0; b < lp; b += 4) {
-      int in[4];
-      load_idx(b + 8, in);
-      double rn[4], fn[4];
-      const int nb = (b + 4 < lp) ? b + 4 : b;  // the last block forms itself again (unused)
-      form(nb, i4, rn, fn);
+    for (int b = 0; b < lp; b += 8) {
+      const bool two = b + 4 < lp;
+      const int nb = two ? b + 4 : b;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const double r = r4[u] + fp * cur;
-        S[rb + b + u] = r;
-        cur = r;
-        fp = f4[u];
+        rB[u] = S[rb + nb + u];
+        fB[u] = S[fb + nb + u];
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        r4[u] = rn[u];
-        f4[u] = fn[u];
-        i4[u] = in[u];
+        const double r = rA[u] + fp * cur;
+        S[rb + b + u] = r;
+        cur = r;
+        fp = fA[u];
+      }
+      if (!two) break;
+      const int na = b + 8 < lp ? b + 8 : b;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        rA[u] = S[rb + na + u];
+        fA[u] = S[fb + na + u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double r = rB[u] + fp * cur;
+        S[rb + b + 4 + u] = r;
+        cur = r;
+        fp = fB[u];
       }
     }
   }
@@ -142,8 +170,7 @@ __device__ __forceinline__ void mcg_chain_lane(const McgChainLane& L) {
   double r0 = 0.0;
   if (L.on) {
     const int pr = L.fc + 2 * L.lp;  // root position
-    r0 = mcg_chain_rinit(L, 0, S[pr + 4 * P], L.v ? S[pr + 5 * P] : 0.0, S[L.x],
-                         L.rc >= 0 ? S[L.rc] : 0.0);
+    r0 = mcg_chain_rinit(L, 0, S[pr + 4 * P], L.v ? S[pr + 5 * P] : 0.0, x_root, rc_root);
   }
   if (L.a_first) {
     r0 = r0 + ta;
@@ -152,56 +179,46 @@ __device__ __forceinline__ void mcg_chain_lane(const McgChainLane& L) {
     r0 = r0 + tb;
     r0 = r0 + ta;
   }
-  // ---- substitution, top first
+  // ---- 3. substitution, top first
   unsigned bad = L.on ? mcg_div_bad(r0) : 0u;
   double xv = 0.0;
   if (L.on) {
     xv = mcg_qdiv(r0, S[L.fc + 2 * P + 2 * L.lp], S[L.fc + 3 * P + 2 * L.lp]);
     if (L.side == 0) S[L.x] = xv;
   }
-  {
-    // blocks of two positions (register budget), next block loaded ahead
-    double r2v[2], c2v[2], d2v[2], y2v[2];
-    int i2v[2];
-    if (lp > 0) {
-      const int b = lp - 2;
+  if (lp > 0) {
+    // two register blocks in turn, as the elimination
+    double rA[4], cA[4], dA[4], yA[4], rB[4], cB[4], dB[4], yB[4];
+    int iA[4], iB[4];
+    auto load = [&](int b, double* r, double* c, double* d, double* y, int* i) {
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        r2v[u] = S[rb + b + u];
-        c2v[u] = S[cb + b + u];
-        d2v[u] = S[db + b + u];
-        y2v[u] = S[yb + b + u];
-        i2v[u] = PI[ib + b + u];
+      for (int u = 0; u < 4; ++u) {
+        r[u] = S[rb + b + u];
+        c[u] = S[cb + b + u];
+        d[u] = S[db + b + u];
+        y[u] = S[yb + b + u];
+        i[u] = PI[ib + b + u];
       }
-    }
-#pragma unroll 1
-    for (int b = lp - 2; b >= 0; b -= 2) {
-      double rn[2], cn[2], dn[2], yn[2];
-      int in[2];
-      const int nb = b >= 2 ? b - 2 : b;
+    };
+    auto links = [&](const double* r, const double* c, const double* d, const double* y,
+                     const int* i) {
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        rn[u] = S[rb + nb + u];
-        cn[u] = S[cb + nb + u];
-        dn[u] = S[db + nb + u];
-        yn[u] = S[yb + nb + u];
-        in[u] = PI[ib + nb + u];
-      }
-#pragma unroll
-      for (int u = 1; u >= 0; --u) {
-        const double num = r2v[u] + c2v[u] * xv;
+      for (int u = 3; u >= 0; --u) {
+        const double num = r[u] + c[u] * xv;
         bad |= mcg_div_bad(num);
-        xv = mcg_qdiv(num, d2v[u], y2v[u]);
-        if (i2v[u] >= 0) S[L.x + i2v[u]] = xv;
+        xv = mcg_qdiv(num, d[u], y[u]);
+        if (i[u] >= 0) S[L.x + i[u]] = xv;
       }
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        r2v[u] = rn[u];
-        c2v[u] = cn[u];
-        d2v[u] = dn[u];
-        y2v[u] = yn[u];
-        i2v[u] = in[u];
-      }
+    };
+    load(lp - 4, rA, cA, dA, yA, iA);
+#pragma unroll 1
+    for (int b = lp - 4; b >= 0; b -= 8) {
+      const bool two = b >= 4;
+      load(two ? b - 4 : b, rB, cB, dB, yB, iB);
+      links(rA, cA, dA, yA, iA);
+      if (!two) break;
+      load(b >= 8 ? b - 8 : b, rA, cA, dA, yA, iA);
+      links(rB, cB, dB, yB, iB);
     }
   }
   bad |= __shfl_xor_sync(0xffffffffu, bad, 1);

@@ -359,3 +359,27 @@ class Engine:
 
     def run_epoch(self, t_ms: float):
         _check(A.lib().mcg_shard_run_epoch(self._h, float(t_ms)))
+
+    # ---- the exchange inside the library (NCCL on the engine's stream) ----
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _check(A.lib().mcg_nccl_unique_id(buf))
+        return bytes(buf)
+
+    def init_nccl(self, uid: bytes):
+        buf = (C.c_uint8 * 128).from_buffer_copy(bytes(uid)[:128].ljust(128, b"\0"))
+        _check(A.lib().mcg_shard_init_nccl(self._h, buf))
+
+    def shard_advance_to(self, t_ms: float):
+        _check(A.lib().mcg_shard_advance_to(self._h, float(t_ms)))
+
+    def global_spike_arrays(self) -> Tuple[np.ndarray, np.ndarray]:
+        """Every rank's spikes (the reference's (epoch, gid, step) order)."""
+        n = int(A.lib().mcg_shard_num_global_spikes(self._h))
+        t = np.empty(n, np.float64)
+        g = np.empty(n, np.uint32)
+        if n:
+            _check(A.lib().mcg_shard_get_global_spikes(self._h, 0, n, t.ctypes.data_as(C.c_void_p),
+                                                       g.ctypes.data_as(C.c_void_p)))
+        return t, g
