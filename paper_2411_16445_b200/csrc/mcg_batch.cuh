@@ -60,6 +60,7 @@ struct McgBatchArgs {
   unsigned long long* chunk_n;
   int64_t* x_send;         // sharded: this rank's spikes of the epoch [count, (gid, step, t) x cap]
   int64_t x_cap;
+  int32_t epoch_base;      // added to the launch's epoch index in the log chunks
   int32_t dbg;             // development trace (MCG_WARP_DBG: (cell + 1) << 8)
   int64_t dbg_s;
 };
@@ -1842,7 +1843,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
     if (tot > 0) {
       const unsigned long long off = atomicAdd(A.log_n, static_cast<unsigned long long>(tot));
       const unsigned long long ci = atomicAdd(A.chunk_n, 1ull);
-      A.chunks[ci] = make_int4(j, b, static_cast<int>(off), tot);
+      A.chunks[ci] = make_int4(A.epoch_base + j, b, static_cast<int>(off), tot);
       s_log_off = static_cast<int>(off);
     }
   }

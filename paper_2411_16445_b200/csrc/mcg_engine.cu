@@ -1248,7 +1248,7 @@ struct Engine {
       }
       CK(cudaMemcpyAsync(d_ctl_ring.p, h_ctl_ring, 4 * n_ep * sizeof(int64_t), cudaMemcpyHostToDevice, st));
       for (int64_t e = 0; e < n_ep; ++e) {
-        launch_epoch_kernel(1, d_ctl_ring.p + 4 * e);
+        launch_epoch_kernel(1, d_ctl_ring.p + 4 * e, static_cast<int32_t>(e));
         api.check(api.all_gather(x_send, x_recv, size_t(block), ncclInt64,
                                  static_cast<ncclComm_t>(nccl_comm), st), "ncclAllGather");
         k_collect_recv<<<1, 256, 0, st>>>(x_recv, x_world, block, d_ctl_ring.p + 4 * e, d_glog.p,
@@ -1276,7 +1276,7 @@ struct Engine {
 
   // one launch of the stepping kernel (k_warp or k_batch) over `planned`
   // epochs described by the device control block `ctl`
-  void launch_epoch_kernel(int64_t planned, const int64_t* ctl) {
+  void launch_epoch_kernel(int64_t planned, const int64_t* ctl, int32_t epoch_base = 0) {
     const bool sharded = x_send != nullptr;
     refresh_dev();
     McgBatchArgs A{};
@@ -1332,6 +1332,7 @@ struct Engine {
       W.chunk_n = d_chunk_n.p;
       W.x_send = A.x_send;
       W.x_cap = A.x_cap;
+      W.epoch_base = epoch_base;
       void* wargs[] = {&Dv, &W, &max_len};
       CK(cudaEventRecord(evk0, st));
       CK(cudaFuncSetAttribute(k_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wg_smem)));
@@ -1365,6 +1366,7 @@ struct Engine {
     A.log_n = d_ctr.p + C_LOG;
     A.chunks = d_chunks.p;
     A.chunk_n = d_chunk_n.p;
+    A.epoch_base = epoch_base;
     A.dbg = std::getenv("MCG_WARP_DBG") ? std::atoi(std::getenv("MCG_WARP_DBG")) : 0;
     A.dbg_s = std::getenv("MCG_WARP_DBG_S") ? std::atoll(std::getenv("MCG_WARP_DBG_S")) : 30;
     void* args[] = {&Dv, &A, &max_len};

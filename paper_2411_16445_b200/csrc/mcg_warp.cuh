@@ -83,6 +83,7 @@ struct McgWarpArgs {
   unsigned long long* chunk_n;
   int64_t* x_send;       // sharded export (as McgBatchArgs)
   int64_t x_cap;
+  int32_t epoch_base;    // added to the launch's epoch index in the log chunks
 };
 
 // one staged network event of the epoch (the pending list's head, with the
@@ -971,7 +972,7 @@ __device__ void mcg_wg_epoch(const McgDev& D, const McgWarpArgs& A, const McgWar
     if (lane == 0) {
       off = static_cast<int>(atomicAdd(A.log_n, static_cast<unsigned long long>(tot)));
       const unsigned long long ci = atomicAdd(A.chunk_n, 1ull);
-      A.chunks[ci] = make_int4(j, g, off, tot);
+      A.chunks[ci] = make_int4(A.epoch_base + j, g, off, tot);
     }
     off = __shfl_sync(MCG_FULL, off, 0);
   }
