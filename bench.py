@@ -13,7 +13,8 @@ spontaneous phase and the onset of the 100 Hz learning stimulus at 10 s).
   e2e     same metric through the public API with host buffers: engine
           construction from the host recipe (H2D), advance over the W+K steps,
           spikes and final STC weights back to the host (D2H), wall-clocked
-  roofline  the persistent batch kernel (k_batch, one launch = up to 32
+  roofline  the persistent stepping kernel the engine picked (k_warp for the
+          consolidation networks, else k_batch; one launch = up to 32
           min-delay epochs): algorithmic bytes per launch (SURVEY §8(d) B_step
           x fine steps per launch) / mean launch duration (CUDA events on the
           engine's stream around each launch)
@@ -151,11 +152,18 @@ def measured_peak_hbm():
         return 6650.0, "fallback"
 
 
-def traffic_per_launch(steps_per_launch):
-    """DRAM bytes (read + write) of one k_batch launch from the committed ncu
-    capture (profiles/batch_kernel_dram.json), scaled to the mean launch's
-    fine steps so it is per launch like `achieved`."""
-    p = os.path.join(ROOT, "profiles", "batch_kernel_dram.json")
+KERNELS = {0: "k_batch", 1: "k_warp", 2: "k_point"}
+
+
+def stepping_kernel(st):
+    return KERNELS.get(int(st.get("stepping_kernel", 0)), "k_batch")
+
+
+def traffic_per_launch(steps_per_launch, kernel="k_batch"):
+    """DRAM bytes (read + write) of one launch of the stepping kernel from the
+    committed ncu capture (profiles/<kernel>_dram.json), scaled to the mean
+    launch's fine steps so it is per launch like `achieved`."""
+    p = os.path.join(ROOT, "profiles", f"{kernel}_dram.json")
     try:
         with open(p) as f:
             d = json.load(f)
@@ -483,8 +491,8 @@ def run_gpu_arm(args):
         "config": config_block(world),
         "compartment_updates_per_s": 50000 * fine_steps / total,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic_per_launch(steps_per_launch),
-                     "kernel": "k_batch", "peak_kind": peak_kind,
+                     "frac": achieved / peak, "traffic": traffic_per_launch(steps_per_launch, stepping_kernel(s1)),
+                     "kernel": stepping_kernel(s1), "peak_kind": peak_kind,
                      "bytes_per_launch": per_launch_bytes, "mean_launch_ms": mean_launch_s * 1e3,
                      "steps_per_launch": steps_per_launch, "bytes_per_fine_step": bstep},
         "cpu_baseline": cpu,
@@ -494,7 +502,7 @@ def run_gpu_arm(args):
                 "parts": e2e_parts[int(np.argmin(e2e_times))]},
         "gpu_launches": int(launches),
         "clocks": clk,
-        "batch_kernel_share": kern_ms * 1e-3 / total,
+        "stepping_kernel_share": kern_ms * 1e-3 / total,
         "wall_ms_per_step": 1e3 * wall_total / args.steps,
         "other_configs": other,
     }
@@ -593,7 +601,7 @@ def run_gpu_arm_sharded(args, world, rank):
             "compartment_updates_per_s": 50000 * fine_steps / total,
             "exchange": backend,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "kernel": "k_batch (rank 0)",
+                         "frac": achieved / peak, "traffic": None, "kernel": stepping_kernel(s1) + " (rank 0)",
                          "peak_kind": peak_kind, "bytes_per_launch": bstep * steps_per_launch,
                          "mean_launch_ms": mean_launch_s * 1e3,
                          "steps_per_launch": steps_per_launch},

@@ -311,6 +311,8 @@ typedef struct {
   int64_t species_comps;      /* sum over cells of species x compartments     */
   double advance_ms;          /* CUDA-event time of advance_to calls (engine stream) */
   int64_t advance_calls;
+  int32_t stepping_kernel;    /* 0: k_batch, 1: k_warp, 2: k_point (mcg_engine.cu) */
+  int32_t reserved;
 } mcg_stats;
 mcg_status mcg_get_stats(mcg_engine* eng, mcg_stats* out);
 /* enable/disable CUDA-event timing of the epoch kernel (adds one event pair per epoch) */

@@ -111,7 +111,8 @@ class mcg_stats(C.Structure):
                 ("epoch_kernel_launches", C.c_int64), ("total_comps", C.c_int64),
                 ("total_synapses", C.c_int64), ("stc_synapses", C.c_int64),
                 ("hh_comps", C.c_int64), ("species_comps", C.c_int64),
-                ("advance_ms", C.c_double), ("advance_calls", C.c_int64)]
+                ("advance_ms", C.c_double), ("advance_calls", C.c_int64),
+                ("stepping_kernel", C.c_int32), ("reserved", C.c_int32)]
 
 
 class mcg_gb_params(C.Structure):

@@ -2215,6 +2215,7 @@ mcg_status mcg_get_stats(mcg_engine* eng, mcg_stats* out) {
   return guarded([&] {
     eng->e.sync_counters_raw();
     eng->e.stats.events_delivered = static_cast<int64_t>(eng->e.h_ctr[mcg::C_DELIVERED]);
+    eng->e.stats.stepping_kernel = eng->e.use_warp ? 1 : 0;
     *out = eng->e.stats;
   });
 }
