@@ -476,7 +476,6 @@ __device__ void mcg_wg_epoch(const McgDev& D, const McgWarpArgs& A, const McgWar
   McgWCell* R = reinterpret_cast<McgWCell*>(mcg_smem + W.rec);
   uint32_t* MK = reinterpret_cast<uint32_t*>(mcg_smem + W.mask);
   McgWEv* EV = reinterpret_cast<McgWEv*>(mcg_smem + W.ev);
-  int32_t* IC = reinterpret_cast<int32_t*>(mcg_smem + W.ic);
   double* S_ = mcg_smem;
   const int G = A.G, m = A.m, S1 = 1 + A.S;
   const bool mine = lane < G && R[lane].c >= 0;
@@ -759,23 +758,30 @@ __device__ void mcg_wg_epoch(const McgDev& D, const McgWarpArgs& A, const McgWar
               }
             }
           }
-          S_[W.db + lane] = delta;
-          IC[lane] = changed ? kslot : -1;
+          // an unchanged item contributes -0.0, the identity of fp64 addition
+          // (x + -0.0 == x for every x, signed zeros and NaN included)
+          S_[W.db + lane] = changed ? delta : -0.0;
           const unsigned chg = __ballot_sync(MCG_FULL, changed);
-          __syncwarp();
           // SPS fold of this round's changed items, cell by cell in instance
-          // order (engine.cpp:634-641)
-          if (chg && mine && R[lane].sps_off >= 0) {
-            double acc = S_[R[lane].sps_off];
-            bool any = false;
-            for (unsigned b = chg; b; b &= b - 1) {
-              const int l = __ffs(b) - 1;
-              if (IC[l] == lane) {
-                acc += S_[W.db + l];
-                any = true;
-              }
+          // order (engine.cpp:634-641).  The round's items are cell-major, so
+          // cell slot k's are one lane range: its lane adds the deltas from
+          // its first to its last changed item, unconditionally (independent
+          // loads, one dependent add per item)
+          unsigned myl = 0;
+          if (chg) {
+            for (int k = 0; k < G; ++k) {
+              const unsigned b = __ballot_sync(MCG_FULL, changed && kslot == k);
+              if (lane == k) myl = b;
             }
-            if (any) S_[R[lane].sps_off] = acc;
+          }
+          __syncwarp();
+          if (myl && R[lane].sps_off >= 0) {
+            const int la = __ffs(myl) - 1, lb = 32 - __clz(myl);
+            double acc = S_[R[lane].sps_off];
+            const double* db = S_ + W.db;
+#pragma unroll 4
+            for (int l = la; l < lb; ++l) acc += db[l];
+            S_[R[lane].sps_off] = acc;
           }
           __syncwarp();
         }
