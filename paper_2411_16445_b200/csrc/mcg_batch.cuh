@@ -72,60 +72,70 @@ __device__ void mcg_expand(const McgEv& E, const McgDev& D, int32_t j, int64_t s
   const int64_t nthr = int64_t(gridDim.x) * blockDim.x;
   const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
-  // one warp per (source, step) task, lanes over the source's out-edges;
-  // consecutive tasks on different CTAs (a burst of one source's edges is
-  // spread over the grid instead of a few threads of CTA 0)
+  // Poisson windows: one warp per (window, step) task, lanes over the
+  // source's out-edges; consecutive tasks on different CTAs (a burst of one
+  // source's edges is spread over the grid instead of a few threads of CTA 0).
+  // Windows that miss the epoch are skipped whole.
   const int64_t nw = nthr >> 5;
   const int64_t gw = int64_t(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
-  const int64_t ntask = int64_t(E.n_tasks) * max_len;
+  (void)max_len;
+  const int64_t ntask = int64_t(E.n_poisson) * len;
   for (int64_t t = gw; t < ntask; t += nw) {
     int64_t q, off;
-    if (((static_cast<uint64_t>(t) | static_cast<uint64_t>(max_len)) >> 32) == 0) {
-      const uint32_t q32 = static_cast<uint32_t>(t) / static_cast<uint32_t>(max_len);
+    if (((static_cast<uint64_t>(t) | static_cast<uint64_t>(len)) >> 32) == 0) {
+      const uint32_t q32 = static_cast<uint32_t>(t) / static_cast<uint32_t>(len);
       q = q32;
-      off = static_cast<uint32_t>(t) - q32 * static_cast<uint32_t>(max_len);
+      off = static_cast<uint32_t>(t) - q32 * static_cast<uint32_t>(len);
     } else {
-      q = t / max_len;
-      off = t - q * max_len;
+      q = t / len;
+      off = t - q * len;
     }
-    if (off >= len) continue;
+    const McgSrcTask T = E.tasks[q];
+    const int64_t s = s0 + off;
+    if (s < T.a || s >= T.b) {
+      if (T.b <= s0 || T.a >= s1) {  // the window misses the epoch: this warp's
+        const int64_t nxt = (q + 1) * len;  // next task in the following window
+        t += ((nxt - t + nw - 1) / nw - 1) * nw;
+      }
+      continue;
+    }
+    const int64_t e0 = E.src_edge_off[T.source], e1 = E.src_edge_off[T.source + 1];
+    if (e1 == e0) continue;
+    int fire = 0;
+    if (lane == 0) {
+      const mcg_key key = mcg_make_key(E.seed, 0x100000000ull + uint64_t(T.source), 3, 0);
+      fire = mcg_uniform_for(&key, static_cast<uint64_t>(s)) < T.prob ? 1 : 0;
+    }
+    if (!__shfl_sync(MCG_FULL, fire, 0)) continue;
+    for (int64_t k = e0 + lane; k < e1; k += 32) {
+      const int64_t r = E.src_edges[k];
+      mcg_push(E, j, r, s + E.e_delay[r]);
+    }
+  }
+  // regular and scripted sources: one warp per source
+  for (int64_t q = E.n_poisson + gw; q < E.n_tasks; q += nw) {
     const McgSrcTask T = E.tasks[q];
     const int64_t e0 = E.src_edge_off[T.source], e1 = E.src_edge_off[T.source + 1];
     if (e1 == e0) continue;
-    if (T.type == MCG_SRC_POISSON) {
-      const int64_t s = s0 + off;
-      if (s < T.a || s >= T.b) continue;
-      int fire = 0;
-      if (lane == 0) {
-        const mcg_key key = mcg_make_key(E.seed, 0x100000000ull + uint64_t(T.source), 3, 0);
-        fire = mcg_uniform_for(&key, static_cast<uint64_t>(s)) < T.prob ? 1 : 0;
-      }
-      if (!__shfl_sync(MCG_FULL, fire, 0)) continue;
-      for (int64_t k = e0 + lane; k < e1; k += 32) {
-        const int64_t r = E.src_edges[k];
-        mcg_push(E, j, r, s + E.e_delay[r]);
-      }
-    } else if (off == 0) {
-      if (T.type == MCG_SRC_SCRIPTED) {
-        for (int64_t i = T.a; i < T.b; ++i) {
-          const int64_t st = E.scripted_steps[i];
-          if (st < s0 || st >= s1) continue;
-          for (int64_t k = e0 + lane; k < e1; k += 32) {
-            const int64_t r = E.src_edges[k];
-            mcg_push(E, j, r, st + E.e_delay[r]);
-          }
+    if (T.type == MCG_SRC_SCRIPTED) {
+      for (int64_t i = T.a; i < T.b; ++i) {
+        const int64_t st = E.scripted_steps[i];
+        if (st < s0 || st >= s1) continue;
+        for (int64_t k = e0 + lane; k < e1; k += 32) {
+          const int64_t r = E.src_edges[k];
+          mcg_push(E, j, r, st + E.e_delay[r]);
         }
-      } else if (T.r_period > 0) {
-        int64_t k0 = static_cast<int64_t>(ceil((double(s0) * E.dt - T.r_t0) / T.r_period - 1e-9));
-        if (k0 < 0) k0 = 0;
-        for (int64_t kk = k0; kk < T.r_count; ++kk) {
-          const int64_t st = static_cast<int64_t>(ceil((T.r_t0 + double(kk) * T.r_period) / E.dt - 1e-9));
-          if (st >= s1) break;
-          if (st < s0) continue;
-          for (int64_t k = e0 + lane; k < e1; k += 32) {
-            const int64_t r = E.src_edges[k];
-            mcg_push(E, j, r, st + E.e_delay[r]);
-          }
+      }
+    } else if (T.r_period > 0) {
+      int64_t k0 = static_cast<int64_t>(ceil((double(s0) * E.dt - T.r_t0) / T.r_period - 1e-9));
+      if (k0 < 0) k0 = 0;
+      for (int64_t kk = k0; kk < T.r_count; ++kk) {
+        const int64_t st = static_cast<int64_t>(ceil((T.r_t0 + double(kk) * T.r_period) / E.dt - 1e-9));
+        if (st >= s1) break;
+        if (st < s0) continue;
+        for (int64_t k = e0 + lane; k < e1; k += 32) {
+          const int64_t r = E.src_edges[k];
+          mcg_push(E, j, r, st + E.e_delay[r]);
         }
       }
     }

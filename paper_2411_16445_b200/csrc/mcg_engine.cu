@@ -27,6 +27,7 @@
 
 #include "mcg_batch.cuh"
 #include "mcg_warp.cuh"
+#include "mcg_point.cuh"
 #include "mcg_protocols.cuh"
 #include "mcg_checkpoint.h"
 #include "mcg_build.h"
@@ -223,7 +224,7 @@ struct Engine {
   // sources
   DBuf<McgSrcTask> d_tasks;
   DBuf<int64_t> d_scripted;
-  int32_t n_tasks = 0;
+  int32_t n_tasks = 0, n_poisson = 0;
   // inboxes
   DBuf<uint64_t> d_inc, d_pend;
   DBuf<int32_t> d_inc_n, d_pend_sel, d_pend_off, d_pend_n;
@@ -278,6 +279,10 @@ struct Engine {
   DBuf<uint32_t> d_stc_mask;
   DBuf<int64_t> d_stc_t;
   bool lazy_valid = false;  // active masks and calcium stamps match the state
+  // register-resident kernel for independent point cells (mcg_point.cuh)
+  bool use_point = false;
+  bool pt_small = false;  // every cell fits k_point<1, 2>
+  int32_t pt_grid = 1;
   bool lazy_dirty = false;  // resting synapses' calcium lags `step` (k_warp ran since the last flush)
   cudaEvent_t evk0 = nullptr, evk1 = nullptr;
   // MCG_PHASE_TIMING=1: per-phase cycle totals of the batch kernel, printed
@@ -627,6 +632,68 @@ struct Engine {
                    wg_G, wg_groups, wg_grid, wg_warps, wg_resident, wg_P, wg_MW, wg_lazy, wg_smem);
   }
 
+  // k_point (mcg_point.cuh) runs networks of exact-LIF point cells with
+  // charge-type synapses and no cell-to-cell connections (one epoch spans the
+  // whole call in the reference, engine.cpp:913-915): one thread carries a
+  // cell's state in registers through the epoch, one CTA per cell.
+  bool point_eligible(int dev_sms, std::string* why) const {
+    auto no = [&](const char* w) {
+      if (why) *why = w;
+      return false;
+    };
+    if (std::getenv("MCG_NO_POINT")) return no("MCG_NO_POINT");
+    if (m.world != 1) return no("sharded");
+    if (m.min_delay_steps > 0) return no("cell-to-cell connections");
+    if (L > MCG_PT_NB) return no("epoch longer than the noise buffer");
+    const int nl = n_local();
+    if (nl == 0 || nl > dev_sms) return no("cell count outside 1..#SMs");
+    for (int c = 0; c < nl; ++c) {
+      const McgKind& K = m.kinds[m.cell_kind[c]];
+      if (K.dyn != MCG_DYN_LIF_EXACT || K.n != 1) return no("not an exact-LIF point cell");
+      if (K.n_species > MCG_PT_SP) return no("too many species");
+      if (K.n_groups > 8) return no("more than 8 placements");
+      int n_stc = 0;
+      for (int gi = 0; gi < K.n_groups; ++gi) {
+        const McgCellGroup& G = m.cgs[m.cg_off[c] + gi];
+        const int kd = m.specs[G.spec].kind;
+        if (kd == MCG_SYN_STC_CHARGE) {
+          ++n_stc;
+          if (G.size > MCG_PT_STC) return no("too many STC synapses on a point cell");
+          if (G.size > 0 && G.fifo < 0) return no("STC group without a delayed-calcium queue");
+        } else if (kd != MCG_SYN_STATIC_CHARGE) {
+          return no("synapse kind other than charge / STC");
+        }
+      }
+      if (n_stc > 1) return no("more than one STC placement");
+    }
+    return true;
+  }
+
+  void setup_point_kernel() {
+    use_point = false;
+    int dev_sms = 148;
+    CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, device));
+    std::string why;
+    if (!point_eligible(dev_sms, &why)) {
+      if (std::getenv("MCG_VERBOSE")) std::fprintf(stderr, "engine: no k_point (%s)\n", why.c_str());
+      return;
+    }
+    pt_grid = n_local();
+    pt_small = true;
+    for (int c = 0; c < pt_grid; ++c) {
+      const McgKind& K = m.kinds[m.cell_kind[c]];
+      if (K.n_species > 2) pt_small = false;
+      for (int gi = 0; gi < K.n_groups; ++gi) {
+        const McgCellGroup& G = m.cgs[m.cg_off[c] + gi];
+        if (m.specs[G.spec].kind == MCG_SYN_STC_CHARGE && G.size > 1) pt_small = false;
+      }
+    }
+    d_chunks.alloc(size_t(kBatch) * std::max<int64_t>(std::max(bc_batches, wg_groups), pt_grid) + 1);
+    use_point = true;
+    use_warp = false;  // no lazy calcium: the synapses' calcium is stepped in registers
+    if (std::getenv("MCG_VERBOSE")) std::fprintf(stderr, "engine: k_point grid=%d L=%lld\n", pt_grid, (long long)L);
+  }
+
   // lazy calcium (mcg_warp.cuh): masks and stamps from the current state
   void lazy_init() {
     if (!use_warp || lazy_valid) return;
@@ -803,7 +870,14 @@ struct Engine {
         tasks.push_back(T);
       }
     }
+    // Poisson windows first (expanded per (window, step)), then the sources
+    // expanded once per epoch; the expansion's push order is irrelevant (the
+    // inbox sort orders the keys)
+    std::stable_partition(tasks.begin(), tasks.end(),
+                          [](const McgSrcTask& T) { return T.type == MCG_SRC_POISSON; });
     n_tasks = static_cast<int32_t>(tasks.size());
+    n_poisson = 0;
+    for (const McgSrcTask& T : tasks) n_poisson += T.type == MCG_SRC_POISSON ? 1 : 0;
     d_tasks.upload(tasks, st);
     d_scripted.upload(scripted, st);
 
@@ -858,6 +932,7 @@ struct Engine {
     const auto t2 = std::chrono::steady_clock::now();
     setup_batch_kernel();
     setup_warp_kernel();
+    setup_point_kernel();
     refresh_dev();
     if (std::getenv("MCG_PROFILE_BUILD")) {
       const auto t3 = std::chrono::steady_clock::now();
@@ -1006,6 +1081,7 @@ struct Engine {
     McgEv E{};
     E.tasks = d_tasks.p;
     E.n_tasks = n_tasks;
+    E.n_poisson = n_poisson;
     E.scripted_steps = d_scripted.p;
     E.src_edge_off = d_src_edge_off.p;
     E.src_edges = d_src_edges.p;
@@ -1294,7 +1370,22 @@ struct Engine {
     McgDev Dv = dev;
     Dv.ctl = ctl;
     int64_t max_len = L;
-    if (use_warp) {
+    if (use_point) {
+      McgPointArgs P{};
+      P.E = A.E;
+      P.n_epochs = A.n_epochs;
+      P.epoch_base = epoch_base;
+      P.log_t = d_log_t.p;
+      P.log_gid = d_log_gid.p;
+      P.log_n = d_ctr.p + C_LOG;
+      P.chunks = d_chunks.p;
+      P.chunk_n = d_chunk_n.p;
+      void* pargs[] = {&Dv, &P, &max_len};
+      CK(cudaEventRecord(evk0, st));
+      void* fn = pt_small ? reinterpret_cast<void*>(k_point<1, 2>)
+                          : reinterpret_cast<void*>(k_point<MCG_PT_STC, MCG_PT_SP>);
+      CK(cudaLaunchCooperativeKernel(fn, pt_grid, MCG_PT_THREADS, pargs, 0, st));
+    } else if (use_warp) {
       McgWarpArgs W{};
       W.E = A.E;
       W.n_epochs = A.n_epochs;
@@ -2215,7 +2306,7 @@ mcg_status mcg_get_stats(mcg_engine* eng, mcg_stats* out) {
   return guarded([&] {
     eng->e.sync_counters_raw();
     eng->e.stats.events_delivered = static_cast<int64_t>(eng->e.h_ctr[mcg::C_DELIVERED]);
-    eng->e.stats.stepping_kernel = eng->e.use_warp ? 1 : 0;
+    eng->e.stats.stepping_kernel = eng->e.use_point ? 2 : (eng->e.use_warp ? 1 : 0);
     *out = eng->e.stats;
   });
 }

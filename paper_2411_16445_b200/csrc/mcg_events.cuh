@@ -27,8 +27,9 @@ struct McgSrcTask {
 };
 
 struct McgEv {
-  const McgSrcTask* tasks;
+  const McgSrcTask* tasks;    // Poisson windows first, then regular / scripted sources
   int32_t n_tasks;
+  int32_t n_poisson;          // tasks [0, n_poisson) are Poisson windows
   const int64_t* scripted_steps;
   const int64_t* src_edge_off;
   const int64_t* src_edges;
