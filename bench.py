@@ -50,9 +50,26 @@ DATA_NOTE = "synthetic: build_consolidation_network(config 3, seed 1) recipe"
 UNIT = "sim-s/wall-s"
 
 
-def workload_config():
+def data_note(n_gpus=1):
+    if n_gpus <= 1:
+        return DATA_NOTE
+    nc, _, p = workload_size(n_gpus)
+    return f"synthetic: build_consolidation_network(N={nc}, p={p:g}, seed 1) recipe"
+
+
+def workload_size(n_gpus=1):
+    """Weak-scaling family of the consolidation network: 2000 N cells over N
+    GPUs with p = 0.1 / N, so every excitatory cell keeps config 3's in-degree
+    (160 recurrent STC synapses).  N = 1 is config 3 itself; N = 2 is the
+    north-star 4,000-neuron network; N = 50 would be config 5's cell count."""
+    n = max(1, int(n_gpus))
+    return N_CELLS * n, N_EXC * n, 0.1 / n
+
+
+def workload_config(n_gpus=1):
     from paper_2411_16445_b200 import network as N
-    return N.ConsolidationConfig(n_cells=N_CELLS, n_exc=N_EXC, seed=SEED, multi_compartment=True,
+    nc, ne, p = workload_size(n_gpus)
+    return N.ConsolidationConfig(n_cells=nc, n_exc=ne, p_conn=p, seed=SEED, multi_compartment=True,
                                  dt_ms=DT_MS)
 
 
@@ -62,10 +79,18 @@ L2_NOTE = ("GPU arm: a 256 MB buffer is written between timed steps (flushes the
 
 def config_block(n_gpus):
     """Identical in both arms (the driver compares them)."""
-    return {"workload": "config3: consolidation network N=2000 (1600 MC exc x 31 comps + 400 point inh), "
-                        "p=0.1, STC synapses, seed 1, dt 0.5 ms, 8h protocol, step = 500 ms bio",
-            "n_cells": N_CELLS, "compartments": 50000, "dt_ms": DT_MS, "step_bio_ms": STEP_MS,
-            "parallelism": f"cells sharded over {n_gpus} GPU(s)" if n_gpus > 1 else "single GPU",
+    if n_gpus <= 1:
+        return {"workload": "config3: consolidation network N=2000 (1600 MC exc x 31 comps + 400 point inh), "
+                            "p=0.1, STC synapses, seed 1, dt 0.5 ms, 8h protocol, step = 500 ms bio",
+                "n_cells": N_CELLS, "compartments": 50000, "dt_ms": DT_MS, "step_bio_ms": STEP_MS,
+                "parallelism": "single GPU", "l2": L2_NOTE}
+    nc, ne, p = workload_size(n_gpus)
+    return {"workload": f"config3 weak-scaled x{n_gpus}: consolidation network N={nc} ({ne} MC exc x 31 comps "
+                        f"+ {nc - ne} point inh), p={p:g} (config 3's in-degree), STC synapses, seed 1, "
+                        "dt 0.5 ms, 8h protocol, step = 500 ms bio",
+            "n_cells": nc, "compartments": 31 * ne + (nc - ne), "dt_ms": DT_MS, "step_bio_ms": STEP_MS,
+            "parallelism": f"cells sharded over {n_gpus} GPUs (contiguous gid ranges), spikes exchanged "
+                           "once per min-delay epoch by an allgather",
             "l2": L2_NOTE}
 
 
@@ -84,13 +109,14 @@ def host_facts():
     return {"cpu_model": model, "glibc": libc, "host_threads": os.cpu_count() or 1}
 
 
-def ref_workload_recipe():
+def ref_workload_recipe(n_gpus=1):
     """The workload's recipe from the REFERENCE's own builder
     (build_consolidation_network, network.cpp:426-598, in oracle/_ref): the
     reference arm never maps this repo's library."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import ref
-    cfg = ref.default_consolidation(n_cells=N_CELLS, n_exc=N_EXC, seed=SEED, multi_compartment=1,
+    nc, ne, p = workload_size(n_gpus)
+    cfg = ref.default_consolidation(n_cells=nc, n_exc=ne, p_conn=p, seed=SEED, multi_compartment=1,
                                     dt_ms=DT_MS)
     return ref.RefRecipe.consolidation(cfg, True)
 
@@ -214,7 +240,7 @@ def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    rr = ref_workload_recipe()
+    rr = ref_workload_recipe(args.gpus)
     import ref
     cores = os.cpu_count() or 1
     e = ref.RefEngine(rr.view, DT_MS, SEED, cores)
@@ -231,7 +257,7 @@ def run_reference_arm(args):
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": DATA_NOTE,
+            "vs_baseline": None, "dtype": "f64", "data": data_note(args.gpus),
             "config": config_block(args.gpus),
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "reference",
                              "sample": f"steps {args.warmup}..{args.warmup + args.steps} of 500 ms bio, "
@@ -511,56 +537,71 @@ def run_gpu_arm(args):
 
 
 def run_gpu_arm_sharded(args, world, rank):
-    """N > 1: cells of the same config-3 network partitioned over the ranks
-    (strong scaling), one min-delay epoch per launch, spikes exchanged by an
-    allgather after every epoch (paper_2411_16445_b200/shard.py).  Timed with
-    CUDA events around the whole step loop (exchange included), max over ranks."""
+    """N > 1: the weak-scaling family (workload_size: 2000 N cells, config 3's
+    in-degree) partitioned over the ranks, one process per GPU.  The exchange
+    runs inside libmcg (mcg_shard_init_nccl + mcg_shard_advance_to): per
+    min-delay epoch one stepping launch and one ncclAllGather of the spike
+    blocks on the engine's stream, the host waiting once per 32 epochs
+    (engine.cpp:913-942 is the reference's epoch/exchange contract).  Timed
+    with the engine's CUDA events around each advance (exchange included),
+    max over ranks.  MCG_EXCHANGE=gloo runs the host-staged ShardedEngine
+    instead (several ranks sharing one GPU; wall-clocked)."""
     import torch
     import torch.distributed as dist
-    from paper_2411_16445_b200 import EngineOptions
+    from paper_2411_16445_b200 import Engine, EngineOptions
     from paper_2411_16445_b200 import network as N
     from paper_2411_16445_b200 import shard
 
     local = int(os.environ.get("LOCAL_RANK", rank))
-    # MCG_EXCHANGE=gloo: host-staged exchange (lets several ranks share one GPU
-    # to exercise this path); default NCCL between the GPUs' device buffers
     backend = os.environ.get("MCG_EXCHANGE", "nccl")
     n_dev = torch.cuda.device_count()
     device = local % max(n_dev, 1)
     torch.cuda.set_device(device)
     dist.init_process_group(backend, rank=rank, world_size=world)
-    b = N.build_consolidation_network(workload_config(), True, device=device)
+    coll_dev = "cuda" if backend == "nccl" else "cpu"
+    b = N.build_consolidation_network(workload_config(world), True, device=device)
     flat = b.recipe.flatten()
     opt = EngineOptions(DT_MS, SEED)
 
     def make():
-        return shard.ShardedEngine(flat, opt, rank, world, device=device, backend=backend)
+        if backend == "nccl":
+            e = Engine(flat, opt, device=device, rank=rank, world=world)
+            uid = torch.zeros(128, dtype=torch.uint8, device=coll_dev)
+            if rank == 0:
+                uid.copy_(torch.tensor(list(Engine.nccl_unique_id()), dtype=torch.uint8))
+            dist.broadcast(uid, 0)
+            e.init_nccl(bytes(uid.cpu().tolist()))
+            return e, e.shard_advance_to, e.global_spike_arrays
+        sh = shard.ShardedEngine(flat, opt, rank, world, device=device, backend=backend,
+                                 record_spikes=True)
+        return sh.engine, sh.advance_to, sh.spike_arrays
 
-    sh = make()
-    sh.engine.set_timing(True)
+    eng, adv, spikes = make()
+    eng.set_timing(True)
     t = 0.0
     for _ in range(args.warmup):
         t += STEP_MS
-        sh.advance_to(t)
+        adv(t)
     flush_l2()
-    s0 = sh.engine.stats()
+    s0 = eng.stats()
     clocks = ClockSampler(device) if rank == 0 else None
     if clocks:
         clocks.start()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dist.barrier()
     torch.cuda.synchronize()
-    ev0.record()
+    w0 = time.perf_counter()
     for _ in range(args.steps):
         t += STEP_MS
-        sh.advance_to(t)
-    ev1.record()
+        adv(t)
     torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
     dist.barrier()
     clk = clocks.stop() if clocks else None
-    s1 = sh.engine.stats()
-    el = torch.tensor([ev0.elapsed_time(ev1) * 1e-3], dtype=torch.float64,
-                      device="cuda" if backend == "nccl" else "cpu")
+    s1 = eng.stats()
+    # device time: the engine's CUDA events around every advance call (the
+    # in-library path); the gloo path stages through the host: wall clock
+    dev_s = (s1["advance_ms"] - s0["advance_ms"]) * 1e-3 if backend == "nccl" else wall
+    el = torch.tensor([dev_s], dtype=torch.float64, device=coll_dev)
     dist.all_reduce(el, op=dist.ReduceOp.MAX)
     total = float(el.item())
     value = args.steps * STEP_MS * 1e-3 / total
@@ -572,39 +613,42 @@ def run_gpu_arm_sharded(args, world, rank):
     steps_per_launch = fine_steps / max(n_launch, 1)
     mean_launch_s = kern_ms * 1e-3 / max(n_launch, 1)
     peak, peak_kind = measured_peak_hbm()
-    achieved = bstep * steps_per_launch / mean_launch_s / 1e9
+    achieved = bstep * steps_per_launch / max(mean_launch_s, 1e-12) / 1e9
+    comps = torch.tensor([float(s1["total_comps"])], dtype=torch.float64, device=coll_dev)
+    dist.all_reduce(comps)
+    eng.close()
     # end to end through the public API: shard construction + W+K steps + spikes back
     torch.cuda.synchronize()
     dist.barrier()
     a = time.perf_counter()
-    sh2 = make()
+    eng2, adv2, spikes2 = make()
     tt = 0.0
     for _ in range(args.warmup + args.steps):
         tt += STEP_MS
-        sh2.advance_to(tt)
-    st, sg = sh2.engine.spike_arrays()
-    e2e_wall = torch.tensor([time.perf_counter() - a], dtype=torch.float64,
-                            device="cuda" if backend == "nccl" else "cpu")
+        adv2(tt)
+    st_, sg_ = spikes2()
+    e2e_wall = torch.tensor([time.perf_counter() - a], dtype=torch.float64, device=coll_dev)
     dist.all_reduce(e2e_wall, op=dist.ReduceOp.MAX)
     nsteps_e2e = args.warmup + args.steps
     e2e_val = nsteps_e2e * STEP_MS * 1e-3 / float(e2e_wall.item())
     v = flat.view
     h2d = v.n_connections * (1 + 4 + 4 + 4 + 1 + 8 + 8) + s1["total_synapses"] * 8 * 12 + s1["total_comps"] * 8 * 5
-    d2h = st.nbytes + sg.nbytes
+    d2h = st_.nbytes + sg_.nbytes
+    eng2.close()
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": DATA_NOTE,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": data_note(world),
             "config": config_block(world),
-            "compartment_updates_per_s": 50000 * fine_steps / total,
-            "exchange": backend,
+            "compartment_updates_per_s": float(comps.item()) * fine_steps / total,
+            "exchange": "ncclAllGather in libmcg" if backend == "nccl" else backend + " (host-staged)",
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "kernel": stepping_kernel(s1) + " (rank 0)",
-                         "peak_kind": peak_kind, "bytes_per_launch": bstep * steps_per_launch,
-                         "mean_launch_ms": mean_launch_s * 1e3,
-                         "steps_per_launch": steps_per_launch},
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": stepping_kernel(s1) + " (rank 0)", "peak_kind": peak_kind,
+                         "bytes_per_launch": bstep * steps_per_launch,
+                         "mean_launch_ms": mean_launch_s * 1e3, "steps_per_launch": steps_per_launch},
             "cpu_baseline": None,
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d / nsteps_e2e),
                     "d2h_bytes_per_step": int(d2h / nsteps_e2e)},

@@ -271,6 +271,9 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
   partition(r, m.world, bounds);
   m.gid_begin = bounds[m.rank];
   m.gid_end = bounds[m.rank + 1];
+  m.max_shard_cells = 0;  // every rank's cell count is known from the partition
+  for (int q = 0; q < m.world; ++q)
+    m.max_shard_cells = std::max<int32_t>(m.max_shard_cells, static_cast<int32_t>(bounds[q + 1] - bounds[q]));
 
   // ---- kinds (build_kind, engine.cpp:189-278) ----
   const int nk = r.n_kinds;

@@ -54,6 +54,7 @@ struct HostModel {
   uint64_t seed = 0;
   int32_t rank = 0, world = 1;
   int32_t n_cells_global = 0;
+  int32_t max_shard_cells = 0;  // largest shard of the partition (spike block capacity)
   uint32_t gid_begin = 0, gid_end = 0;  // local shard [begin, end)
   int64_t min_delay_steps = -1;
 

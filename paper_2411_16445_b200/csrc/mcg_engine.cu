@@ -1248,9 +1248,10 @@ struct Engine {
     ncclComm_t comm = nullptr;
     api.check(api.comm_init_rank(&comm, m.world, uid, m.rank), "ncclCommInitRank");
     nccl_comm = comm;
-    // a common block capacity: every rank's shard_spike_cap is below
-    // n_cells_global * sp_cap, and sp_cap depends only on the kinds and L
-    const int64_t cap = int64_t(std::max(m.n_cells_global, 1)) * sp_cap;
+    // a common block capacity: every rank's spikes per epoch are at most its
+    // cell count times sp_cap, sp_cap depends only on the kinds and L, and the
+    // partition (hence the largest shard) is the same on every rank
+    const int64_t cap = int64_t(std::max(m.max_shard_cells, 1)) * sp_cap;
     const int64_t block = 1 + 3 * cap;
     d_xs.alloc(size_t(block));
     d_xs.zero(st);
