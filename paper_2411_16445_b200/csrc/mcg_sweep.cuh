@@ -63,6 +63,11 @@ struct McgChainLane {
   int rc;        // V: rhs_current by node (-1: no current this step)
   int pc;        // species: synthesis compartment (-1: no production)
   double prod;   // species: production at pc
+  // register mode (mcg_chain_lane<false>): the only nonzero rhs_current of a
+  // step is at node rc_node (-2: no current), value rc_val = 0.0 + I (the
+  // zero-filled buffer plus the one current, engine.cpp:575/662)
+  int rc_node;
+  double rc_val;
 };
 
 // r2 of a position before elimination, cap*x + rhs (tree_solver.cpp:57), with
@@ -74,6 +79,15 @@ __device__ __forceinline__ double mcg_chain_rinit(const McgChainLane& L, int nod
   return cap * x + rhs;
 }
 
+// register mode: rc is the node's rhs_current (0.0 off the current's node);
+// gl + 0.0 + 0.0 == gl + 0.0 for every gl, so the V right-hand side is the
+// reference's whether or not the step has a current
+__device__ __forceinline__ double mcg_chain_rinit_reg(const McgChainLane& L, int node, double cap,
+                                                      double gl, double x, double rc) {
+  const double rhs = L.v ? (gl + 0.0 + rc) : (node == L.pc ? L.prod : 0.0);
+  return cap * x + rhs;
+}
+
 // all 32 lanes of the warp must call this (inactive lanes with on = 0).
 // Three passes over the lane's chain side, so that the two dependent chains
 // carry nothing but their own fp64 operations:
@@ -82,6 +96,7 @@ __device__ __forceinline__ double mcg_chain_rinit(const McgChainLane& L, int nod
 //   3. the root, then substitution, top to leaf, with the reciprocal quotient
 // Each chain loop loads the next block's operands before the current block's
 // links, so the shared-memory latency stays off the chain.
+template <bool kRcBuf = true>
 __device__ __forceinline__ void mcg_chain_lane(const McgChainLane& L) {
   double* S = mcg_smem;
   const int32_t* PI = reinterpret_cast<const int32_t*>(mcg_smem);
@@ -94,7 +109,7 @@ __device__ __forceinline__ void mcg_chain_lane(const McgChainLane& L) {
   // the root's state, read before the root shuffle: side 0 stores the root's
   // new value right after it, and the two lanes need not be converged there
   const double x_root = L.on ? S[L.x] : 0.0;
-  const double rc_root = (L.on && L.rc >= 0) ? S[L.rc] : 0.0;
+  const double rc_root = kRcBuf ? ((L.on && L.rc >= 0) ? S[L.rc] : 0.0) : (L.rc_node == 0 ? L.rc_val : 0.0);
 
   // ---- 1. r2 = cap*x + rhs (tree_solver.cpp:57); padding positions +0
 #pragma unroll 1
@@ -111,11 +126,12 @@ __device__ __forceinline__ void mcg_chain_lane(const McgChainLane& L) {
     for (int u = 0; u < 4; ++u) {
       const int q = nd[u] >= 0 ? nd[u] : 0;  // padding reads node 0 and discards it
       xv[u] = S[L.x + q];
-      rcv[u] = S[(L.rc >= 0 ? L.rc : L.x) + q];
+      rcv[u] = kRcBuf ? S[(L.rc >= 0 ? L.rc : L.x) + q] : (nd[u] == L.rc_node ? L.rc_val : 0.0);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const double r = mcg_chain_rinit(L, nd[u], cp[u], gl[u], xv[u], rcv[u]);
+      const double r = kRcBuf ? mcg_chain_rinit(L, nd[u], cp[u], gl[u], xv[u], rcv[u])
+                              : mcg_chain_rinit_reg(L, nd[u], cp[u], gl[u], xv[u], rcv[u]);
       S[rb + b + u] = nd[u] >= 0 ? r : 0.0;
     }
   }
@@ -170,7 +186,8 @@ __device__ __forceinline__ void mcg_chain_lane(const McgChainLane& L) {
   double r0 = 0.0;
   if (L.on) {
     const int pr = L.fc + 2 * L.lp;  // root position
-    r0 = mcg_chain_rinit(L, 0, S[pr + 4 * P], L.v ? S[pr + 5 * P] : 0.0, x_root, rc_root);
+    r0 = kRcBuf ? mcg_chain_rinit(L, 0, S[pr + 4 * P], L.v ? S[pr + 5 * P] : 0.0, x_root, rc_root)
+                : mcg_chain_rinit_reg(L, 0, S[pr + 4 * P], L.v ? S[pr + 5 * P] : 0.0, x_root, rc_root);
   }
   if (L.a_first) {
     r0 = r0 + ta;

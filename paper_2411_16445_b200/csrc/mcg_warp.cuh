@@ -110,6 +110,7 @@ struct McgWCell {
   double vol, rvol, cf;  // of the STC placement's compartment
   double h0, cpre_s, cpost_s, ccf;  // STC spec fields on the delivery / post chains
   double prod;
+  double rc_val;         // rhs_current at noise_comp this step (0.0 + I_bg); others are 0.0
   double sp_den, sp_rden;  // n == 1 species closed form: cap + gs, its reciprocal (per lane)
   int32_t c;             // local cell index (-1: empty slot)
   int32_t kind;
@@ -549,6 +550,33 @@ __device__ void mcg_wg_epoch(const McgDev& D, const McgWarpArgs& A, const McgWar
       sp_rden = __drcp_rn(sp_den);
     }
   }
+  // this lane's chain-sweep descriptor (mcg_sweep.cuh), static through the
+  // epoch; the step fills in on / current / production
+  McgChainLane Lst{};
+  Lst.rc_node = -2;
+  int lane_noise = -2, lane_prp = -1, lane_prp_comp = -1;
+  if (sys_lane && sys < S1) {
+    const McgWCell& X = R[sys_k];
+    const McgKind& K = kinds[X.kind];
+    const bool ok = K.ch_lp > 0 && (sys == 0 ? (K.dyn == MCG_DYN_LIF && K.v_const)
+                                             : (sys - 1 < K.n_species && K.n > 1 && K.sp_const));
+    if (ok) {
+      const int n = K.n, Pk = 2 * K.ch_lp + 1;
+      const int cho = A.kb_off[X.kind] + mcg_kind_chain_off(n, K.n_species);
+      Lst.side = side;
+      Lst.lp = K.ch_lp;
+      Lst.r2c = W.r2c + sys_k * S1 * A.P + sys * A.P;
+      Lst.idx = 2 * cho;
+      Lst.fc = cho + (Pk + 1) / 2 + sys * 6 * Pk;
+      Lst.x = X.base + (sys == 0 ? 0 : m + (sys - 1) * n);
+      Lst.a_first = K.ch_afirst;
+      Lst.v = sys == 0;
+      Lst.rc = -1;
+      lane_noise = K.noise_comp;
+      lane_prp = K.prp_idx;
+      lane_prp_comp = K.prp_comp;
+    }
+  }
   __syncwarp();
   WPH(0);
 
@@ -577,11 +605,9 @@ __device__ void mcg_wg_epoch(const McgDev& D, const McgWarpArgs& A, const McgWar
         if (n0 + 1 < w1) S_[W.nb + k * 32 + int(n0 + 1 - s)] = z1;
       }
     }
-    // rhs_current = 0 for every compartment (engine.cpp:575)
-    for (int idx = lane; idx < G * m; idx += 32) {
-      const int k = idx / m, i = idx - k * m;
-      S_[W.cells + k * A.cell_doubles + (1 + A.S) * m + i] = 0.0;
-    }
+    // rhs_current (engine.cpp:575): k_warp's kinds carry no current synapse,
+    // so the buffer is zero but for the background current at noise_comp,
+    // kept in a register (McgWCell::rc_val, McgChainLane::rc_node / rc_val)
     __syncwarp();
     WPH(1);
     // ---- A. delivery (engine.cpp:549-560): the inbox in (step, src, seq)
@@ -592,6 +618,7 @@ __device__ void mcg_wg_epoch(const McgDev& D, const McgWarpArgs& A, const McgWar
       const bool refractory = X.lif && s < X.refr;
       X.refractory = refractory;
       X.has_current = 0;
+      X.rc_val = 0.0;
       double* V = S_ + X.base;
       auto stc_event = [&](uint32_t inst, double w, uint32_t src) {
         // apply_event, stc_charge etype 0 (engine.cpp:497-510)
@@ -802,7 +829,7 @@ __device__ void mcg_wg_epoch(const McgDev& D, const McgWarpArgs& A, const McgWar
       if (X.lif && K.has_bg && !bg_gated) {
         double ib = K.i_bg;
         if (K.sig_bg != 0.0) ib += K.sig_bg * S_[W.nb + lane * 32 + int(so & 31)];
-        S_[X.base + (1 + A.S) * m + K.noise_comp] += ib;
+        X.rc_val = 0.0 + ib;  // the zero-filled rhs_current plus ib
         X.has_current = 1;
       }
     }
@@ -810,38 +837,26 @@ __device__ void mcg_wg_epoch(const McgDev& D, const McgWarpArgs& A, const McgWar
     WPH(4);
     // ---- D. membrane and species systems: (cell, system, chain side) lanes
     {
-      McgChainLane L{};
+      McgChainLane L = Lst;  // static part (epoch entry)
       int kind = -1;
-      if (sys_lane && sys < S1) {
+      if (Lst.lp > 0) {
         const McgWCell& X = R[sys_k];
         kind = X.kind;
-        const McgKind& K = kinds[kind];
-        const bool ok = K.ch_lp > 0 && (sys == 0 ? (K.dyn == MCG_DYN_LIF && K.v_const)
-                                                 : (sys - 1 < K.n_species && K.n > 1 && K.sp_const));
-        if (ok) {
-          const int n = K.n, Pk = 2 * K.ch_lp + 1;
-          const int cho = A.kb_off[kind] + mcg_kind_chain_off(n, K.n_species);
-          L.on = (sys != 0 || !X.refractory) ? 1 : 0;
-          L.side = side;
-          L.lp = K.ch_lp;
-          L.r2c = W.r2c + sys_k * S1 * A.P + sys * A.P;
-          L.idx = 2 * cho;
-          L.fc = cho + (Pk + 1) / 2 + sys * 6 * Pk;
-          L.x = X.base + (sys == 0 ? 0 : m + (sys - 1) * n);
-          L.a_first = K.ch_afirst;
-          L.v = sys == 0;
-          L.rc = (sys == 0 && X.has_current) ? X.base + (1 + A.S) * m : -1;
-          L.pc = (sys > 0 && sys - 1 == K.prp_idx && X.prod != 0.0) ? K.prp_comp : -1;
-          L.prod = X.prod;
-        }
+        L.on = (sys != 0 || !X.refractory) ? 1 : 0;
+        L.rc_node = (sys == 0 && X.has_current) ? lane_noise : -2;
+        L.rc_val = X.rc_val;
+        L.pc = (sys > 0 && sys - 1 == lane_prp && X.prod != 0.0) ? lane_prp_comp : -1;
+        L.prod = X.prod;
+      } else if (sys_lane && sys < S1) {
+        kind = R[sys_k].kind;
       }
-      mcg_chain_lane(L);
+      mcg_chain_lane<false>(L);
       // single-compartment systems on their side-0 lanes
       if (sys_lane && sys < S1 && side == 0 && sys_n == 1) {
         const McgWCell& X = R[sys_k];
         const McgKind& K = kinds[kind];
         double* V = S_ + X.base;
-        const double rc0 = S_[X.base + (1 + A.S) * m];
+        const double rc0 = X.rc_val;  // rhs_current[0] (noise_comp == 0 for n == 1)
         if (sys == 0) {
           if (K.dyn == MCG_DYN_LIF_EXACT) {
             if (!X.refractory) {  // engine.cpp:667-673
@@ -866,7 +881,7 @@ __device__ void mcg_wg_epoch(const McgDev& D, const McgWarpArgs& A, const McgWar
     if (mine && (A.dbg >> 8) == R[lane].c + 1 && s >= A.dbg_s && s <= A.dbg_s + 5)
       printf("[k_warp] cell %d s %lld after solve V0 %.17g Vb %.17g hc %d rc %.17g\n", R[lane].c, (long long)s,
              S_[R[lane].base], S_[R[lane].base + R[lane].stc_comp], R[lane].has_current,
-             S_[R[lane].base + (1 + A.S) * m + kinds[R[lane].kind].noise_comp]);
+             R[lane].rc_val);
     // ---- E. spike detection (engine.cpp:753-769)
     if (mine) {
       McgWCell& X = R[lane];
