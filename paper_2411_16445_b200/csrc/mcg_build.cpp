@@ -12,6 +12,8 @@
 #include <cmath>
 #include <map>
 #include <numbers>
+#include <exception>
+#include <thread>
 
 #include "mcg_rng.h"
 
@@ -144,6 +146,29 @@ int chain_schedule(int n, const int32_t* parent, std::vector<int32_t>& idx, int&
   for (size_t k = 0; k < B.size(); ++k) idx[2 * lp - 1 - k] = B[k];
   idx[2 * lp] = 0;
   return lp;
+}
+
+// host threads for the connection passes of build_model (MCG_BUILD_THREADS,
+// default: the hardware threads, at most 16; one below 1 M connections)
+int build_threads(int64_t nconn) {
+  if (const char* e = std::getenv("MCG_BUILD_THREADS")) return std::clamp(std::atoi(e), 1, 64);
+  if (nconn < (int64_t(1) << 20)) return 1;
+  return std::clamp(static_cast<int>(std::thread::hardware_concurrency()), 1, 16);
+}
+
+// v = n copies of x, filled by nthr threads (parallel first touch)
+template <class T, class Al>
+void par_fill(std::vector<T, Al>& v, int64_t n, T x, int nthr) {
+  v.clear();
+  v.resize(static_cast<size_t>(n));
+  if (nthr <= 1 || n < (int64_t(1) << 16)) {
+    std::fill(v.begin(), v.end(), x);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 0; t < nthr; ++t)
+    th.emplace_back([&, t] { std::fill(v.begin() + n * t / nthr, v.begin() + n * (t + 1) / nthr, x); });
+  for (auto& q : th) q.join();
 }
 
 int64_t ceil_steps(double t_ms, double dt_ms) {
@@ -554,97 +579,168 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
   }
 
   tm.mark("cells");
-  // ---- synapse instances: pre-placed then per connection ----
-  // gather per (local cell, group) instance lists in creation order
-  std::vector<std::vector<int32_t>> inst_comp(cgs);
-  std::vector<std::vector<double>> inst_w(cgs);
+  // ---- connections (Impl::build, engine.cpp:357-391) in two passes over the
+  // connection list, both in the reference's order:
+  //   pass 0  the reference's checks in its order (dst, label, targeting,
+  //           source/src range, delay vs dt), min_delay_steps, and counts:
+  //           appended instances per (cell, group), edges per rank bucket
+  //           (src_key, sources last: EventOrder, engine.cpp:25-31), source
+  //           edges per source;
+  //   pass 1  instance selection (append or select_target's cursors) and each
+  //           local edge written straight into its slot of the rank order
+  //           (a stable counting sort by src_key: connections arrive in seq
+  //           order), with the static-charge payload (comp, w * cf[comp]).
+  const int64_t nconn = r.n_connections;
+  const size_t nk1 = static_cast<size_t>(r.n_cells) + 1;  // rank buckets; the last: sources
+  std::vector<int64_t> app(cgs, 0);            // appended instances per (cell, group)
+  std::vector<int64_t> cg_conns(cgs, 0);       // local connections per (cell, group)
+  std::vector<int64_t> bucket(nk1 + 1, 0);     // local edges per rank bucket
+  std::vector<int64_t> src_cnt(std::max(r.n_sources, 0) + 1, 0);
+  {
+    // contiguous chunks of the connection list on host threads, each with its
+    // own counts; an error is rethrown from the first failing connection, so
+    // the message is the one the reference's sequential loop raises
+    struct Part {
+      std::vector<int64_t> app, cg_conns, bucket, src_cnt;
+      int64_t min_delay = -1;
+      int64_t err_ci = -1;
+      std::exception_ptr err;
+    };
+    const int nthr0 = build_threads(nconn);
+    std::vector<Part> parts(nthr0);
+    auto scan = [&](int t) {
+      Part& P = parts[t];
+      const bool own = t > 0;  // thread 0 counts into the totals directly
+      if (own) {
+        P.app.assign(cgs, 0);
+        P.cg_conns.assign(cgs, 0);
+        P.bucket.assign(nk1 + 1, 0);
+        P.src_cnt.assign(src_cnt.size(), 0);
+      }
+      int64_t* ap = own ? P.app.data() : app.data();
+      int64_t* cc = own ? P.cg_conns.data() : cg_conns.data();
+      int64_t* bk = own ? P.bucket.data() : bucket.data();
+      int64_t* sc = own ? P.src_cnt.data() : src_cnt.data();
+      const int64_t c0 = nconn * t / nthr0, c1 = nconn * (t + 1) / nthr0;
+      int scratch = 0;
+      int64_t ci = c0;
+      try {
+        for (; ci < c1; ++ci) {
+          const uint32_t dst = r.conn_dst[ci];
+          if (dst >= static_cast<uint32_t>(r.n_cells)) engine_error("connection dst out of range");
+          const int32_t gi = r.conn_group[ci];
+          const mcg_kind& dspec = r.kinds[r.cell_kind[dst]];
+          if (gi < 0 || gi >= dspec.n_placements) {
+            const int32_t li = (r.labels && r.conn_label) ? r.conn_label[ci] : -1;
+            engine_error("connection label '" +
+                         ((li >= 0 && li < r.n_labels && r.labels[li]) ? std::string(r.labels[li])
+                                                                        : "#" + std::to_string(gi)) +
+                         "' not found");
+          }
+          const bool local = dst >= g0 && dst < g1;
+          const mcg_placement& pl = dspec.placements[gi];
+          if (local) {
+            const int64_t cg = m.cg_off[dst - g0] + gi;
+            if (pl.count == 0) ++ap[cg];
+            else (void)select_target(pl.count, r.conn_policy[ci], scratch);  // its errors, in order
+            ++cc[cg];
+          }
+          if (r.conn_from_source[ci]) {
+            if (r.conn_src[ci] >= static_cast<uint32_t>(r.n_sources))
+              engine_error("connection source out of range");
+            if (local) {
+              ++bk[nk1];
+              ++sc[r.conn_src[ci] + 1];
+            }
+          } else {
+            if (r.conn_src[ci] >= static_cast<uint32_t>(r.n_cells))
+              engine_error("connection src out of range");
+            if (r.conn_delay_ms[ci] < dt * (1.0 - 1e-12))
+              engine_error("configuration: dt exceeds a connection delay");
+            const int64_t d = ceil_steps(r.conn_delay_ms[ci], dt);
+            if (P.min_delay < 0 || d < P.min_delay) P.min_delay = d;
+            if (local) ++bk[r.conn_src[ci] + 1];
+          }
+        }
+      } catch (...) {
+        P.err_ci = ci;
+        P.err = std::current_exception();
+      }
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < nthr0; ++t) th.emplace_back(scan, t);
+    scan(0);
+    for (auto& x : th) x.join();
+    for (int t = 0; t < nthr0; ++t)  // chunks are in order: the first error is the reference's
+      if (parts[t].err) std::rethrow_exception(parts[t].err);
+    for (int t = 0; t < nthr0; ++t) {
+      const Part& P = parts[t];
+      if (P.min_delay >= 0 && (m.min_delay_steps < 0 || P.min_delay < m.min_delay_steps))
+        m.min_delay_steps = P.min_delay;
+      if (t == 0) continue;
+      for (int64_t q = 0; q < cgs; ++q) {
+        app[q] += P.app[q];
+        cg_conns[q] += P.cg_conns[q];
+      }
+      for (size_t q = 0; q < bucket.size(); ++q) bucket[q] += P.bucket[q];
+      for (size_t q = 0; q < src_cnt.size(); ++q) src_cnt[q] += P.src_cnt[q];
+    }
+  }
+  tm.mark("connections");
+  // ---- instance layout: per (cell, group) the pre-placed instances, then the
+  // appended ones in connection order
+  m.cgs.resize(cgs);
+  int64_t ninst = 0;
   for (int c = 0; c < nl; ++c) {
     const McgKind& K = m.kinds[m.cell_kind[c]];
     for (int gi = 0; gi < K.n_groups; ++gi) {
+      const int64_t cg = m.cg_off[c] + gi;
       const McgSpec& S = m.specs[K.spec0 + gi];
-      for (int i = 0; i < S.count; ++i) {
-        inst_comp[m.cg_off[c] + gi].push_back(S.comp);
-        inst_w[m.cg_off[c] + gi].push_back(0.0);
-      }
+      McgCellGroup& G = m.cgs[cg];
+      G.inst = ninst;
+      G.size = static_cast<int32_t>(S.count + app[cg]);
+      G.active_n = 0;
+      G.spec = K.spec0 + gi;
+      G.fifo = -1;
+      ninst += G.size;
     }
   }
-  struct Edge {
-    uint32_t src_key;
-    uint32_t seq;
-    int32_t dst_local, group;
-    uint32_t inst;
-    double w;
-    int64_t delay;
-    int32_t source;  // -1 for cell edges
-  };
-  std::vector<Edge> edges;
-  std::map<std::pair<uint32_t, int32_t>, int> cursors;
-  const int64_t nconn = r.n_connections;
-  edges.reserve(static_cast<size_t>(nconn));
-  for (int64_t ci = 0; ci < nconn; ++ci) {
-    const uint32_t dst = r.conn_dst[ci];
-    if (dst >= static_cast<uint32_t>(r.n_cells)) engine_error("connection dst out of range");
-    const int32_t gi = r.conn_group[ci];
-    const mcg_kind& dspec = r.kinds[r.cell_kind[dst]];
-    if (gi < 0 || gi >= dspec.n_placements) {
-      const int32_t li = (r.labels && r.conn_label) ? r.conn_label[ci] : -1;
-      engine_error("connection label '" +
-                   ((li >= 0 && li < r.n_labels && r.labels[li]) ? std::string(r.labels[li])
-                                                                  : "#" + std::to_string(gi)) +
-                   "' not found");
-    }
-    const bool local = dst >= g0 && dst < g1;
-    uint32_t instance = 0;
-    const mcg_placement& pl = dspec.placements[gi];
-    if (local) {
-      const int64_t cg = m.cg_off[dst - g0] + gi;
-      if (pl.count == 0) {
-        inst_comp[cg].push_back(pl.comp);
-        inst_w[cg].push_back(r.conn_weight[ci]);
-        instance = static_cast<uint32_t>(inst_comp[cg].size() - 1);
-      } else {
-        int& cur = cursors[{dst, gi}];
-        instance = static_cast<uint32_t>(
-            select_target(static_cast<int>(inst_comp[cg].size()), r.conn_policy[ci], cur));
-      }
-    } else if (pl.count != 0) {
-      // cursor state is per destination; non-local destinations never matter
-    }
-    const int64_t d = ceil_steps(r.conn_delay_ms[ci], dt);
-    Edge e{0, static_cast<uint32_t>(ci), local ? static_cast<int32_t>(dst - g0) : -1, gi,
-           instance, r.conn_weight[ci], d, -1};
-    if (r.conn_from_source[ci]) {
-      if (r.conn_src[ci] >= static_cast<uint32_t>(r.n_sources))
-        engine_error("connection source out of range");
-      e.src_key = 0xFFFFFFFFu;
-      e.source = static_cast<int32_t>(r.conn_src[ci]);
-    } else {
-      if (r.conn_src[ci] >= static_cast<uint32_t>(r.n_cells))
-        engine_error("connection src out of range");
-      if (r.conn_delay_ms[ci] < dt * (1.0 - 1e-12))
-        engine_error("configuration: dt exceeds a connection delay");
-      if (m.min_delay_steps < 0 || d < m.min_delay_steps) m.min_delay_steps = d;
-      e.src_key = r.conn_src[ci];
-    }
-    if (local) edges.push_back(e);
+  const int nthr = build_threads(nconn);
+  // instance state: the arrays that start all zero (kernel, STDP traces,
+  // z, calcium, |h - h0|, and STDP / homeostatic weights when no group has
+  // that kind) stay empty here and are zero-filled on the device
+  m.n_inst = ninst;
+  bool any_stdp = false, any_homeo = false;
+  for (const McgCellGroup& G : m.cgs) {
+    any_stdp |= m.specs[G.spec].kind == MCG_SYN_STDP_COND && G.size > 0;
+    any_homeo |= m.specs[G.spec].kind == MCG_SYN_HOMEO_CURRENT && G.size > 0;
   }
-  tm.mark("connections");
-  // rank order: (src_key, seq) — EventOrder (engine.cpp:25-31)
-  // edges were generated in seq order, so a stable bucket sort by src_key
-  // (sources, key 0xFFFFFFFF, last) is the (src_key, seq) order in O(n)
-  {
-    const size_t nk = static_cast<size_t>(r.n_cells) + 1;
-    std::vector<int64_t> cnt(nk + 1, 0);
-    auto key = [&](const Edge& e) {
-      return e.src_key == 0xFFFFFFFFu ? nk - 1 : static_cast<size_t>(e.src_key);
-    };
-    for (const Edge& e : edges) ++cnt[key(e) + 1];
-    for (size_t k = 0; k < nk; ++k) cnt[k + 1] += cnt[k];
-    std::vector<Edge> sorted(edges.size());
-    for (const Edge& e : edges) sorted[cnt[key(e)]++] = e;
-    edges.swap(sorted);
+  m.i_kernel.clear();
+  m.i_stdp_pre.clear();
+  m.i_stdp_post.clear();
+  m.i_stdp_last.clear();
+  m.i_stc_z.clear();
+  m.i_stc_c.clear();
+  m.i_sps_abs.clear();
+  par_fill(m.i_comp, ninst, int32_t(0), nthr);
+  par_fill(m.i_weight, ninst, 0.0, nthr);
+  par_fill(m.i_stc_h, ninst, 0.0, nthr);
+  if (any_stdp) par_fill(m.i_stdp_w, ninst, 0.0, nthr);
+  else m.i_stdp_w.clear();
+  if (any_homeo) par_fill(m.i_homeo_w, ninst, 0.0, nthr);
+  else m.i_homeo_w.clear();
+  for (int c = 0; c < nl; ++c) {
+    const McgKind& K = m.kinds[m.cell_kind[c]];
+    for (int gi = 0; gi < K.n_groups; ++gi) {
+      const McgCellGroup& G = m.cgs[m.cg_off[c] + gi];
+      const McgSpec& S = m.specs[K.spec0 + gi];
+      for (int i = 0; i < G.size; ++i) m.i_comp[G.inst + i] = S.comp;  // appended ones: pl.comp too
+    }
   }
-  const int64_t ne = static_cast<int64_t>(edges.size());
+  // ---- rank order: bucket offsets (cell src keys ascending, sources last)
+  for (size_t k = 0; k < nk1; ++k) bucket[k + 1] += bucket[k];
+  const int64_t ne = bucket[nk1];
+  // every edge slot is written by pass 1 (no fill), but the payload columns
   m.e_dst.resize(ne);
   m.e_group.resize(ne);
   m.e_inst.resize(ne);
@@ -652,70 +748,123 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
   m.e_delay.resize(ne);
   m.e_src.resize(ne);
   m.e_seq.resize(ne);
+  par_fill(m.e_comp, ne, int32_t(-1), nthr);
+  par_fill(m.e_wcf, ne, 0.0, nthr);
   m.out_begin.assign(r.n_cells, 0);
   m.out_end.assign(r.n_cells, 0);
-  std::vector<std::vector<int64_t>> src_lists(r.n_sources);
-  for (int64_t i = 0; i < ne; ++i) {
-    const Edge& e = edges[i];
-    m.e_dst[i] = e.dst_local;
-    m.e_group[i] = e.group;
-    m.e_inst[i] = e.inst;
-    m.e_weight[i] = e.w;
-    m.e_delay[i] = e.delay;
-    m.e_src[i] = e.src_key;
-    m.e_seq[i] = e.seq;
-    m.max_delay_steps = std::max(m.max_delay_steps, e.delay);
-    if (e.source < 0) {
-      if (m.out_end[e.src_key] == 0 && m.out_begin[e.src_key] == 0) m.out_begin[e.src_key] = i;
-      m.out_end[e.src_key] = i + 1;
-    } else {
-      src_lists[e.source].push_back(i);
+  for (int g = 0; g < r.n_cells; ++g)
+    if (bucket[g + 1] > bucket[g]) {
+      m.out_begin[g] = bucket[g];
+      m.out_end[g] = bucket[g + 1];
     }
+  for (int q = 0; q < r.n_sources; ++q) src_cnt[q + 1] += src_cnt[q];
+  m.src_edge_off.assign(src_cnt.begin(), src_cnt.begin() + (r.n_sources + 1));
+  m.src_edges.resize(src_cnt[std::max(r.n_sources, 0)]);
+  // ---- pass 1: instances, then edges; both scan the connections in order,
+  // split over host threads by what they write (destination cells for the
+  // instances, rank buckets for the edges) so that every thread sees its own
+  // connections in the reference's order
+  HVec<uint32_t> inst_of(static_cast<size_t>(nconn));  // every local one is written
+  {
+    auto instances = [&](int c_lo, int c_hi) {
+      std::vector<int32_t> cursor;  // SelectionCursor per (dst, label), cells [c_lo, c_hi)
+      const int64_t cg_lo = m.cg_off[c_lo], cg_hi = m.cg_off[c_hi];
+      std::vector<int64_t> run(cg_hi - cg_lo, 0);  // appended so far per (cell, group)
+      cursor.assign(cg_hi - cg_lo, 0);
+      for (int64_t ci = 0; ci < nconn; ++ci) {
+        const uint32_t dst = r.conn_dst[ci];
+        if (dst < g0 + uint32_t(c_lo) || dst >= g0 + uint32_t(c_hi)) continue;
+        const int64_t cg = m.cg_off[dst - g0] + r.conn_group[ci];
+        const McgCellGroup& G = m.cgs[cg];
+        const int32_t count = m.specs[G.spec].count;
+        uint32_t instance;
+        if (count == 0) {
+          instance = static_cast<uint32_t>(run[cg - cg_lo]++);
+          m.i_weight[G.inst + instance] = r.conn_weight[ci];
+        } else {
+          instance = static_cast<uint32_t>(select_target(count, r.conn_policy[ci], cursor[cg - cg_lo]));
+        }
+        inst_of[ci] = instance;
+      }
+    };
+    std::vector<std::thread> th;
+    for (int t = 0; t < nthr; ++t) {
+      const int c_lo = static_cast<int>(int64_t(nl) * t / nthr), c_hi = static_cast<int>(int64_t(nl) * (t + 1) / nthr);
+      if (t + 1 < nthr) th.emplace_back(instances, c_lo, c_hi);
+      else instances(c_lo, c_hi);
+    }
+    for (auto& x : th) x.join();
   }
-  m.src_edge_off.assign(r.n_sources + 1, 0);
-  for (int s = 0; s < r.n_sources; ++s) {
-    m.src_edge_off[s + 1] = m.src_edge_off[s] + static_cast<int64_t>(src_lists[s].size());
-    for (int64_t x : src_lists[s]) m.src_edges.push_back(x);
+  {
+    // bucket ranges balanced by edge count; the source bucket (last) with the
+    // source CSR goes to the last thread
+    auto edges = [&](size_t k_lo, size_t k_hi) {
+      std::vector<int64_t> pos(bucket.begin() + k_lo, bucket.begin() + k_hi);
+      std::vector<int64_t> spos;
+      if (k_hi == nk1) spos.assign(src_cnt.begin(), src_cnt.begin() + std::max(r.n_sources, 0));
+      int64_t maxd = 0;
+      for (int64_t ci = 0; ci < nconn; ++ci) {
+        const uint32_t dst = r.conn_dst[ci];
+        if (dst < g0 || dst >= g1) continue;
+        const bool from_src = r.conn_from_source[ci] != 0;
+        const size_t key = from_src ? nk1 - 1 : static_cast<size_t>(r.conn_src[ci]);
+        if (key < k_lo || key >= k_hi) continue;
+        const int32_t gi = r.conn_group[ci];
+        const int c = static_cast<int>(dst - g0);
+        const McgCellGroup& G = m.cgs[m.cg_off[c] + gi];
+        const McgSpec& S = m.specs[G.spec];
+        const double w = r.conn_weight[ci];
+        const uint32_t instance = inst_of[ci];
+        const int64_t e = pos[key - k_lo]++;
+        m.e_dst[e] = c;
+        m.e_group[e] = gi;
+        m.e_inst[e] = instance;
+        m.e_weight[e] = w;
+        m.e_delay[e] = ceil_steps(r.conn_delay_ms[ci], dt);
+        m.e_src[e] = from_src ? 0xFFFFFFFFu : r.conn_src[ci];
+        m.e_seq[e] = static_cast<uint32_t>(ci);
+        maxd = std::max(maxd, m.e_delay[e]);
+        if (from_src) m.src_edges[spos[r.conn_src[ci]]++] = e;
+        // static-charge edges: the instance's compartment and w * cf[comp]
+        // (the product apply_event forms, engine.cpp:455-459), so staged
+        // delivery reads one edge record instead of chasing group -> comp
+        if (S.kind == MCG_SYN_STATIC_CHARGE) {
+          const McgKind& K = m.kinds[m.cell_kind[c]];
+          const int comp = m.i_comp[G.inst + instance];
+          m.e_comp[e] = comp;
+          m.e_wcf[e] = w * m.k_cf[K.arr + comp];
+        }
+      }
+      return maxd;
+    };
+    std::vector<size_t> cut(nthr + 1, nk1);
+    cut[0] = 0;
+    for (int t = 1; t < nthr; ++t) {  // first bucket whose start passes t / nthr of the edges
+      const int64_t want = ne * t / nthr;
+      cut[t] = static_cast<size_t>(std::upper_bound(bucket.begin(), bucket.begin() + nk1, want) - bucket.begin()) - 1;
+      cut[t] = std::max(cut[t], cut[t - 1]);
+      cut[t] = std::min(cut[t], nk1 - 1);
+    }
+    std::vector<int64_t> maxd(nthr, 0);
+    std::vector<std::thread> th;
+    for (int t = 0; t < nthr; ++t) {
+      if (t + 1 < nthr) th.emplace_back([&, t] { maxd[t] = edges(cut[t], cut[t + 1]); });
+      else maxd[t] = edges(cut[t], cut[t + 1]);
+    }
+    for (auto& x : th) x.join();
+    for (int64_t d : maxd) m.max_delay_steps = std::max(m.max_delay_steps, d);
   }
-
-  tm.mark("edge sort + CSR");
-  // flatten instances
-  m.cgs.resize(cgs);
-  int64_t ninst = 0;
-  for (int64_t cg = 0; cg < cgs; ++cg) ninst += static_cast<int64_t>(inst_comp[cg].size());
-  m.i_comp.resize(ninst);
-  m.i_weight.resize(ninst);
-  m.i_kernel.assign(ninst, 0.0);
-  m.i_stdp_pre.assign(ninst, 0.0);
-  m.i_stdp_post.assign(ninst, 0.0);
-  m.i_stdp_w.assign(ninst, 0.0);
-  m.i_stdp_last.assign(ninst, 0);
-  m.i_homeo_w.assign(ninst, 0.0);
-  m.i_stc_h.assign(ninst, 0.0);
-  m.i_stc_z.assign(ninst, 0.0);
-  m.i_stc_c.assign(ninst, 0.0);
-  m.i_sps_abs.assign(ninst, 0.0);
-  tm.mark("instances");
-  // number of connections per (cg) for fifo sizing
-  std::vector<int64_t> cg_conns(cgs, 0);
-  for (const Edge& e : edges) cg_conns[m.cg_off[e.dst_local] + e.group] += 1;
-  int64_t off = 0;
+  tm.mark("edges + instances");
+  // ---- per-group state and delayed-calcium queues
   for (int c = 0; c < nl; ++c) {
     const McgKind& K = m.kinds[m.cell_kind[c]];
     for (int gi = 0; gi < K.n_groups; ++gi) {
       const int64_t cg = m.cg_off[c] + gi;
       const McgSpec& S = m.specs[K.spec0 + gi];
       McgCellGroup& G = m.cgs[cg];
-      G.inst = off;
-      G.size = static_cast<int32_t>(inst_comp[cg].size());
-      G.active_n = 0;
-      G.spec = K.spec0 + gi;
-      G.fifo = -1;
       for (int i = 0; i < G.size; ++i) {
-        const int64_t j = off + i;
-        m.i_comp[j] = inst_comp[cg][i];
-        m.i_weight[j] = inst_w[cg][i];
-        if (S.kind == MCG_SYN_STDP_COND) m.i_stdp_w[j] = inst_w[cg][i];
+        const int64_t j = G.inst + i;
+        if (S.kind == MCG_SYN_STDP_COND) m.i_stdp_w[j] = m.i_weight[j];  // any_stdp: allocated
         if (S.kind == MCG_SYN_HOMEO_CURRENT) m.i_homeo_w[j] = r.kinds[m.cell_kind[c]].placements[gi].syn.homeo.w_init_nA;
         if (S.kind == MCG_SYN_STC_CHARGE) m.i_stc_h[j] = S.h0;
       }
@@ -734,7 +883,6 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
         G.fifo = static_cast<int32_t>(m.fifos.size());
         m.fifos.push_back(F);
       }
-      off += G.size;
       m.total_syn += G.size;
       if (S.kind == MCG_SYN_STC_CHARGE) m.stc_syn += G.size;
     }
@@ -790,24 +938,7 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
         if (m.k_g_na[K.arr + i] != 0.0) ++m.hh_comps;
   }
   tm.mark("totals");
-  // static-charge edges: the instance's compartment and w * cf[comp] (the
-  // product apply_event forms, engine.cpp:455-459), so staged delivery reads
-  // one edge record instead of chasing group -> instance -> compartment
-  {
-    const int64_t ne = static_cast<int64_t>(m.e_dst.size());
-    m.e_comp.assign(ne, -1);
-    m.e_wcf.assign(ne, 0.0);
-    for (int64_t r = 0; r < ne; ++r) {
-      const int c = m.e_dst[r];
-      const McgCellGroup& G = m.cgs[m.cg_off[c] + m.e_group[r]];
-      if (m.specs[G.spec].kind != MCG_SYN_STATIC_CHARGE) continue;
-      const McgKind& K = m.kinds[m.cell_kind[c]];
-      const int comp = m.i_comp[G.inst + m.e_inst[r]];
-      m.e_comp[r] = comp;
-      m.e_wcf[r] = m.e_weight[r] * m.k_cf[K.arr + comp];
-    }
-  }
-  tm.mark("edge payloads");
+
 }
 
 }  // namespace mcg

@@ -8,12 +8,41 @@
 #pragma once
 #include <stdexcept>
 #include <string>
+#include <memory>
+#include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "../../include/mcg.h"
 #include "mcg_model.h"
 
 namespace mcg {
+
+// std::allocator that default-initializes (no zero fill on resize): the
+// build's large arrays are written completely, or filled by host threads
+// (first touch in parallel), so the serial value-initialization of
+// std::vector::resize would only cost page faults on one core
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = NoInitAlloc<U>;
+  };
+  NoInitAlloc() = default;
+  template <class U>
+  NoInitAlloc(const NoInitAlloc<U>&) noexcept {}
+  template <class U>
+  void construct(U* p) noexcept(std::is_nothrow_default_constructible<U>::value) {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <class U, class... Args>
+  void construct(U* p, Args&&... args) {
+    ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...);
+  }
+};
+template <class T>
+using HVec = std::vector<T, NoInitAlloc<T>>;
+
 
 struct Error : std::runtime_error {
   mcg_status code;
@@ -83,21 +112,22 @@ struct HostModel {
 
   // synapse groups and instances
   std::vector<McgCellGroup> cgs;
-  std::vector<int32_t> i_comp;
-  std::vector<double> i_weight, i_kernel, i_stdp_pre, i_stdp_post, i_stdp_w, i_homeo_w;
-  std::vector<int64_t> i_stdp_last;
-  std::vector<double> i_stc_h, i_stc_z, i_stc_c, i_sps_abs;
+  int64_t n_inst = 0;  // synapse instances (arrays left empty by the build are all zero)
+  HVec<int32_t> i_comp;
+  HVec<double> i_weight, i_kernel, i_stdp_pre, i_stdp_post, i_stdp_w, i_homeo_w;
+  HVec<int64_t> i_stdp_last;
+  HVec<double> i_stc_h, i_stc_z, i_stc_c, i_sps_abs;
   std::vector<McgFifo> fifos;
   int64_t fifo_total = 0;
 
   // edges with a local destination, sorted by (src_key, seq) -> rank
-  std::vector<int32_t> e_dst, e_group;
-  std::vector<uint32_t> e_inst;
-  std::vector<double> e_weight;
-  std::vector<uint32_t> e_src, e_seq;       // EventRec.src / seq of each edge (EventOrder)
-  std::vector<int32_t> e_comp;              // static-charge edges: target compartment (else -1)
-  std::vector<double> e_wcf;                // and weight * charge_factor[comp] (engine.cpp:457)
-  std::vector<int64_t> e_delay;
+  HVec<int32_t> e_dst, e_group;
+  HVec<uint32_t> e_inst;
+  HVec<double> e_weight;
+  HVec<uint32_t> e_src, e_seq;              // EventRec.src / seq of each edge (EventOrder)
+  HVec<int32_t> e_comp;                     // static-charge edges: target compartment (else -1)
+  HVec<double> e_wcf;                       // and weight * charge_factor[comp] (engine.cpp:457)
+  HVec<int64_t> e_delay;
   std::vector<int64_t> out_begin, out_end;  // per global gid
   std::vector<int64_t> src_edge_off;        // per source CSR into src_edges
   std::vector<int64_t> src_edges;           // ranks

@@ -72,7 +72,8 @@ struct DBuf {
       CK(cudaStreamSynchronize(0));
     }
   }
-  void upload(const std::vector<T>& v, cudaStream_t st) {
+  template <class Al>
+  void upload(const std::vector<T, Al>& v, cudaStream_t st) {
     alloc(std::max<size_t>(v.size(), 1));
     if (!v.empty())
       CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
@@ -815,17 +816,26 @@ struct Engine {
     d_fifo_w.alloc(std::max<int64_t>(m.fifo_total, 1));
     d_i_comp.upload(m.i_comp, st);
     d_i_active.alloc(std::max<size_t>(m.i_comp.size(), 1));
-    d_i_weight.upload(m.i_weight, st);
-    d_i_kernel.upload(m.i_kernel, st);
-    d_i_stdp_pre.upload(m.i_stdp_pre, st);
-    d_i_stdp_post.upload(m.i_stdp_post, st);
-    d_i_stdp_w.upload(m.i_stdp_w, st);
-    d_i_stdp_last.upload(m.i_stdp_last, st);
-    d_i_homeo_w.upload(m.i_homeo_w, st);
-    d_i_stc_h.upload(m.i_stc_h, st);
-    d_i_stc_z.upload(m.i_stc_z, st);
-    d_i_stc_c.upload(m.i_stc_c, st);
-    d_i_sps_abs.upload(m.i_sps_abs, st);
+    // instance arrays the build left empty start all zero: fill on the device
+    auto up_or_zero = [&](auto& d, const auto& h) {
+      if (!h.empty()) {
+        d.upload(h, st);
+      } else {
+        d.alloc(std::max<size_t>(size_t(m.n_inst), 1));
+        d.zero(st);
+      }
+    };
+    up_or_zero(d_i_weight, m.i_weight);
+    up_or_zero(d_i_kernel, m.i_kernel);
+    up_or_zero(d_i_stdp_pre, m.i_stdp_pre);
+    up_or_zero(d_i_stdp_post, m.i_stdp_post);
+    up_or_zero(d_i_stdp_w, m.i_stdp_w);
+    up_or_zero(d_i_stdp_last, m.i_stdp_last);
+    up_or_zero(d_i_homeo_w, m.i_homeo_w);
+    up_or_zero(d_i_stc_h, m.i_stc_h);
+    up_or_zero(d_i_stc_z, m.i_stc_z);
+    up_or_zero(d_i_stc_c, m.i_stc_c);
+    up_or_zero(d_i_sps_abs, m.i_sps_abs);
     d_stc_nz.alloc(std::max<size_t>(m.i_stc_h.size(), 1));
     if (d_stc_nz.p)
       CK(cudaMemsetAsync(d_stc_nz.p, 0xff, d_stc_nz.n * sizeof(McgNzCache), st));  // tag -1
@@ -1833,8 +1843,8 @@ struct Engine {
     if (n) CK(cudaMemcpyAsync(h.data(), b.p, n * sizeof(T), cudaMemcpyDeviceToHost, st));
     return h;
   }
-  template <class T>
-  void upload_to(DBuf<T>& b, const std::vector<T>& h) {
+  template <class T, class Al>
+  void upload_to(DBuf<T>& b, const std::vector<T, Al>& h) {
     if (!h.empty()) CK(cudaMemcpyAsync(b.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st));
   }
 
@@ -2441,12 +2451,16 @@ __global__ void k_er(uint64_t seed, uint32_t n, double p, uint64_t k0, uint64_t 
   int64_t c = 0, o = offs ? offs[t] : 0;
   uint64_t x[4];
   uint64_t blk = ~0ull;
-  for (uint64_t k = a; k < b; ++k) {
+  uint32_t i = uint32_t(a / n), j = uint32_t(a - uint64_t(i) * n);  // (i, j) of pair k, stepped
+  for (uint64_t k = a; k < b; ++k, ++j) {
+    if (j == n) {
+      j = 0;
+      ++i;
+    }
     if ((k >> 2) != blk) {
       blk = k >> 2;
       mcg_threefry(&key, blk, x);
     }
-    const uint32_t i = uint32_t(k / n), j = uint32_t(k % n);
     if (i == j) continue;
     const double u = (double)(x[k & 3u] >> 11) * MCG_2POW_M53;
     if (u < p) {

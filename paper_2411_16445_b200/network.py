@@ -23,6 +23,7 @@ import numpy as np
 
 from . import _abi as A
 from .engine import Engine, EngineOptions
+from .recipe import par_take
 from .recipe import (CellKindSpec, ConnectionTable, EngineError, HhMembrane, LifMembrane,
                      MorphologyError, PlacementSpec, PoissonSource, PoissonWindow, ProbeSpec,
                      ProbeWhat, Recipe, Region, ScriptedSource, Segment, SelectionPolicy,
@@ -49,20 +50,28 @@ def uniform_stream(key, n0: int, count: int, device: int = 0) -> np.ndarray:
 
 
 def er_pairs(seed: int, n: int, p: float, device: int = 0) -> Tuple[np.ndarray, np.ndarray]:
-    """All (i, j) with er_connected(seed, i, j, n, p), in i-major, j-minor order."""
+    """All (i, j) with er_connected(seed, i, j, n, p), in i-major, j-minor order.
+
+    One call into the sampler with buffers sized to the expected count plus a
+    wide margin (mean n(n-1)p, +16 standard deviations); only if the sample
+    is larger still does a second call run with the exact size."""
     L = A.lib()
-    cnt = C.c_int64(0)
-    st = L.mcg_er_connect(device, seed, n, p, 0, n, None, None, C.byref(cnt))
-    if st != 0:
-        raise RuntimeError(L.mcg_last_error().decode())
-    src = np.empty(cnt.value, np.uint32)
-    dst = np.empty(cnt.value, np.uint32)
-    if cnt.value:
+    mean = float(n) * max(n - 1, 0) * min(max(p, 0.0), 1.0)
+    cap = int(mean + 16.0 * math.sqrt(mean + 1.0) + 1024)
+    for _ in range(2):
+        src = np.empty(cap, np.uint32)
+        dst = np.empty(cap, np.uint32)
+        cnt = C.c_int64(cap)
         st = L.mcg_er_connect(device, seed, n, p, 0, n, src.ctypes.data_as(C.c_void_p),
                               dst.ctypes.data_as(C.c_void_p), C.byref(cnt))
+        if st == 0:
+            return src[:cnt.value], dst[:cnt.value]
+        cnt = C.c_int64(0)  # buffer too small: the exact count, then once more
+        st = L.mcg_er_connect(device, seed, n, p, 0, n, None, None, C.byref(cnt))
         if st != 0:
             raise RuntimeError(L.mcg_last_error().decode())
-    return src, dst
+        cap = int(cnt.value)
+    raise RuntimeError(L.mcg_last_error().decode())
 
 
 # ---- morphology (morphology.cpp) --------------------------------------------------
@@ -275,27 +284,45 @@ def build_consolidation_network(cfg: ConsolidationConfig, eight_hour: bool,
     cell_kind[:n_exc] = 0
 
     src, dst = er_pairs(cfg.seed, n, cfg.p_conn, device)
-    se, de = src < n_exc, dst < n_exc
-    lab = np.where(se & de, 0, np.where(se, 1, np.where(de, 2, 3))).astype(np.int32)
-    wlut = np.array([cfg.w_rec_scale * c_morpho, cfg.w_ei_mV, cfg.w_ie_mV, cfg.w_ii_mV])
-    rec = ConnectionTable(0, src, dst, ["rec", "ein", "isyn", "iin"], lab,
-                          int(SelectionPolicy.univalent), wlut[lab], cfg.delay_ms)
+    # label per pair (network.cpp:551-569): exc->exc "rec", exc->inh "ein",
+    # inh->exc "isyn", inh->inh "iin" = 2 (src is inh) + (dst is inh)
+    n_rec = len(src)
+    pat = cfg.pattern
+    n_stim = cfg.n_stim_sources * (pat + pat // 2)
+    tot = n_rec + n_stim
+    # the connection table's columns, filled in place (no concatenation copies)
+    lab = np.empty(tot, np.int32)
+    np.add(np.left_shift((src >= n_exc).view(np.uint8), 1, dtype=np.int32), (dst >= n_exc).view(np.uint8),
+           out=lab[:n_rec], dtype=np.int32)
+    wlut = np.array([cfg.w_rec_scale * c_morpho, cfg.w_ei_mV, cfg.w_ie_mV, cfg.w_ii_mV, cfg.w_stim_mV])
+    c_src = np.empty(tot, np.uint32)
+    c_dst = np.empty(tot, np.uint32)
+    c_src[:n_rec] = src
+    c_dst[:n_rec] = dst
+    del src, dst
+    from_source = np.zeros(tot, np.uint8)
+    delay = np.full(tot, cfg.delay_ms, np.float64)
 
     sources: List = []
-    tables = [rec]
-    pat = cfg.pattern
+    off = n_rec
 
-    def add_pool(t0, dur, rate, g1):
+    def add_pool(t0, dur, rate, g1):  # network.cpp:576-592
+        nonlocal off
         for _ in range(cfg.n_stim_sources):
             sources.append(PoissonSource([PoissonWindow(t0, t0 + dur, rate)]))
-            s = len(sources) - 1
-            tables.append(ConnectionTable(1, np.full(g1, s, np.uint32), np.arange(g1), ["ext"], 0,
-                                          int(SelectionPolicy.univalent), cfg.w_stim_mV, cfg.dt_ms))
+            sl = slice(off, off + g1)
+            c_src[sl] = len(sources) - 1
+            c_dst[sl] = np.arange(g1, dtype=np.uint32)
+            lab[sl] = 4  # "ext"
+            from_source[sl] = 1
+            delay[sl] = cfg.dt_ms
+            off += g1
 
     add_pool(cfg.t_learn_ms, cfg.learn_duration_ms, cfg.learn_rate_hz, pat)
     add_pool(t_recall, cfg.recall_duration_ms, cfg.recall_rate_hz, pat // 2)
-    r = Recipe(kinds=[exc, inh], cell_kind=cell_kind, sources=sources,
-               connections=ConnectionTable.concat(tables))
+    conns = ConnectionTable(from_source, c_src, c_dst, ["rec", "ein", "isyn", "iin", "ext"], lab,
+                            int(SelectionPolicy.univalent), par_take(wlut, lab), delay)
+    r = Recipe(kinds=[exc, inh], cell_kind=cell_kind, sources=sources, connections=conns)
     return ConsolidationBuild(r, list(range(pat // 2)), list(range(pat // 2, pat)),
                               list(range(pat, n_exc)), c_morpho)
 

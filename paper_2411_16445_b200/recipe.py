@@ -336,6 +336,25 @@ class Recipe:  # recipe.hpp:183-189
         return FlatRecipe(self)
 
 
+def par_take(table, idx, out=None, dtype=None):
+    """np.take(table, idx) split over host threads for long index arrays
+    (numpy releases the GIL inside take)."""
+    n = len(idx)
+    if out is None:
+        out = np.empty(n, dtype or table.dtype)
+    if n < (1 << 20):
+        np.take(table, idx, out=out)
+        return out
+    import concurrent.futures as cf
+    import os
+    k = max(1, min(16, os.cpu_count() or 1))
+    bounds = [n * i // k for i in range(k + 1)]
+    with cf.ThreadPoolExecutor(k) as ex:
+        list(ex.map(lambda i: np.take(table, idx[bounds[i]:bounds[i + 1]], out=out[bounds[i]:bounds[i + 1]]),
+                    range(k)))
+    return out
+
+
 def _arr(a, ctype):
     """(numpy array kept alive, ctypes pointer)"""
     return a.ctypes.data_as(C.POINTER(ctype))
@@ -447,7 +466,18 @@ class FlatRecipe:
         # as -1: the engine's build reports them in the reference's order
         # (engine.cpp:317-391), naming the label from the table below
         group = np.full(len(t), -1, np.int32)
-        if len(t):
+        if len(t) and n_cells > 0 and int(t.dst.max()) < n_cells and int(cell_kind.max()) < nk \
+                and int(t.label_idx.min()) >= 0 and int(t.label_idx.max()) < lut.shape[1]:
+            # every destination and kind in range: one gather through the
+            # flattened (kind, label) table
+            flat_lut = lut.ravel()
+            if lut.shape[1] == 1:
+                idx = par_take(cell_kind.astype(np.int32), t.dst)
+            else:
+                idx = par_take(cell_kind.astype(np.int32) * np.int32(lut.shape[1]), t.dst)
+                idx += t.label_idx
+            par_take(flat_lut, idx, out=group)
+        elif len(t):
             ok = t.dst < n_cells
             dk = np.full(len(t), -1, np.int64)
             dk[ok] = cell_kind[t.dst[ok]]
