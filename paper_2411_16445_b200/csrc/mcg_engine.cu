@@ -276,6 +276,7 @@ struct Engine {
   int32_t wg_G = 1, wg_groups = 1, wg_warps = 1, wg_grid = 1, wg_resident = 0, wg_P = 0, wg_MW = 1;
   int32_t wg_ev_cap = 0, wg_warp_doubles = 0, wg_kind_doubles = 0, wg_specs_sm = 0, wg_lazy = 0;
   size_t wg_smem = 0;
+  int32_t wg_no_abort = 0;
   DBuf<int32_t> d_kb_off;
   DBuf<uint32_t> d_stc_mask;
   DBuf<int64_t> d_stc_t;
@@ -300,7 +301,8 @@ struct Engine {
       std::fprintf(stderr, "k_warp phase us/step/warp (mean | max warp), steps=%lld warps=%.0f:",
                    (long long)call_steps, warps);
       static const char* nm[MCG_WPH_N] = {"epoch_in", "noise", "deliver", "stc", "trigger", "solve",
-                                          "detect_post", "probes", "epoch_out", "groups", "expand", "gsync"};
+                                          "detect_post", "probes", "epoch_out", "groups", "expand", "gsync",
+                                          "solve_chain", "abort_chk"};
       for (int i = 0; i < MCG_WPH_N; ++i)
         std::fprintf(stderr, " %s %.3f|%.3f", nm[i], ph[i] / warps / 1965.0 / std::max<int64_t>(call_steps, 1),
                      ph[MCG_WPH_N + i] / 1965.0 / std::max<int64_t>(call_steps, 1));
@@ -628,9 +630,20 @@ struct Engine {
     use_warp = true;
     lazy_valid = false;
     lazy_dirty = false;
+    // inboxes sized so that no epoch's expansion can overflow them: the
+    // kernel then skips the per-epoch overflow check (up to 1/4 of the free
+    // device memory, at most 8 GiB)
+    {
+      size_t fr = 0, tot = 0;
+      CK(cudaMemGetInfo(&fr, &tot));
+      wg_no_abort = (!std::getenv("MCG_WARP_ABORT_CHECK") &&
+                     size_inboxes_for_worst_case(std::min(fr / 4, size_t(8) << 30))) ? 1 : 0;
+    }
     if (std::getenv("MCG_VERBOSE"))
-      std::fprintf(stderr, "engine: k_warp G=%d groups=%d grid=%d warps=%d resident=%d P=%d MW=%d lazy=%d smem=%zu\n",
-                   wg_G, wg_groups, wg_grid, wg_warps, wg_resident, wg_P, wg_MW, wg_lazy, wg_smem);
+      std::fprintf(stderr, "engine: k_warp G=%d groups=%d grid=%d warps=%d resident=%d P=%d MW=%d lazy=%d smem=%zu "
+                   "no_abort=%d inc_cap=%d pend_cap=%d\n",
+                   wg_G, wg_groups, wg_grid, wg_warps, wg_resident, wg_P, wg_MW, wg_lazy, wg_smem, wg_no_abort,
+                   inc_cap, pend_cap);
   }
 
   // k_point (mcg_point.cuh) runs networks of exact-LIF point cells with
@@ -1207,19 +1220,28 @@ struct Engine {
   bool async_ok = false;             // inboxes sized so that no expansion can overflow
 
   // inbox capacities that no epoch can exceed: per destination, every in-edge
-  // delivers at most sp_cap (cell edges) or L (source edges: one event per
+  // delivers at most sp_cap (cell edges) or, from a source, one event per step
+  // (Poisson) or per scheduled time (regular / scripted, which may share a
   // step) events per epoch, and an event waits at most ceil(delay / L) + 1
   // epochs in the pending list; false (and nothing changed) above the budget
   bool size_inboxes_for_worst_case(size_t budget_bytes) {
     const int nl = n_local();
     std::vector<int64_t> inc(std::max(nl, 1), 0), pend(std::max(nl, 1), 0);
-    for (size_t r = 0; r < m.e_dst.size(); ++r) {
+    auto add = [&](size_t r, int64_t per) {
       const int c = m.e_dst[r];
-      if (c < 0) continue;
-      const int64_t per = (m.e_src[r] == 0xFFFFFFFFu) ? L : sp_cap;
+      if (c < 0) return;
       const int64_t d = m.e_delay[r];
       inc[c] += per;
       pend[c] += per * ((d + L - 1) / L + 1);
+    };
+    for (size_t r = 0; r < m.e_dst.size(); ++r)
+      if (m.e_src[r] != 0xFFFFFFFFu) add(r, sp_cap);
+    for (size_t q = 0; q < m.sources.size(); ++q) {
+      const Source& S = m.sources[q];
+      const int64_t per = S.type == MCG_SRC_POISSON ? L
+                          : S.type == MCG_SRC_REGULAR ? std::max<int64_t>(S.r_count, 0)
+                                                      : static_cast<int64_t>(S.steps.size());
+      for (int64_t k = m.src_edge_off[q]; k < m.src_edge_off[q + 1]; ++k) add(size_t(m.src_edges[k]), per);
     }
     const int64_t mi = *std::max_element(inc.begin(), inc.end());
     const int64_t mp = *std::max_element(pend.begin(), pend.end());
@@ -1435,6 +1457,7 @@ struct Engine {
       W.x_send = A.x_send;
       W.x_cap = A.x_cap;
       W.epoch_base = epoch_base;
+      W.no_abort = wg_no_abort;
       void* wargs[] = {&Dv, &W, &max_len};
       CK(cudaEventRecord(evk0, st));
       CK(cudaFuncSetAttribute(k_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wg_smem)));

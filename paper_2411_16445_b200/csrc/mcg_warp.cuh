@@ -37,7 +37,7 @@
 #include "mcg_batch.cuh"
 
 #define MCG_WG_MAX 8  // cells per warp group
-#define MCG_WPH_N 12   // phase-timing slots (MCG_PHASE_TIMING)
+#define MCG_WPH_N 14   // phase-timing slots (MCG_PHASE_TIMING)
 
 // optional per-phase cycle accounting: lane 0 of each warp, one row per warp
 __shared__ unsigned long long mcg_wph[8][MCG_WPH_N + 1];
@@ -84,6 +84,7 @@ struct McgWarpArgs {
   int64_t* x_send;       // sharded export (as McgBatchArgs)
   int64_t x_cap;
   int32_t epoch_base;    // added to the launch's epoch index in the log chunks
+  int32_t no_abort;      // inboxes sized for the worst case: no expansion can overflow
 };
 
 // one staged network event of the epoch (the pending list's head, with the
@@ -851,6 +852,7 @@ __device__ void mcg_wg_epoch(const McgDev& D, const McgWarpArgs& A, const McgWar
         kind = R[sys_k].kind;
       }
       mcg_chain_lane<false>(L);
+      WPH(12);
       // single-compartment systems on their side-0 lanes
       if (sys_lane && sys < S1 && side == 0 && sys_n == 1) {
         const McgWCell& X = R[sys_k];
@@ -1061,7 +1063,10 @@ __global__ void __launch_bounds__(256, 1) k_warp(const __grid_constant__ McgDev 
     WPH(10);
     grid.sync();
     WPH(11);
-    if (*D.abort) break;
+    // the overflow flag, read by every warp after the barrier, costs ~5 us
+    // per epoch (one contended line); unneeded when overflow is impossible
+    if (!A.no_abort && *D.abort) break;
+    WPH(13);
     for (int g = gw; g < A.n_groups; g += nw) {
       if (!A.resident) mcg_wg_enter(D, A, W, g, lane);
       WPH(9);
