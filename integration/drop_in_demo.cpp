@@ -14,8 +14,9 @@
 #include "mcsim/network.hpp"
 #include "mcsim_gpu.hpp"
 
+// spikes and sampled cell state of both engines after advance_to(t_ms)
 template <class A, class B>
-static int compare(A& ref, B& gpu, const mcsim::Recipe& r, double t_ms) {
+static int compare_state(A& ref, B& gpu, const mcsim::Recipe& r, double t_ms) {
   ref.advance_to(t_ms);
   gpu.advance_to(t_ms);
   const auto& s0 = ref.spikes();
@@ -47,6 +48,14 @@ static int compare(A& ref, B& gpu, const mcsim::Recipe& r, double t_ms) {
         }
       }
   }
+  return 0;
+}
+
+template <class A, class B>
+static int compare(A& ref, B& gpu, const mcsim::Recipe& r, double t_ms) {
+  if (const int rc = compare_state(ref, gpu, r, t_ms)) return rc;
+  const std::size_t n_spikes = ref.spikes().size();
+  const uint32_t n = static_cast<uint32_t>(r.cell_kind.size());
   // checkpoints: the same MCSCKPT1 bytes, and each engine restores the other's
   const auto b0 = ref.make_checkpoint().serialize();
   const auto b1 = gpu.make_checkpoint().serialize();
@@ -81,7 +90,7 @@ static int compare(A& ref, B& gpu, const mcsim::Recipe& r, double t_ms) {
   }
   std::printf("OK %zu spikes identical, checkpoints identical (%zu bytes), t = %.1f ms; "
               "restore + %zu spikes to %.1f ms identical\n",
-              s0.size(), b0.size(), t_ms, r0.size(), t2);
+              n_spikes, b0.size(), t_ms, r0.size(), t2);
   return 0;
 }
 
@@ -137,6 +146,16 @@ int main(int argc, char** argv) {
     const mcsim::ConsolidationBuild b = mcsim::build_consolidation_network(cfg, true);
     const mcsim::EngineOptions opt{cfg.dt_ms, cfg.seed, 8};
     mcsim::Engine ref(b.recipe, opt);
+    if (which == "sharded") {
+      // the shard constructor with a one-rank communicator: the exchange runs
+      // inside libmcg (stepping launch + ncclAllGather per epoch)
+      mcsim_gpu::Shard sh;
+      sh.nccl_id = mcsim_gpu::nccl_unique_id();
+      mcsim_gpu::Engine gpu(b.recipe, opt, sh);
+      const int rc = compare_state(ref, gpu, b.recipe, t_ms);
+      if (rc == 0) std::printf("OK sharded: %zu spikes identical, t = %.1f ms\n", gpu.spikes().size(), t_ms);
+      return rc;
+    }
     mcsim_gpu::Engine gpu(b.recipe, opt);
     return compare(ref, gpu, b.recipe, t_ms);
   } catch (const std::exception& e) {

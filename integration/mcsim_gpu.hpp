@@ -17,6 +17,8 @@
 // own Checkpoint type; either engine restores the other's.
 #pragma once
 
+#include <array>
+#include <cstdint>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -239,6 +241,20 @@ class FlatRecipe {
   mcg_recipe view_{};
 };
 
+// one rank of a sharded engine (one process per GPU): this rank's index, the
+// rank count, its device, and the NCCL id made by nccl_unique_id() on one rank
+// and shared by the caller (MPI_Bcast, a file, torch.distributed, ...)
+struct Shard {
+  int rank = 0, world = 1, device = 0;
+  std::array<std::uint8_t, 128> nccl_id{};
+};
+
+inline std::array<std::uint8_t, 128> nccl_unique_id() {
+  std::array<std::uint8_t, 128> id{};
+  check(mcg_nccl_unique_id(id.data()));
+  return id;
+}
+
 class Engine {
  public:
   Engine(const mcsim::Recipe& recipe, const mcsim::EngineOptions& opt, int device = 0)
@@ -247,6 +263,19 @@ class Engine {
     const mcg_options o{opt.dt_ms, opt.seed, opt.workers, device, 0, 1};
     check(mcg_create(flat.view(), &o, &eng_));
     dt_ = mcg_dt_ms(eng_);
+  }
+  // a shard: this rank's cells (contiguous gid range, mcg_partition) with the
+  // spike exchange inside the library (ncclAllGather once per min-delay
+  // epoch, engine.cpp:913-942); spikes() is the global list, cell(gid) is
+  // defined for this rank's gids.  make_checkpoint / restore / fast_forward_to
+  // are refused, as mcg_* refuses them for a sharded engine.
+  Engine(const mcsim::Recipe& recipe, const mcsim::EngineOptions& opt, const Shard& shard)
+      : recipe_(recipe), sharded_(true) {
+    const FlatRecipe flat(recipe);
+    const mcg_options o{opt.dt_ms, opt.seed, opt.workers, shard.device, shard.rank, shard.world};
+    check(mcg_create(flat.view(), &o, &eng_));
+    dt_ = mcg_dt_ms(eng_);
+    check(mcg_shard_init_nccl(eng_, shard.nccl_id.data()));
   }
   ~Engine() {
     if (eng_) mcg_destroy(eng_);
@@ -260,7 +289,7 @@ class Engine {
 
   void advance_to(double t_ms) {
     flush_mirrors();
-    check(mcg_advance_to(eng_, t_ms));
+    check(sharded_ ? mcg_shard_advance_to(eng_, t_ms) : mcg_advance_to(eng_, t_ms));
     invalidate();
   }
   void fast_forward_to(double t_ms, double coarse_dt_ms) {
@@ -271,10 +300,12 @@ class Engine {
 
   const std::vector<mcsim::SpikeRecord>& spikes() const {
     if (!spikes_ok_) {
-      const int64_t n = mcg_num_spikes(eng_);
+      const int64_t n = sharded_ ? mcg_shard_num_global_spikes(eng_) : mcg_num_spikes(eng_);
       std::vector<double> t(static_cast<std::size_t>(n));
       std::vector<uint32_t> g(static_cast<std::size_t>(n));
-      if (n > 0) check(mcg_get_spikes(eng_, 0, n, t.data(), g.data()));
+      if (n > 0)
+        check(sharded_ ? mcg_shard_get_global_spikes(eng_, 0, n, t.data(), g.data())
+                       : mcg_get_spikes(eng_, 0, n, t.data(), g.data()));
       spikes_.resize(static_cast<std::size_t>(n));
       for (int64_t i = 0; i < n; ++i) spikes_[i] = {t[i], g[i]};
       spikes_ok_ = true;
@@ -331,6 +362,7 @@ class Engine {
   }
 
   mcg_engine* handle() { return eng_; }
+  bool sharded() const { return sharded_; }
 
  private:
   template <class T>
@@ -440,6 +472,7 @@ class Engine {
 
   mcsim::Recipe recipe_;
   mcg_engine* eng_ = nullptr;
+  bool sharded_ = false;
   double dt_ = 0.0;
   std::map<uint32_t, mcsim::CellRT> cells_;
   mutable std::vector<mcsim::SpikeRecord> spikes_;
