@@ -294,6 +294,15 @@ mcg_status mcg_shard_get_global_spikes(mcg_engine* eng, int64_t first, int64_t c
 /* the shard bounds mcg_create uses for (recipe, world): rank r owns gids
  * [bounds[r], bounds[r+1]); bounds has world + 1 entries.  Host only (no GPU). */
 mcg_status mcg_partition(const mcg_recipe* recipe, int32_t world, uint32_t* bounds);
+/* Host only (no GPU): run the recipe -> runtime build (Impl::build,
+ * engine.cpp:189-408) with `threads` host threads (<= 0: the default) and
+ * return a digest of the resulting layout (edges in rank order, instances,
+ * CSR, queues): out = {FNV-1a hash, edges, instances, min_delay_steps}.
+ * Errors are the build's (the reference's messages, first failing connection
+ * first).  Used to check that the threaded build is independent of the
+ * thread count. */
+mcg_status mcg_build_digest(const mcg_recipe* recipe, const mcg_options* opt, int32_t threads,
+                            uint64_t out[4]);
 
 /* ---- instrumentation (bench.py) -------------------------------------------- */
 

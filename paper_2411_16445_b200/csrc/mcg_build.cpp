@@ -284,7 +284,7 @@ struct StageTimer {
 };
 }  // namespace
 
-void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
+void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m, int threads) {
   StageTimer tm;
   const double dt = opt.dt_ms;
   m.dt = dt;
@@ -606,7 +606,7 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m) {
       int64_t err_ci = -1;
       std::exception_ptr err;
     };
-    const int nthr0 = build_threads(nconn);
+    const int nthr0 = threads > 0 ? threads : build_threads(nconn);
     std::vector<Part> parts(nthr0);
     auto scan = [&](int t) {
       Part& P = parts[t];

@@ -154,7 +154,8 @@ bool eliminate_constant(int n, const int32_t* parent, const double* cap, const d
 int chain_schedule(int n, const int32_t* parent, std::vector<int32_t>& idx, int& a_first);
 
 // Materialize; throws mcg::Error with the reference's messages.
-void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m);
+// threads <= 0: build_threads() (MCG_BUILD_THREADS or the hardware threads)
+void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m, int threads = 0);
 
 // Shard assignment: contiguous gid ranges balanced by (compartments +
 // synapse instances); identical on every rank.

@@ -2379,6 +2379,62 @@ mcg_status mcg_partition(const mcg_recipe* recipe, int32_t world, uint32_t* boun
   });
 }
 
+mcg_status mcg_build_digest(const mcg_recipe* recipe, const mcg_options* opt, int32_t threads,
+                            uint64_t out[4]) {
+  return guarded([&] {
+    if (!recipe || !opt || !out) throw mcg::Error(MCG_ERR_ARGUMENT, "build_digest: null pointer");
+    mcg::HostModel m;
+    mcg::build_model(*recipe, *opt, m, threads);
+    uint64_t h = 1469598103934665603ull;  // FNV-1a over the layout
+    auto mix = [&](uint64_t x) {
+      h ^= x;
+      h *= 1099511628211ull;
+    };
+    auto mixd = [&](double x) {
+      uint64_t b;
+      std::memcpy(&b, &x, 8);
+      mix(b);
+    };
+    for (size_t i = 0; i < m.e_dst.size(); ++i) {
+      mix(uint64_t(m.e_dst[i]));
+      mix(uint64_t(m.e_group[i]));
+      mix(m.e_inst[i]);
+      mix(m.e_src[i]);
+      mix(m.e_seq[i]);
+      mix(uint64_t(m.e_delay[i]));
+      mix(uint64_t(int64_t(m.e_comp[i])));
+      mixd(m.e_weight[i]);
+      mixd(m.e_wcf[i]);
+    }
+    for (size_t i = 0; i < m.i_comp.size(); ++i) {
+      mix(uint64_t(m.i_comp[i]));
+      mixd(m.i_weight[i]);
+      mixd(m.i_stc_h[i]);
+    }
+    for (double x : m.i_stdp_w) mixd(x);
+    for (double x : m.i_homeo_w) mixd(x);
+    for (int64_t x : m.src_edge_off) mix(uint64_t(x));
+    for (int64_t x : m.src_edges) mix(uint64_t(x));
+    for (int64_t x : m.out_begin) mix(uint64_t(x));
+    for (int64_t x : m.out_end) mix(uint64_t(x));
+    for (const McgCellGroup& G : m.cgs) {
+      mix(uint64_t(G.inst));
+      mix(uint64_t(G.size));
+      mix(uint64_t(int64_t(G.fifo)));
+    }
+    for (const McgFifo& F : m.fifos) {
+      mix(uint64_t(F.base));
+      mix(uint64_t(F.cap));
+    }
+    mix(uint64_t(m.min_delay_steps));
+    mix(uint64_t(m.max_delay_steps));
+    out[0] = h;
+    out[1] = m.e_dst.size();
+    out[2] = uint64_t(m.n_inst);
+    out[3] = uint64_t(m.min_delay_steps);
+  });
+}
+
 mcg_status mcg_shard_run_epoch(mcg_engine* eng, double t_ms) {
   return guarded([&] { eng->e.run_epoch(t_ms); });
 }
