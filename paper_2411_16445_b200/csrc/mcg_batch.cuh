@@ -1392,10 +1392,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
       __syncthreads();
       MCG_PH(0);
     }
-    // ---- A. delivery (owner thread): inbox, then internal (engine.cpp:549-560);
-    // the other threads clear the STC changed flags of the step
-    if (A.stc_sm && tid >= nc)
-      for (int w = tid - nc; w <= (stc_total >> 5); w += T - nc) B.fmask[w] = 0u;
+    // ---- A. delivery (owner thread): inbox, then internal (engine.cpp:549-560)
     if (tid < nc) {
       const int c = c0 + tid;
       McgCellSm& X = cs[tid];
@@ -1578,6 +1575,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
             const double h = B.stc[f], cc = B.stc[2 * S4 + f], a = B.stc[3 * S4 + f];
             if (mcg_stc_at_rest(R, late, prp, h, cc, a)) {
               B.stc[2 * S4 + f] = cc * R.cf;  // the step reduces to the calcium decay
+              B.dbuf[f] = -0.0;               // no SPS change (the additive identity)
               continue;
             }
             McgStcVal v{h, B.stc[S4 + f], cc, a};
@@ -1589,10 +1587,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
             B.stc[S4 + f] = v.z;
             B.stc[2 * S4 + f] = v.c;
             B.stc[3 * S4 + f] = v.a;
-            if (changed) {
-              B.dbuf[f] = delta;
-              atomicOr(&B.fmask[f >> 5], 1u << (f & 31));
-            }
+            B.dbuf[f] = changed ? delta : -0.0;
           }
         }
       };
@@ -1655,10 +1650,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
             if (changed) D.i_sps_abs[jj[u]] = v[u].a;
           }
         }
-        const unsigned bal = __ballot_sync(MCG_FULL, changed);
-        const int fw = (r0 + u) * T + (tid - lane);
-        if (changed) B.dbuf[f] = dlt[u];
-        if (lane == 0) B.fmask[fw >> 5] = bal;
+        if (jj[u] >= 0) B.dbuf[f] = changed ? dlt[u] : -0.0;
       }
     }
     MCG_PH(16);
@@ -1679,35 +1671,23 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
         for (int q = 0; q < X.n_stc_seg; ++q) {
           const McgSegSm& g = B.seg[tid * A.n_stc_max + q];
           const int fe = f + g.size;
-          // every instance of a placement sits on the placement's compartment
+          // every instance of a placement sits on the placement's compartment;
+          // every slot holds its delta or -0.0 (unchanged: x + -0.0 == x for
+          // every x), so the in-order fold is one dependent add per instance,
+          // its loads issued eight ahead
           double acc = sps[g.comp];
-          while (f < fe) {
-            // the segment's changed slots of this 32-slot word, in instance order
-            const int w = f >> 5, lo = f & 31;
-            const int lim = min(32 - lo, fe - f);
-            uint32_t bits = B.fmask[w] >> lo;
-            if (lim < 32) bits &= (1u << lim) - 1u;
-            // up to four slots' loads are issued ahead of their in-order adds
-            while (bits) {
-              const int i0 = __ffs(bits) - 1;
-              bits &= bits - 1u;
-              const int i1 = bits ? __ffs(bits) - 1 : -1;
-              bits &= bits - 1u;
-              const int i2 = bits ? __ffs(bits) - 1 : -1;
-              bits &= bits - 1u;
-              const int i3 = bits ? __ffs(bits) - 1 : -1;
-              bits &= bits - 1u;
-              const double a0 = B.dbuf[f + i0];
-              const double a1 = i1 >= 0 ? B.dbuf[f + i1] : 0.0;
-              const double a2 = i2 >= 0 ? B.dbuf[f + i2] : 0.0;
-              const double a3 = i3 >= 0 ? B.dbuf[f + i3] : 0.0;
-              acc += a0;
-              if (i1 >= 0) acc += a1;
-              if (i2 >= 0) acc += a2;
-              if (i3 >= 0) acc += a3;
-            }
-            f += lim;
+          const double* d = B.dbuf + f;
+          const int nseg = fe - f;
+          int i = 0;
+          for (; i + 8 <= nseg; i += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = d[i + u];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc += v[u];
           }
+          for (; i < nseg; ++i) acc += d[i];
+          f = fe;
           sps[g.comp] = acc;
         }
       }
