@@ -1531,9 +1531,9 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
             hg = true;
             __syncwarp();
           }
-          mcg_decay_active(D, G, S.f_decay, true, M.gsyn, M.gsyn_rhs, S.e_rev, lane);
+          mcg_decay_active(D, G, S.f_decay, true, M.gsyn, M.gsyn_rhs, S.e_rev, S.comp, lane);
         } else if (S.kind == MCG_SYN_STATIC_CURRENT || S.kind == MCG_SYN_HOMEO_CURRENT) {
-          if (mcg_decay_active(D, G, S.f_decay, false, M.rhs_cur, nullptr, 0.0, lane)) hc = true;
+          if (mcg_decay_active(D, G, S.f_decay, false, M.rhs_cur, nullptr, 0.0, S.comp, lane)) hc = true;
         }
       }
       if (lane == 0) {
@@ -1541,6 +1541,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
         cs[k].has_current = hc;
       }
     }
+    MCG_PH(18);
     // ---- C. STC synapses of every cell of the batch, one flat index space
     // (engine.cpp:617-646), four instances per thread in flight; changed
     // flags as warp ballots for the fold

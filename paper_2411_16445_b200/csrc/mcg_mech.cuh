@@ -6,80 +6,63 @@
 #include "mcg_device.cuh"
 
 
-// decay an active list, fold kept kernels in active-list order (engine.cpp:578-616)
+// decay an active list, fold kept kernels in active-list order (engine.cpp:578-616).
+// Every instance of a group sits on the placement's compartment `comp`
+// (append_instance(g, pl.comp, ...), engine.cpp:330-372), so the fold is one
+// running sum (two for conductances) in registers, read and written once.  A
+// chunk of 32 kernels is folded lane by lane from shuffles: dropped kernels
+// contribute -0.0, the identity of fp64 addition, so dense chunks need no
+// per-lane branch; sparse chunks (few kept) take only the kept lanes.
 __device__ __forceinline__ bool mcg_decay_active(const McgDev& D, McgCellGroup* G, double f,
                                                  bool cond, double* acc, double* acc2,
-                                                 double erev, int lane) {
+                                                 double erev, int comp, int lane) {
   const int na = G->active_n;
+  if (na == 0) return false;
   const int64_t base = G->inst;
   int out = 0;
-  // the reference's in-order fold acc[comp] += kv (and acc2[comp] += kv * erev),
-  // run by every lane on shuffled values with the running sums in registers
-  // while consecutive kernels share a compartment (they usually all do)
-  int rc = -1;
-  double r1 = 0.0, r2 = 0.0;
+  double r1 = acc[comp];
+  double r2 = cond ? acc2[comp] : 0.0;
+  int i_next = lane < na ? D.i_active[base + lane] : 0;  // index loads one chunk ahead
   for (int a0 = 0; a0 < na; a0 += 32) {
     const int a = a0 + lane;
-    int i = 0, comp = 0;
+    const int i = i_next;
+    i_next = (a + 32 < na) ? D.i_active[base + a + 32] : 0;
     double kv = 0.0;
     bool keep = false;
     if (a < na) {
-      i = D.i_active[base + a];
       const int64_t j = base + i;
       kv = D.i_kernel[j] * f;
       if (cond ? (kv < 1e-30) : (fabs(kv) < 1e-30)) kv = 0.0;
       D.i_kernel[j] = kv;
       keep = kv != 0.0;
-      comp = D.i_comp[j];
     }
     const unsigned m = __ballot_sync(MCG_FULL, keep);
-    __syncwarp();
+    // compaction: the slots written, [out, out + popc), lie below a0 + 32,
+    // and the next chunk's indices are already in registers
     if (keep) D.i_active[base + out + __popc(m & mcg_lanemask_lt())] = i;
-    unsigned mm = m;
-    while (mm) {
-      // up to four kept kernels per batch of shuffles, folded in order
-      int l[4];
-      int cnt = 0;
+    const double c1 = keep ? kv : -0.0;
+    const double c2 = keep ? kv * erev : -0.0;
+    if (__popc(m) > 8) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        l[u] = mm ? __ffs(mm) - 1 : 0;
-        if (mm) {
-          mm &= mm - 1;
-          cnt = u + 1;
-        }
+      for (int l = 0; l < 32; ++l) {
+        r1 += __shfl_sync(MCG_FULL, c1, l);
+        if (cond) r2 += __shfl_sync(MCG_FULL, c2, l);
       }
-      double kl[4];
-      int cl[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        kl[u] = __shfl_sync(MCG_FULL, kv, l[u]);
-        cl[u] = __shfl_sync(MCG_FULL, comp, l[u]);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (u >= cnt) break;
-        if (cl[u] != rc) {
-          if (rc >= 0 && lane == 0) {
-            acc[rc] = r1;
-            if (cond) acc2[rc] = r2;
-          }
-          __syncwarp();
-          rc = cl[u];
-          r1 = acc[rc];
-          if (cond) r2 = acc2[rc];
-        }
-        r1 += kl[u];
-        if (cond) r2 += kl[u] * erev;
+    } else {
+      for (unsigned mm = m; mm; mm &= mm - 1) {
+        const int l = __ffs(mm) - 1;
+        r1 += __shfl_sync(MCG_FULL, c1, l);
+        if (cond) r2 += __shfl_sync(MCG_FULL, c2, l);
       }
     }
     out += __popc(m);
   }
-  if (rc >= 0 && lane == 0) {
-    acc[rc] = r1;
-    if (cond) acc2[rc] = r2;
-  }
   __syncwarp();
-  if (lane == 0) G->active_n = out;
+  if (lane == 0) {
+    acc[comp] = r1;  // r1 + (-0.0) * k == r1: unchanged when nothing was kept
+    if (cond) acc2[comp] = r2;
+    G->active_n = out;
+  }
   __syncwarp();
   return out > 0;
 }
