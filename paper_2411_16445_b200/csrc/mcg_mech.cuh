@@ -22,23 +22,29 @@ __device__ __forceinline__ bool mcg_decay_active(const McgDev& D, McgCellGroup* 
   int out = 0;
   double r1 = acc[comp];
   double r2 = cond ? acc2[comp] : 0.0;
-  int i_next = lane < na ? D.i_active[base + lane] : 0;  // index loads one chunk ahead
+  // loads run ahead of the chunk being folded: kernels one chunk, indices two
+  int i_cur = lane < na ? D.i_active[base + lane] : 0;
+  double k_cur = lane < na ? D.i_kernel[base + i_cur] : 0.0;
+  int i_nx = lane + 32 < na ? D.i_active[base + lane + 32] : 0;
   for (int a0 = 0; a0 < na; a0 += 32) {
     const int a = a0 + lane;
-    const int i = i_next;
-    i_next = (a + 32 < na) ? D.i_active[base + a + 32] : 0;
+    const int i = i_cur;
+    const double k_nx = (a + 32 < na) ? D.i_kernel[base + i_nx] : 0.0;
+    const int i_nx2 = (a + 64 < na) ? D.i_active[base + a + 64] : 0;
     double kv = 0.0;
     bool keep = false;
     if (a < na) {
-      const int64_t j = base + i;
-      kv = D.i_kernel[j] * f;
+      kv = k_cur * f;
       if (cond ? (kv < 1e-30) : (fabs(kv) < 1e-30)) kv = 0.0;
-      D.i_kernel[j] = kv;
+      D.i_kernel[base + i] = kv;
       keep = kv != 0.0;
     }
+    i_cur = i_nx;
+    k_cur = k_nx;
+    i_nx = i_nx2;
     const unsigned m = __ballot_sync(MCG_FULL, keep);
     // compaction: the slots written, [out, out + popc), lie below a0 + 32,
-    // and the next chunk's indices are already in registers
+    // and the next two chunks' indices are already in registers
     if (keep) D.i_active[base + out + __popc(m & mcg_lanemask_lt())] = i;
     const double c1 = keep ? kv : -0.0;
     const double c2 = keep ? kv * erev : -0.0;
