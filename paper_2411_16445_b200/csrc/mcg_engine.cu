@@ -583,16 +583,30 @@ struct Engine {
     const int S = sp_max;
     // every cell of a group has 2 (1 + S) system lanes (mcg_wg_epoch phase D)
     const int g_max = std::max(1, std::min(MCG_WG_MAX, 32 / (2 * (1 + S))));
-    wg_G = g_max;
-    if (const char* gv = std::getenv("MCG_WARP_G")) wg_G = std::clamp(std::atoi(gv), 1, g_max);
-    wg_groups = (nl + wg_G - 1) / wg_G;
     wg_specs_sm = m.specs.size() * sizeof(McgSpec) <= 16 * 1024 ? static_cast<int32_t>(m.specs.size()) : 0;
     wg_ev_cap = 128;
     if (const char* ev = std::getenv("MCG_WARP_EVCAP")) wg_ev_cap = std::max(0, std::atoi(ev));
-    wg_warp_doubles = mcg_warp_region_doubles(wg_G, smem_n, S, wg_P, wg_MW, wg_ev_cap);
     const size_t fixed = size_t(wg_kind_doubles) * 8 + ((m.kinds.size() * sizeof(McgKind) + 7) / 8) * 8 +
                         ((size_t(wg_specs_sm) * sizeof(McgSpec) + 7) / 8) * 8;
     const size_t lim = size_t(smem_optin) - 2048;
+    auto warps_fit = [&](int g) {  // warps per CTA that fit the shared memory with groups of g
+      const size_t wd = size_t(mcg_warp_region_doubles(g, smem_n, S, wg_P, wg_MW, wg_ev_cap)) * 8;
+      return fixed + wd > lim ? 0 : static_cast<int>(std::min<size_t>(8, (lim - fixed) / wd));
+    };
+    // group size: each warp's step is a latency-bound chain whose length
+    // hardly depends on G, so more, smaller groups put more warps on each SM
+    // (config 3: G = 2 runs 10-15 % faster than G = 5); the smallest G >= 2
+    // that keeps every group resident, else the largest (fewer groups to
+    // stage per epoch)
+    wg_G = g_max;
+    for (int g = std::min(2, g_max); g <= g_max; ++g)
+      if ((nl + g - 1) / g <= dev_sms * warps_fit(g)) {
+        wg_G = g;
+        break;
+      }
+    if (const char* gv = std::getenv("MCG_WARP_G")) wg_G = std::clamp(std::atoi(gv), 1, g_max);
+    wg_groups = (nl + wg_G - 1) / wg_G;
+    wg_warp_doubles = mcg_warp_region_doubles(wg_G, smem_n, S, wg_P, wg_MW, wg_ev_cap);
     if (fixed + size_t(wg_warp_doubles) * 8 > lim) {
       if (std::getenv("MCG_VERBOSE")) std::fprintf(stderr, "engine: k_batch (warp region too large)\n");
       return;
