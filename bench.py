@@ -25,6 +25,7 @@ spontaneous phase and the onset of the 100 Hz learning stimulus at 10 s).
 (rank 0 only) and prints the same JSON line with "impl": "reference".
 """
 import argparse
+import gc
 import json
 import math
 import os
@@ -284,6 +285,8 @@ def other_configs():
         ne = n * 4 // 5
         c = N.ConsolidationConfig(n_cells=n, n_exc=ne, p_conn=min(0.1, 0.1 * 1600 / ne), seed=SEED,
                                   multi_compartment=True, dend_size=dend, dt_ms=DT_MS)
+        e = b = None  # the previous configuration's engine and recipe released first
+        gc.collect()
         t0 = _t.perf_counter()
         b = N.build_consolidation_network(c, True)
         e = Engine(b.recipe, EngineOptions(DT_MS, SEED))
