@@ -122,6 +122,7 @@ struct McgWCell {
   int32_t stc_n, stc_comp, stc_spec, stc_gi, fifo, f_cap;
   uint32_t iseq;
   int32_t armed, lif, noise, fired, refractory, has_current, n_groups;
+  int32_t probe0, probe1;  // the cell's probe range (D.probe_off), read once per entry
   int32_t prp_off;       // mcg_smem offset of PRP at the STC compartment (-1: no pool)
   int32_t sps_off;       // mcg_smem offset of SPS at the STC compartment (-1: none)
   int32_t base;          // mcg_smem offset of the cell block
@@ -229,6 +230,8 @@ __device__ void mcg_wg_enter(const McgDev& D, const McgWarpArgs& A, const McgWar
       X.nsp = 0;
       X.staged = 0;
       X.next_due = INT64_MAX;
+      X.probe0 = D.probe_off[c];
+      X.probe1 = D.probe_off[c + 1];
       const int64_t cg0 = D.cg_off[c];
       for (int gi = 0; gi < K.n_groups && gi < 8; ++gi) {
         const McgCellGroup Gr = D.cgs[cg0 + gi];
@@ -958,7 +961,7 @@ __device__ void mcg_wg_epoch(const McgDev& D, const McgWarpArgs& A, const McgWar
         }
         X.det_prev = V[K.detector_comp];
       }
-      const int p0 = D.probe_off[X.c], p1 = D.probe_off[X.c + 1];
+      const int p0 = X.probe0, p1 = X.probe1;
       for (int q = p0; q < p1; ++q) {
         const int p = D.probe_idx[q];
         const McgProbe& Pr = D.probes[p];
