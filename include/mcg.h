@@ -326,6 +326,14 @@ typedef struct {
 mcg_status mcg_get_stats(mcg_engine* eng, mcg_stats* out);
 /* enable/disable CUDA-event timing of the epoch kernel (adds one event pair per epoch) */
 mcg_status mcg_set_timing(mcg_engine* eng, int32_t enabled);
+/* Independent trials in one engine (the stc-protocols experiment,
+ * experiments.cpp:262-289, runs run_stc_protocol(cfg, p, t) for t < trials,
+ * each an Engine with seed cfg.seed + t and one cell, gid 0): cell c of this
+ * engine draws its random numbers with the key (seeds[c], key_gids[c], ...)
+ * instead of (options.seed, c, ...).  seeds / key_gids have one entry per
+ * cell.  Only for the point-cell kernel (k_point): MCG_ERR_ENGINE otherwise.
+ * Not part of mcsim::Engine; protocols.run_stc_protocols uses it. */
+mcg_status mcg_set_cell_rng(mcg_engine* eng, const uint64_t* seeds, const uint32_t* key_gids);
 
 /* ---- device numerics (differential tests of the glibc-faithful ports) ---- */
 

@@ -109,6 +109,11 @@ struct McgDev {
   // status
   int32_t* err;
   unsigned long long* delivered;
+  // optional per-cell RNG key override (mcg_set_cell_rng; k_point only):
+  // cell c draws with key (cell_seed[c], cell_key_gid[c], ...) instead of
+  // (seed, gid0 + c, ...): independent trials of one protocol in one engine
+  const uint64_t* cell_seed;
+  const uint32_t* cell_key_gid;
 };
 
 // x / d, bitwise IEEE division, from y = mcg_recip(d) = RN(1/d): with

@@ -284,6 +284,8 @@ struct Engine {
   // register-resident kernel for independent point cells (mcg_point.cuh)
   bool use_point = false;
   bool pt_small = false;  // every cell fits k_point<1, 2>
+  DBuf<uint64_t> d_cell_seed;      // per-cell RNG key override (mcg_set_cell_rng)
+  DBuf<uint32_t> d_cell_key_gid;
   int32_t pt_grid = 1;
   bool lazy_dirty = false;  // resting synapses' calcium lags `step` (k_warp ran since the last flush)
   cudaEvent_t evk0 = nullptr, evk1 = nullptr;
@@ -1112,6 +1114,8 @@ struct Engine {
     D.trace_base = d_trace_base.p;
     D.err = d_err.p;
     D.delivered = d_ctr.p + C_DELIVERED;
+    D.cell_seed = d_cell_seed.n ? d_cell_seed.p : nullptr;
+    D.cell_key_gid = d_cell_key_gid.n ? d_cell_key_gid.p : nullptr;
   }
 
   McgEv ev_dev() {
@@ -2358,6 +2362,21 @@ mcg_status mcg_get_stats(mcg_engine* eng, mcg_stats* out) {
     *out = eng->e.stats;
   });
 }
+mcg_status mcg_set_cell_rng(mcg_engine* eng, const uint64_t* seeds, const uint32_t* key_gids) {
+  return guarded([&] {
+    mcg::Engine& E = eng->e;
+    if (!E.use_point)
+      throw mcg::Error(MCG_ERR_ENGINE, "per-cell RNG keys need the point-cell kernel (k_point)");
+    const int nl = E.n_local();
+    std::vector<uint64_t> sd(seeds, seeds + nl);
+    std::vector<uint32_t> kg(key_gids, key_gids + nl);
+    E.d_cell_seed.upload(sd, E.st);
+    E.d_cell_key_gid.upload(kg, E.st);
+    E.refresh_dev();
+    mcg::cuda_check(cudaStreamSynchronize(E.st), "cudaStreamSynchronize");
+  });
+}
+
 mcg_status mcg_set_timing(mcg_engine* eng, int32_t enabled) {
   return guarded([&] { eng->e.timing = enabled != 0; });
 }

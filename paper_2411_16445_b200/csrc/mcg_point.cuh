@@ -88,6 +88,10 @@ __device__ void mcg_pt_run(const McgDev& D, const McgPointArgs& A, int c, int32_
   const McgKind& Kg = D.kinds[D.cell_kind[c]];  // global copy: the rare probe path reads it
   const McgKind K = Kg;
   const uint32_t gid = D.gid0 + uint32_t(c);
+  // RNG key of this cell: (seed, gid) unless overridden per cell (independent
+  // trials in one engine, mcg_set_cell_rng)
+  const uint64_t kseed = D.cell_seed ? D.cell_seed[c] : D.seed;
+  const uint32_t kgid = D.cell_key_gid ? D.cell_key_gid[c] : gid;
   const int64_t cg0 = D.cg_off[c];
   // ---- state into registers
   double V = D.v[D.comp_off[c]];
@@ -251,7 +255,7 @@ __device__ void mcg_pt_run(const McgDev& D, const McgPointArgs& A, int c, int32_
       for (int i = 0; i < NSTC; ++i) {
         if (i < stc_n) {
           double delta = 0.0;
-          const bool changed = mcg_stc_step(Sp, D.dt, D.seed, gid, stc_gi, i, s, late, prp, vol, rvol, st[i],
+          const bool changed = mcg_stc_step(Sp, D.dt, kseed, kgid, stc_gi, i, s, late, prp, vol, rvol, st[i],
                                             delta, D.stc_nz + stc_inst + i);
           if (changed && K.sps_idx >= 0) {
 #pragma unroll
@@ -412,7 +416,8 @@ __global__ void __launch_bounds__(MCG_PT_THREADS, 1) k_point(const __grid_consta
       // background normals of [s0, s1): step n takes half n & 1 of pair n >> 1,
       // pair p of Threefry block p >> 1 (rng.cpp:67-78)
       if (K.has_bg && K.sig_bg != 0.0) {
-        const mcg_key key = mcg_make_key(D.seed, D.gid0 + uint32_t(c), 1, 0);
+        const mcg_key key = mcg_make_key(D.cell_seed ? D.cell_seed[c] : D.seed,
+                                         D.cell_key_gid ? D.cell_key_gid[c] : D.gid0 + uint32_t(c), 1, 0);
         const int64_t pa = s0 >> 1, pb = (s1 - 1) >> 1;
         for (int64_t pr = pa + tid; pr <= pb; pr += blockDim.x) {
           uint64_t x[4];

@@ -345,6 +345,16 @@ class Engine:
     def set_timing(self, enabled: bool):
         _check(A.lib().mcg_set_timing(self._h, 1 if enabled else 0))
 
+    def set_cell_rng(self, seeds, key_gids):
+        """Per-cell RNG keys (mcg_set_cell_rng): cell c draws with (seeds[c],
+        key_gids[c]) instead of (options.seed, c) -- independent trials of a
+        single-cell protocol in one engine (point-cell kernel only)."""
+        sd = np.ascontiguousarray(seeds, dtype=np.uint64)
+        kg = np.ascontiguousarray(key_gids, dtype=np.uint32)
+        if len(sd) != self.num_cells() or len(kg) != self.num_cells():
+            raise ValueError("set_cell_rng: one seed and one key gid per cell")
+        _check(A.lib().mcg_set_cell_rng(self._h, sd.ctypes.data_as(C.c_void_p), kg.ctypes.data_as(C.c_void_p)))
+
     # ---- sharded epoch loop (include/mcg.h; driven by shard.ShardedEngine) ----
     def shard_spike_cap(self) -> int:
         return int(A.lib().mcg_shard_spike_cap(self._h))

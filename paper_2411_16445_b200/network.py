@@ -17,7 +17,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 from dataclasses import dataclass, field, replace
-from typing import List, Optional, Tuple
+from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -457,6 +457,72 @@ def run_stc_protocol(cfg: StcSingleConfig, proto: int, trial: int, device: int =
     g = eng.cell(0).groups[0]
     return StcRunResult(float(g.stc_h[0]), float(g.stc_z[0]), float(eng.cell(0).species[1][0]),
                         max_dh, max_dh > cfg.stc.theta_tag_mV, max_dh > cfg.stc.theta_pro_mV, tr)
+
+
+def run_stc_protocols(cfg: StcSingleConfig, protocols: Sequence[int], trials: int, device: int = 0,
+                      max_cells: int = 128) -> List[List["StcRunResult"]]:
+    """The stc-protocols experiment (experiments.cpp:262-289) on the device:
+    run_stc_protocol(cfg, p, t) for every protocol p and trial t < trials,
+    results[i][t] for protocols[i], each bitwise the single-trial run.
+
+    Trials are independent single-cell simulations that differ only in the
+    seed (cfg.seed + t) and share the stimulus times, so one engine holds up to
+    `max_cells` trials as cells of one recipe (same kind, one shared scripted
+    source, four probes per cell) with per-cell RNG keys (seed + t, gid 0:
+    mcg_set_cell_rng), and runs them on the point-cell kernel, one cell per
+    CTA; the protocols' engines run concurrently on their own streams."""
+    import threading
+    jobs = []
+    for pi, proto in enumerate(protocols):
+        for t0 in range(0, trials, max_cells):
+            jobs.append((pi, proto, list(range(t0, min(trials, t0 + max_cells)))))
+    out: List[List[Optional[StcRunResult]]] = [[None] * trials for _ in protocols]
+    errors: List[BaseException] = []
+
+    def run(pi, proto, tids):
+        try:
+            times = stc_protocol_times(proto, cfg.t_onset_ms)
+            t_last = times[-1] if times else cfg.t_onset_ms
+            one = build_stc_single(cfg, times)
+            t_detailed = math.ceil((t_last + 2000.0) / 1000.0) * 1000.0
+            kind = one.kinds[0]
+            kind.membrane.bg_quiet_t0_ms = t_detailed - 500.0
+            kind.membrane.bg_quiet_t1_ms = cfg.t_eval_ms
+            n = len(tids)
+            every = one.probes[0].every_steps
+            probes = []
+            for c in range(n):  # the single-trial probes, per cell
+                probes += [replace(p, gid=c) for p in one.probes]
+            r = Recipe(kinds=[kind], cell_kind=[0] * n, sources=list(one.sources),
+                       connections=ConnectionTable(1, [0] * n, list(range(n)), ["syn"], 0, 0, 1.0, cfg.dt_ms),
+                       probes=probes)
+            eng = Engine(r, EngineOptions(cfg.dt_ms, cfg.seed, 1), device=device)
+            eng.set_cell_rng([cfg.seed + t for t in tids], [0] * n)
+            eng.advance_to(t_detailed)
+            span = cfg.t_eval_ms - t_detailed
+            n_coarse = math.floor(span / cfg.coarse_dt_ms)
+            eng.fast_forward_to(t_detailed + n_coarse * cfg.coarse_dt_ms, cfg.coarse_dt_ms)
+            tr = eng.traces()
+            for c, t in enumerate(tids):
+                hs = [v for _, v in tr[4 * c]]
+                max_dh = max([abs(h - cfg.stc.h0_mV) for h in hs], default=0.0)
+                g = eng.cell(c).groups[0]
+                out[pi][t] = StcRunResult(float(g.stc_h[0]), float(g.stc_z[0]), float(eng.cell(c).species[1][0]),
+                                          max_dh, max_dh > cfg.stc.theta_tag_mV, max_dh > cfg.stc.theta_pro_mV,
+                                          tr[4 * c:4 * c + 4])
+            eng.close()
+            del every
+        except BaseException as e:  # noqa: BLE001
+            errors.append(e)
+
+    th = [threading.Thread(target=run, args=j) for j in jobs]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    if errors:
+        raise errors[0]
+    return out
 
 
 # ---- busyring (bench.hpp / bench.cpp) ---------------------------------------------
