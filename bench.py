@@ -365,7 +365,38 @@ def other_configs():
                                       "wall_s": wall,
                                       "trial_steps_per_s": len(deltas) * proto.trials * n_steps / wall,
                                       "mean_change": [pt.mean_change for pt in curve]}
+    out["config1_stc_protocols"] = stc_protocols_config()
     return out
+
+
+def stc_protocols_config(trials=10):
+    """Config 1 as the reference runs it: the stc-protocols experiment
+    (experiments.cpp:262-289; 4 protocols x 10 trials of run_stc_protocol, the
+    single STC synapse on a point neuron, each trial to 5 h with fast-forward).
+    B200: trials as cells of one engine per protocol (network.run_stc_protocols);
+    reference: oracle/_ref, the trials one after another on one core, as the
+    experiment does.  Wall clock, both including engine construction."""
+    import time as _t
+    from paper_2411_16445_b200 import network as N
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import ref
+    cfg = N.StcSingleConfig()
+    protos = [N.StcProtocol.stet, N.StcProtocol.wtet, N.StcProtocol.slfs, N.StcProtocol.wlfs]
+    N.run_stc_protocols(cfg, [N.StcProtocol.wtet], 1)  # module load, context
+    t0 = _t.perf_counter()
+    res = N.run_stc_protocols(cfg, protos, trials)
+    t1 = _t.perf_counter()
+    same = True
+    for pi, p in enumerate(protos):
+        for t in range(trials):
+            h, z, prp = ref.run_stc_protocol(p, t)
+            g = res[pi][t]
+            same = same and (g.h_final, g.z_final, g.p_final) == (h, z, prp)
+    t2 = _t.perf_counter()
+    return {"protocols": 4, "trials": trials, "wall_s": t1 - t0,
+            "reference": {"wall_s": t2 - t1, "kind": "reference (oracle/_ref)", "cores": 1},
+            "speedup_vs_reference": (t2 - t1) / (t1 - t0), "every_trial_identical": same,
+            "mean_z": [sum(r.z_final for r in row) / trials for row in res]}
 
 
 BUSYRING_W = 0.050515121785495443  # SURVEY §8(c) golden: calibrated ring weight (bench.cpp:105-132)
