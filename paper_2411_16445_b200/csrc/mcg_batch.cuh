@@ -1164,6 +1164,12 @@ __device__ __noinline__ void mcg_ph_solve(const McgDev& D, const McgBatchArgs& A
   const int nch = (A.ch_stride > 0) ? ((2 * S1 * nc + 31) & ~31) : 0;
   // LIF-only launches (A.lean): the other systems are point cells, one warp suffices
   const int split = nch > 0 ? (A.lean ? min(nch, T - 32) : min(256, T / 2)) : 0;
+  // the other systems, one thread per (cell, system), spread over warps
+  // first (item w + W l on lane l of the w-th warp of the range): a system's
+  // solve is a serial chain whose branches and slow paths diverge between
+  // cells, so items on separate warps run concurrently instead of taking
+  // turns in one warp
+  const int wr0 = split >> 5, nwr = (T - split) >> 5;
   if (tid < split) {
     for (int t = tid; t < nch; t += split) {
       McgChainLane L{};
@@ -1193,7 +1199,7 @@ __device__ __noinline__ void mcg_ph_solve(const McgDev& D, const McgBatchArgs& A
       MCG_PH(20);
     }
   } else
-  for (int t = tid - split; t < nc * S1; t += T - split) {
+  for (int t = (warp - wr0) + nwr * lane; split <= tid && t < nc * S1; t += nwr * 32) {
     const int k = t / S1, sys = t - k * S1;
     const int c = c0 + k;
     const McgCellSm& X = cs[k];
@@ -1258,9 +1264,11 @@ __device__ __noinline__ void mcg_ph_solve(const McgDev& D, const McgBatchArgs& A
           M.gsyn[i] = gs;
           M.gsyn_rhs[i] = rr;
         }
-        ok = mcg_solve_tree(n, KS.par, KS.cap, M.gsyn, KS.ax, M.gsyn_rhs, M.V, M.diag, M.r2);
+        ok = mcg_solve_tree_fast(n, KS.par, KS.cap, M.gsyn, KS.ax, M.gsyn_rhs, M.V, M.diag, M.r2);
       } else if (K.dyn == MCG_DYN_HH) {
-        ok = mcg_solve_tree(n, KS.par, KS.cap, M.gsyn, KS.ax, M.gsyn_rhs, M.V, M.diag, M.r2);
+        // M.gsyn is rebuilt every step before the solve (phase E1 / B), so
+        // the solve may keep its reciprocals there
+        ok = mcg_solve_tree_fast(n, KS.par, KS.cap, M.gsyn, KS.ax, M.gsyn_rhs, M.V, M.diag, M.r2);
       }
       // singular species systems need the full solver's scratch: run them
       // here, after V, in species order (never happens for valid recipes)

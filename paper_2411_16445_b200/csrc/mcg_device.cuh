@@ -282,6 +282,85 @@ __device__ bool mcg_solve_tree(int n, const int32_t* par, const double* cap, con
   return true;
 }
 
+// RN(1/d) when d is in the range where Markstein's quotient from it is exact
+// (|d| in [2^-200, 2^200]); 0.0 otherwise, which sends mcg_div to IEEE division
+__device__ __forceinline__ double mcg_rcp_or_zero(double d) {
+  const double ad = fabs(d);
+  return (ad >= 0x1p-200 && ad <= 0x1p200) ? __drcp_rn(d) : 0.0;
+}
+
+// solve_tree (tree_solver.cpp:46-74) with the reference's operations in the
+// reference's order, arranged for one thread's latency: the elimination
+// carries the node it last updated (a chain's next node, usually) in
+// registers instead of a shared-memory round trip, every division is
+// Markstein's quotient from RN(1/d) (mcg_div; IEEE division outside its
+// proven range), and the substitution's reciprocals are formed during the
+// elimination, off its dependent chain (stored over gs, which the caller no
+// longer needs).  Returns false if singular, at the same node as the loop.
+__device__ bool mcg_solve_tree_fast(int n, const int32_t* par, const double* cap, double* gs_y,
+                                    const double* coup, const double* rhs, double* v, double* diag,
+                                    double* r2) {
+  for (int i = 0; i < n; ++i) {
+    diag[i] = cap[i] + gs_y[i];
+    r2[i] = cap[i] * v[i] + rhs[i];
+  }
+  for (int i = 1; i < n; ++i) {
+    diag[i] += coup[i];
+    diag[par[i]] += coup[i];
+  }
+  int cp = -1;  // node whose diag / r2 (every contribution so far) are in cd / cr only
+  double cd = 0.0, cr = 0.0;
+  for (int i = n - 1; i >= 1; --i) {
+    double di, ri;
+    if (i == cp) {
+      di = cd;
+      ri = cr;
+      diag[i] = di;
+      r2[i] = ri;
+    } else {
+      if (cp >= 0) {
+        diag[cp] = cd;
+        r2[cp] = cr;
+      }
+      di = diag[i];
+      ri = r2[i];
+    }
+    if (di <= 0.0) return false;
+    const double ci = coup[i];
+    const double yi = mcg_rcp_or_zero(di);
+    gs_y[i] = yi;
+    const double f = mcg_div(ci, di, yi);
+    const int p = par[i];
+    double dp, rp;
+    if (p == cp && cp != i) {  // still current in registers (also just stored)
+      dp = cd;
+      rp = cr;
+    } else {
+      dp = diag[p];
+      rp = r2[p];
+    }
+    dp -= f * ci;  // diag[par[i]] -= f * coup[i]
+    rp += f * ri;  // r2[par[i]] += f * r2[i]
+    cp = p;
+    cd = dp;
+    cr = rp;
+  }
+  if (cp >= 0) {
+    diag[cp] = cd;
+    r2[cp] = cr;
+  }
+  if (diag[0] <= 0.0) return false;
+  double vp = mcg_div(r2[0], diag[0], mcg_rcp_or_zero(diag[0]));
+  v[0] = vp;
+  for (int i = 1; i < n; ++i) {
+    const int p = par[i];
+    const double vpar = (p == i - 1) ? vp : v[p];
+    vp = mcg_div(r2[i] + coup[i] * vpar, diag[i], gs_y[i]);
+    v[i] = vp;
+  }
+  return true;
+}
+
 // solve_tree with a precomputed constant elimination (McgKind::v_const /
 // sp_const): the rhs sweep and back-substitution of tree_solver.cpp:55-73
 // with f[i] = coupling[i]/diag[i] and the eliminated diagonal d[i] taken from
