@@ -1291,6 +1291,10 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
                                 int64_t s0, int64_t s1) {
   const McgBatchSm B = mcg_batch_sm(A);
   const int tid = threadIdx.x;
+  // the owner thread of cell k (the cells' serial chains: delivery, folds,
+  // detection) is lane k / W of warp k % W: owners on different warps run
+  // concurrently instead of taking turns inside one warp
+  const int ko = (threadIdx.x >> 5) + (blockDim.x >> 5) * (threadIdx.x & 31);
   const int T = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarps = T >> 5;
   const int c0 = b * A.cells_per_cta;
@@ -1401,13 +1405,13 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
       MCG_PH(0);
     }
     // ---- A. delivery (owner thread): inbox, then internal (engine.cpp:549-560)
-    if (tid < nc) {
-      const int c = c0 + tid;
-      McgCellSm& X = cs[tid];
-      const McgKind& K = kc[tid];
+    if (ko < nc) {
+      const int c = c0 + ko;
+      McgCellSm& X = cs[ko];
+      const McgKind& K = kc[ko];
       const bool refractory = X.lif && s < X.refr;
       X.refractory = refractory;
-      double* V = (K.n <= m) ? mcg_comp_block(A, B, tid) : D.v + D.comp_off[c];
+      double* V = (K.n <= m) ? mcg_comp_block(A, B, ko) : D.v + D.comp_off[c];
       const int64_t cg0 = D.cg_off[c];
       const bool trace = (A.dbg >> 8) == c + 1 && s >= A.dbg_s && s <= A.dbg_s + 5;
       if (trace)
@@ -1424,7 +1428,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
           if (X.gk[E.group] == MCG_SYN_STATIC_CHARGE) {
             if (!refractory && (E.inst >> 31)) V[E.comp] += E.w;  // w * cf[comp]
           } else {  // stc_charge, engine.cpp:493-510
-            McgSegSm& g = B.seg[tid * A.n_stc_max + X.gseg[E.group]];
+            McgSegSm& g = B.seg[ko * A.n_stc_max + X.gseg[E.group]];
             if (g.f_tail - g.f_head >= g.f_cap) {
               atomicOr(D.err, MCG_ERR_FLAG_FIFO);
             } else {
@@ -1455,7 +1459,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
         int q = X.in_cur;
         while (q < X.in_end && int(B.evb[q].so) == int(so)) {
           const McgEvSm E = B.evb[q];
-          const McgSegSm& g = B.seg[tid * A.n_stc_max + X.gseg[E.group]];
+          const McgSegSm& g = B.seg[ko * A.n_stc_max + X.gseg[E.group]];
           if (A.stc_sm) B.stc[2 * S4 + X.stc_off + g.start + int(E.inst)] += g.cpre_s;
           else D.i_stc_c[g.inst + E.inst] += g.cpre_s;
           ++q;
@@ -1470,7 +1474,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
             const int64_t r = int64_t(key & rank_mask);
             const int32_t grp = D.e_group[r];
             mcg_apply_event(D, K, c, cg0, V, grp, D.e_inst[r], D.e_weight[r], 0, refractory, s,
-                            mcg_stc_ref(A, B, tid, grp), D.e_src[r]);
+                            mcg_stc_ref(A, B, ko, grp), D.e_src[r]);
             ++cur;
             ++X.ndel;
             key = (cur < X.end) ? pend[cur] : ~0ull;
@@ -1504,7 +1508,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
             const uint64_t si = D.fifo_si[F.base + mcg_mod(F.head, F.cap)];
             ++F.head;
             mcg_apply_event(D, K, c, cg0, V, best, uint32_t(si & 0xffffffffu), 0.0, 1,
-                            refractory, s, mcg_stc_ref(A, B, tid, best));
+                            refractory, s, mcg_stc_ref(A, B, ko, best));
           }
           X.fifo_next = mcg_fifo_next(D, K, cg0);
         }
@@ -1667,18 +1671,18 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
     MCG_PH(2);
 
     // ---- D. SPS fold, synthesis trigger, background current (owner thread)
-    if (tid < nc) {
-      const int c = c0 + tid;
-      McgCellSm& X = cs[tid];
-      const McgKind& K = kc[tid];
+    if (ko < nc) {
+      const int c = c0 + ko;
+      McgCellSm& X = cs[ko];
+      const McgKind& K = kc[ko];
       const bool in_sm = K.n <= m;
-      double* base = in_sm ? mcg_comp_block(A, B, tid) : nullptr;
+      double* base = in_sm ? mcg_comp_block(A, B, ko) : nullptr;
       double* SP = in_sm ? base + m : D.species + D.sp_off[c];
       if (K.sps_idx >= 0) {
         double* sps = SP + int64_t(K.sps_idx) * K.n;
         int f = X.stc_off;
         for (int q = 0; q < X.n_stc_seg; ++q) {
-          const McgSegSm& g = B.seg[tid * A.n_stc_max + q];
+          const McgSegSm& g = B.seg[ko * A.n_stc_max + q];
           const int fe = f + g.size;
           // every instance of a placement sits on the placement's compartment;
           // every slot holds its delta or -0.0 (unchanged: x + -0.0 == x for
@@ -1707,7 +1711,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
       const bool bg_gated = K.bg_t1 > K.bg_t0 && ts >= K.bg_t0 && ts < K.bg_t1;
       if (X.lif && K.has_bg && !bg_gated) {
         double ib = K.i_bg;
-        if (K.sig_bg != 0.0) ib += K.sig_bg * B.nbuf[tid * 32 + int(so & 31)];
+        if (K.sig_bg != 0.0) ib += K.sig_bg * B.nbuf[ko * 32 + int(so & 31)];
         double* rc = in_sm ? base + (1 + D.sp_max) * m : D.s_rhs_cur + D.comp_off[c];
         rc[K.noise_comp] += ib;
         X.has_current = 1;
@@ -1765,13 +1769,13 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
     MCG_PH(6);
 
     // ---- F. spike detection (engine.cpp:753-769)
-    if (tid < nc) {
-      const int c = c0 + tid;
-      McgCellSm& X = cs[tid];
-      const McgKind& K = kc[tid];
+    if (ko < nc) {
+      const int c = c0 + ko;
+      McgCellSm& X = cs[ko];
+      const McgKind& K = kc[ko];
       X.fired = 0;
       if (K.has_detector && !X.refractory) {
-        const double* V = (K.n <= m) ? mcg_comp_block(A, B, tid) : D.v + D.comp_off[c];
+        const double* V = (K.n <= m) ? mcg_comp_block(A, B, ko) : D.v + D.comp_off[c];
         const double va = V[K.detector_comp];
         if (X.armed && X.det_prev < K.threshold && va >= K.threshold) {
           double f = (va > X.det_prev) ? (K.threshold - X.det_prev) / (va - X.det_prev) : 1.0;
@@ -1803,12 +1807,12 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
     __syncthreads();
     MCG_PH(8);
     // detector bookkeeping and probes (engine.cpp:770-793)
-    if (tid < nc) {
-      const int c = c0 + tid;
-      McgCellSm& X = cs[tid];
-      const McgKind& K = kc[tid];
+    if (ko < nc) {
+      const int c = c0 + ko;
+      McgCellSm& X = cs[ko];
+      const McgKind& K = kc[ko];
       const bool in_sm = K.n <= m;
-      const double* V = in_sm ? mcg_comp_block(A, B, tid) : D.v + D.comp_off[c];
+      const double* V = in_sm ? mcg_comp_block(A, B, ko) : D.v + D.comp_off[c];
       if (K.has_detector && !X.refractory) {
         if (X.fired) {
           if (X.lif) X.refr = s + 1 + K.ref_steps;
@@ -1825,7 +1829,7 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
         const int64_t m0 = (D.ctl[3] + Pr.every) / Pr.every;
         const double* SP = in_sm ? V + m : D.species + D.sp_off[c];
         D.trace_buf[D.trace_base[p] + ((s + 1) / Pr.every - m0)] =
-            mcg_probe_value(D, K, c, Pr, V, SP, mcg_stc_ref(A, B, tid, Pr.group));
+            mcg_probe_value(D, K, c, Pr, V, SP, mcg_stc_ref(A, B, ko, Pr.group));
       }
     }
     __syncthreads();
@@ -1847,13 +1851,13 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
     }
   }
   __syncthreads();
-  if (tid < nc) {
-    const int c = c0 + tid;
-    const McgCellSm& X = cs[tid];
+  if (ko < nc) {
+    const int c = c0 + ko;
+    const McgCellSm& X = cs[ko];
     const int k = min(X.nsp, D.sp_cap);
     if (k > 0) {
       int before = 0;
-      for (int q = 0; q < tid; ++q) before += min(cs[q].nsp, D.sp_cap);
+      for (int q = 0; q < ko; ++q) before += min(cs[q].nsp, D.sp_cap);
       for (int i = 0; i < k; ++i) {
         A.log_t[s_log_off + before + i] = D.sp_t[int64_t(c) * D.sp_cap + i];
         A.log_gid[s_log_off + before + i] = D.gid0 + uint32_t(c);
