@@ -597,16 +597,17 @@ def run_gpu_arm_sharded(args, world, rank):
     flat = b.recipe.flatten()
     opt = EngineOptions(DT_MS, SEED)
 
-    def make():
+    def make(rec=None):
+        rec = flat if rec is None else rec
         if backend == "nccl":
-            e = Engine(flat, opt, device=device, rank=rank, world=world)
+            e = Engine(rec, opt, device=device, rank=rank, world=world)
             uid = torch.zeros(128, dtype=torch.uint8, device=coll_dev)
             if rank == 0:
                 uid.copy_(torch.tensor(list(Engine.nccl_unique_id()), dtype=torch.uint8))
             dist.broadcast(uid, 0)
             e.init_nccl(bytes(uid.cpu().tolist()))
             return e, e.shard_advance_to, e.global_spike_arrays
-        sh = shard.ShardedEngine(flat, opt, rank, world, device=device, backend=backend,
+        sh = shard.ShardedEngine(rec, opt, rank, world, device=device, backend=backend,
                                  record_spikes=True)
         return sh.engine, sh.advance_to, sh.spike_arrays
 
@@ -669,6 +670,37 @@ def run_gpu_arm_sharded(args, world, rank):
     h2d = v.n_connections * (1 + 4 + 4 + 4 + 1 + 8 + 8) + s1["total_synapses"] * 8 * 12 + s1["total_comps"] * 8 * 5
     d2h = st_.nbytes + sg_.nbytes
     eng2.close()
+    # config 5 strong-scaled: the 100 k-cell network (48 comps, p = 0.002)
+    # over the same ranks, 100 -> 300 ms after a 100 ms warm-up
+    other = None
+    if not args.no_other:
+        c5 = N.ConsolidationConfig(n_cells=100000, n_exc=80000, p_conn=0.002, seed=SEED, multi_compartment=True,
+                                   dend_size=N.DendriteSize.large_dendrites, dt_ms=DT_MS)
+        t_s = time.perf_counter()
+        f5 = N.build_consolidation_network(c5, True, device=device).recipe.flatten()
+        e5, adv5, _ = make(f5)
+        setup5 = time.perf_counter() - t_s
+        e5.set_timing(True)
+        adv5(100.0)
+        a5 = e5.stats()
+        torch.cuda.synchronize()
+        dist.barrier()
+        w5 = time.perf_counter()
+        adv5(300.0)
+        torch.cuda.synchronize()
+        w5 = time.perf_counter() - w5
+        b5 = e5.stats()
+        d5 = (b5["advance_ms"] - a5["advance_ms"]) * 1e-3 if backend == "nccl" else w5
+        t5 = torch.tensor([d5, setup5], dtype=torch.float64, device=coll_dev)
+        dist.all_reduce(t5, op=dist.ReduceOp.MAX)
+        steps5 = b5["steps"] - a5["steps"]
+        other = {"config5_strong": {"n_cells": 100000, "n_gpus": world, "bio_ms": 200.0,
+                                    "sim_s_per_wall_s": 0.2 / float(t5[0].item()),
+                                    "us_per_fine_step": 1e6 * float(t5[0].item()) / max(steps5, 1),
+                                    "setup_s": float(t5[1].item()), "scaling": "strong",
+                                    "timing": "engine CUDA events, max over ranks" if backend == "nccl"
+                                    else "wall clock (host-staged exchange), max over ranks"}}
+        e5.close()
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -689,6 +721,8 @@ def run_gpu_arm_sharded(args, world, rank):
             "gpu_launches": int(s1["kernel_launches"] - s0["kernel_launches"]),
             "clocks": clk,
         }
+        if other:
+            line["other_configs"] = other
         print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()
