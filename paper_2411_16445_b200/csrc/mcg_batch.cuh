@@ -1151,7 +1151,7 @@ __device__ void mcg_batch_exit(const McgDev& D, const McgBatchArgs& A, int32_t b
 __device__ __noinline__ void mcg_ph_solve(const McgDev& D, const McgBatchArgs& A, int32_t b) {
   const McgBatchSm B = mcg_batch_sm(A);
   const int tid = threadIdx.x, T = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5, nwarps = T >> 5;
+  const int lane = tid & 31, warp = tid >> 5;
   const int c0 = b * A.cells_per_cta;
   const int nc = min(A.cells_per_cta, D.n_cells - c0);
   const int S1 = 1 + D.sp_max;
@@ -1299,7 +1299,6 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
   const int lane = tid & 31, warp = tid >> 5, nwarps = T >> 5;
   const int c0 = b * A.cells_per_cta;
   const int nc = min(A.cells_per_cta, D.n_cells - c0);
-  const int S1 = 1 + D.sp_max;  // systems per cell
   const int m = D.smem_n;
   McgCellSm* cs = B.cs;
   const McgKind* kc = B.kc;

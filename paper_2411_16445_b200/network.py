@@ -489,7 +489,6 @@ def run_stc_protocols(cfg: StcSingleConfig, protocols: Sequence[int], trials: in
             kind.membrane.bg_quiet_t0_ms = t_detailed - 500.0
             kind.membrane.bg_quiet_t1_ms = cfg.t_eval_ms
             n = len(tids)
-            every = one.probes[0].every_steps
             probes = []
             for c in range(n):  # the single-trial probes, per cell
                 probes += [replace(p, gid=c) for p in one.probes]
@@ -511,7 +510,6 @@ def run_stc_protocols(cfg: StcSingleConfig, protocols: Sequence[int], trials: in
                                           max_dh, max_dh > cfg.stc.theta_tag_mV, max_dh > cfg.stc.theta_pro_mV,
                                           tr[4 * c:4 * c + 4])
             eng.close()
-            del every
         except BaseException as e:  # noqa: BLE001
             errors.append(e)
 
