@@ -141,19 +141,21 @@ struct McgWarpSm {
   int ev;      // ev_cap McgWEv
   int rec;     // G McgWCell
   int mask;    // G x MW uint32
+  int mbar;    // mbarrier of the warp's bulk (TMA) staging copies + its phase word
 };
 
 __host__ __device__ __forceinline__ int mcg_warp_region_doubles(int G, int m, int S, int P, int MW,
                                                                 int ev_cap) {
   const int rec = (int(sizeof(McgWCell)) + 7) / 8;
-  return G * (2 + S) * m + G * (1 + S) * P + G * 32 + 32 + 16 + ev_cap * 3 + G * rec +
-         (G * MW + 1) / 2 + 2;
+  const int d = G * (2 + S) * m + G * (1 + S) * P + G * 32 + 32 + 16 + ev_cap * 3 + G * rec +
+                (G * MW + 1) / 2 + 2 + 2;
+  return (d + 1) & ~1;  // even: 16-byte aligned warp regions (bulk copies)
 }
 
 __device__ __forceinline__ McgWarpSm mcg_warp_sm(const McgWarpArgs& A, int w) {
   McgWarpSm R;
-  const int base0 = A.kind_doubles + (A.n_kinds * int(sizeof(McgKind)) + 7) / 8 +
-                    (A.n_specs_sm * int(sizeof(McgSpec)) + 7) / 8;
+  const int base0 = (A.kind_doubles + (A.n_kinds * int(sizeof(McgKind)) + 7) / 8 +
+                     (A.n_specs_sm * int(sizeof(McgSpec)) + 7) / 8 + 1) & ~1;  // 16-byte aligned
   const int b = base0 + w * A.warp_doubles;
   R.cells = b;
   R.r2c = R.cells + A.G * A.cell_doubles;
@@ -163,7 +165,49 @@ __device__ __forceinline__ McgWarpSm mcg_warp_sm(const McgWarpArgs& A, int w) {
   R.ev = R.ic + 16;
   R.rec = R.ev + A.ev_cap * 3;
   R.mask = R.rec + A.G * ((int(sizeof(McgWCell)) + 7) / 8);
+  R.mbar = R.mask + (A.G * A.MW + 1) / 2 + 2;
   return R;
+}
+
+// ---- bulk (TMA) copies of a group's compartment blocks ----------------------
+// cp.async.bulk moves a cell's V block and its species blocks (contiguous in
+// global memory and in the cell's shared-memory block) as one transfer each,
+// completing on the warp's mbarrier; blocks whose addresses or sizes are not
+// 16-byte multiples take the element-wise path
+__device__ __forceinline__ uint32_t mcg_sa(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ bool mcg_bulk_ok(const void* g, const void* sm, int bytes) {
+  return bytes > 0 && (bytes & 15) == 0 && (reinterpret_cast<uintptr_t>(g) & 15) == 0 && (mcg_sa(sm) & 15) == 0;
+}
+__device__ __forceinline__ void mcg_mbar_init(uint32_t bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mcg_mbar_expect(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mcg_mbar_wait(uint32_t bar, uint32_t phase) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void mcg_bulk_load(void* sm, const void* g, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          mcg_sa(sm)),
+      "l"(g), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mcg_bulk_store(void* g, const void* sm, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(g), "r"(mcg_sa(sm)),
+               "r"(bytes)
+               : "memory");
 }
 
 __device__ __forceinline__ McgKind* mcg_warp_kinds(const McgWarpArgs& A) {
@@ -266,15 +310,51 @@ __device__ void mcg_wg_enter(const McgDev& D, const McgWarpArgs& A, const McgWar
     }
   }
   __syncwarp();
-  // compartment state: asynchronous copies, every load in flight at once
+  // compartment state: a cell's V block and its species blocks are
+  // contiguous in global memory and in its shared-memory block, so each is one
+  // bulk (TMA) copy when 16-byte aligned; the rest go element by element
+  // (cp.async), every load in flight at once
+  const uint32_t bar = mcg_sa(mcg_smem + W.mbar);
+  uint32_t* bphase = reinterpret_cast<uint32_t*>(mcg_smem + W.mbar + 1);
+  uint32_t tx = 0;
+  uint32_t bulk_mask = 0;  // bit 2k: cell k's V block by bulk copy, bit 2k + 1: its species
+  for (int k = 0; k < A.G; ++k) {
+    const int c = R[k].c;
+    if (c < 0) continue;
+    const McgKind& K = kinds[R[k].kind];
+    const int n = K.n;
+    if (mcg_bulk_ok(D.v + D.comp_off[c], mcg_smem + R[k].base, n * 8)) {
+      bulk_mask |= 1u << (2 * k);
+      tx += uint32_t(n) * 8u;
+    }
+    if (K.n_species > 0 &&
+        mcg_bulk_ok(D.species + D.sp_off[c], mcg_smem + R[k].base + m, K.n_species * n * 8)) {
+      bulk_mask |= 2u << (2 * k);
+      tx += uint32_t(K.n_species * n) * 8u;
+    }
+  }
+  if (tx > 0) {
+    if (lane == 0) mcg_mbar_expect(bar, tx);
+    __syncwarp();
+    if (lane < A.G && R[lane].c >= 0) {
+      const int c = R[lane].c;
+      const McgKind& K = kinds[R[lane].kind];
+      if (bulk_mask & (1u << (2 * lane)))
+        mcg_bulk_load(mcg_smem + R[lane].base, D.v + D.comp_off[c], uint32_t(K.n) * 8u, bar);
+      if (bulk_mask & (2u << (2 * lane)))
+        mcg_bulk_load(mcg_smem + R[lane].base + m, D.species + D.sp_off[c], uint32_t(K.n_species * K.n) * 8u,
+                      bar);
+    }
+  }
   const int per = (1 + A.S) * m;
   for (int idx = lane; idx < A.G * per; idx += 32) {
     const int k = idx / per, r = idx - k * per;
     const int c = R[k].c;
     if (c < 0) continue;
+    const int a = r / m, i = r - a * m;
+    if (bulk_mask & ((a == 0 ? 1u : 2u) << (2 * k))) continue;
     const McgKind& K = kinds[R[k].kind];
     const int n = K.n;
-    const int a = r / m, i = r - a * m;
     if (i >= n || (a > 0 && a - 1 >= K.n_species)) continue;
     const double* src = a == 0 ? D.v + D.comp_off[c] + i : D.species + D.sp_off[c] + (a - 1) * n + i;
     double* dst = mcg_smem + R[k].base + (a == 0 ? i : m + (a - 1) * n + i);
@@ -288,6 +368,12 @@ __device__ void mcg_wg_enter(const McgDev& D, const McgWarpArgs& A, const McgWar
     MK[idx] = (c >= 0 && w * 32 < R[k].stc_n) ? A.stc_mask[int64_t(c) * A.MW + w] : 0u;
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
+  if (tx > 0) {
+    const uint32_t ph = *bphase;
+    mcg_mbar_wait(bar, ph & 1u);
+    __syncwarp();
+    if (lane == 0) *bphase = ph + 1;
+  }
   __syncwarp();
 }
 
@@ -296,14 +382,46 @@ __device__ void mcg_wg_exit(const McgDev& D, const McgWarpArgs& A, const McgWarp
   const McgKind* kinds = mcg_warp_kinds(A);
   McgWCell* R = reinterpret_cast<McgWCell*>(mcg_smem + W.rec);
   const int m = A.m;
+  // blocks that entered by bulk copy leave by bulk copy (the shared-memory
+  // writes of the epoch made visible to the async proxy first); the rest
+  // element by element
+  uint32_t bulk_mask = 0;
+  for (int k = 0; k < A.G; ++k) {
+    const int c = R[k].c;
+    if (c < 0) continue;
+    const McgKind& K = kinds[R[k].kind];
+    const int n = K.n;
+    if (mcg_bulk_ok(D.v + D.comp_off[c], mcg_smem + R[k].base, n * 8)) bulk_mask |= 1u << (2 * k);
+    if (K.n_species > 0 &&
+        mcg_bulk_ok(D.species + D.sp_off[c], mcg_smem + R[k].base + m, K.n_species * n * 8))
+      bulk_mask |= 2u << (2 * k);
+  }
+  if (bulk_mask) {
+    __syncwarp();
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    if (lane < A.G && R[lane].c >= 0) {
+      const int c = R[lane].c;
+      const McgKind& K = kinds[R[lane].kind];
+      if (bulk_mask & (1u << (2 * lane)))
+        mcg_bulk_store(D.v + D.comp_off[c], mcg_smem + R[lane].base, uint32_t(K.n) * 8u);
+      if (bulk_mask & (2u << (2 * lane)))
+        mcg_bulk_store(D.species + D.sp_off[c], mcg_smem + R[lane].base + m, uint32_t(K.n_species * K.n) * 8u);
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      // the shared-memory blocks are reused by the next group: wait until the
+      // copies have read them (their global writes complete before the
+      // grid barrier: the wait_group at the end of the warp's epoch)
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    }
+  }
   const int per = (1 + A.S) * m;
   for (int idx = lane; idx < A.G * per; idx += 32) {
     const int k = idx / per, r = idx - k * per;
     const int c = R[k].c;
     if (c < 0) continue;
+    const int a = r / m, i = r - a * m;
+    if (bulk_mask & ((a == 0 ? 1u : 2u) << (2 * k))) continue;
     const McgKind& K = kinds[R[k].kind];
     const int n = K.n;
-    const int a = r / m, i = r - a * m;
     if (i >= n || (a > 0 && a - 1 >= K.n_species)) continue;
     const double v = mcg_smem[R[k].base + (a == 0 ? i : m + (a - 1) * n + i)];
     if (a == 0) D.v[D.comp_off[c] + i] = v;
@@ -1055,6 +1173,12 @@ __global__ void __launch_bounds__(256, 1) k_warp(const __grid_constant__ McgDev 
   }
   __syncthreads();
   const McgWarpSm W = mcg_warp_sm(A, w);
+  if (lane == 0) {  // the warp's bulk-copy mbarrier, phase 0
+    mcg_mbar_init(mcg_sa(mcg_smem + W.mbar));
+    *reinterpret_cast<uint32_t*>(mcg_smem + W.mbar + 1) = 0u;
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncwarp();
   const int gw = w * gridDim.x + blockIdx.x;  // consecutive groups on different SMs
   const int nw = gridDim.x * (blockDim.x >> 5);
   if (A.resident && gw < A.n_groups) mcg_wg_enter(D, A, W, gw, lane);
@@ -1077,9 +1201,13 @@ __global__ void __launch_bounds__(256, 1) k_warp(const __grid_constant__ McgDev 
       if (!A.resident) mcg_wg_exit(D, A, W, lane);
       WPH(9);
     }
+    // the warp's bulk stores of this epoch complete before the barrier (the
+    // next epoch's bulk loads, other kernels, the host read them)
+    if (!A.resident && lane < A.G) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
     grid.sync();
   }
   if (A.resident && gw < A.n_groups) mcg_wg_exit(D, A, W, lane);
+  if (lane < A.G) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
   WPH(9);
   if (A.phase && lane == 0 && gw < A.n_groups)
     for (int i = 0; i < MCG_WPH_N; ++i) {
