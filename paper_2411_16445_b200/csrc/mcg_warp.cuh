@@ -37,7 +37,7 @@
 #include "mcg_batch.cuh"
 
 #define MCG_WG_MAX 8  // cells per warp group
-#define MCG_WPH_N 14   // phase-timing slots (MCG_PHASE_TIMING)
+#define MCG_WPH_N 15   // phase-timing slots (MCG_PHASE_TIMING)
 
 // optional per-phase cycle accounting: lane 0 of each warp, one row per warp
 __shared__ unsigned long long mcg_wph[8][MCG_WPH_N + 1];
@@ -310,6 +310,7 @@ __device__ void mcg_wg_enter(const McgDev& D, const McgWarpArgs& A, const McgWar
     }
   }
   __syncwarp();
+  WPH(14);  // cell records done (the rest of the entry counts as "groups")
   // compartment state: a cell's V block and its species blocks are
   // contiguous in global memory and in its shared-memory block, so each is one
   // bulk (TMA) copy when 16-byte aligned; the rest go element by element
@@ -346,20 +347,24 @@ __device__ void mcg_wg_enter(const McgDev& D, const McgWarpArgs& A, const McgWar
                       bar);
     }
   }
-  const int per = (1 + A.S) * m;
-  for (int idx = lane; idx < A.G * per; idx += 32) {
-    const int k = idx / per, r = idx - k * per;
+  // the blocks that are not bulk-copied, element by element, cell by cell
+  for (int k = 0; k < A.G; ++k) {
     const int c = R[k].c;
     if (c < 0) continue;
-    const int a = r / m, i = r - a * m;
-    if (bulk_mask & ((a == 0 ? 1u : 2u) << (2 * k))) continue;
     const McgKind& K = kinds[R[k].kind];
     const int n = K.n;
-    if (i >= n || (a > 0 && a - 1 >= K.n_species)) continue;
-    const double* src = a == 0 ? D.v + D.comp_off[c] + i : D.species + D.sp_off[c] + (a - 1) * n + i;
-    double* dst = mcg_smem + R[k].base + (a == 0 ? i : m + (a - 1) * n + i);
-    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src) : "memory");
+    const int nb = (bulk_mask & (1u << (2 * k)) ? 0 : n) + (bulk_mask & (2u << (2 * k)) ? 0 : K.n_species * n);
+    for (int e = lane; e < nb; e += 32) {
+      // e < n_v: V element e (when V is element-wise); then the species
+      const bool v_el = !(bulk_mask & (1u << (2 * k)));
+      const int nv = v_el ? n : 0;
+      const bool is_v = e < nv;
+      const int j = is_v ? e : e - nv;  // species: offset in the (species x n) block
+      const double* src = is_v ? D.v + D.comp_off[c] + j : D.species + D.sp_off[c] + j;
+      double* dst = mcg_smem + R[k].base + (is_v ? j : m + j);
+      const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src) : "memory");
+    }
   }
   uint32_t* MK = reinterpret_cast<uint32_t*>(mcg_smem + W.mask);
   for (int idx = lane; idx < A.G * A.MW; idx += 32) {
@@ -413,19 +418,21 @@ __device__ void mcg_wg_exit(const McgDev& D, const McgWarpArgs& A, const McgWarp
       asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
     }
   }
-  const int per = (1 + A.S) * m;
-  for (int idx = lane; idx < A.G * per; idx += 32) {
-    const int k = idx / per, r = idx - k * per;
+  for (int k = 0; k < A.G; ++k) {
     const int c = R[k].c;
     if (c < 0) continue;
-    const int a = r / m, i = r - a * m;
-    if (bulk_mask & ((a == 0 ? 1u : 2u) << (2 * k))) continue;
     const McgKind& K = kinds[R[k].kind];
     const int n = K.n;
-    if (i >= n || (a > 0 && a - 1 >= K.n_species)) continue;
-    const double v = mcg_smem[R[k].base + (a == 0 ? i : m + (a - 1) * n + i)];
-    if (a == 0) D.v[D.comp_off[c] + i] = v;
-    else D.species[D.sp_off[c] + (a - 1) * n + i] = v;
+    const bool v_el = !(bulk_mask & (1u << (2 * k)));
+    const int nv = v_el ? n : 0;
+    const int nb = nv + (bulk_mask & (2u << (2 * k)) ? 0 : K.n_species * n);
+    for (int e = lane; e < nb; e += 32) {
+      const bool is_v = e < nv;
+      const int j = is_v ? e : e - nv;
+      const double v = mcg_smem[R[k].base + (is_v ? j : m + j)];
+      if (is_v) D.v[D.comp_off[c] + j] = v;
+      else D.species[D.sp_off[c] + j] = v;
+    }
   }
   const uint32_t* MK = reinterpret_cast<const uint32_t*>(mcg_smem + W.mask);
   for (int idx = lane; idx < A.G * A.MW; idx += 32) {
