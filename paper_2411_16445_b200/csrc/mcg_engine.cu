@@ -304,7 +304,7 @@ struct Engine {
                    (long long)call_steps, warps);
       static const char* nm[MCG_WPH_N] = {"epoch_in", "noise", "deliver", "stc", "trigger", "solve",
                                           "detect_post", "probes", "epoch_out", "groups", "expand", "gsync",
-                                          "solve_chain", "abort_chk", "enter_rec"};
+                                          "solve_chain", "abort_chk", "enter_rec", "inbox"};
       for (int i = 0; i < MCG_WPH_N; ++i)
         std::fprintf(stderr, " %s %.3f|%.3f", nm[i], ph[i] / warps / 1965.0 / std::max<int64_t>(call_steps, 1),
                      ph[MCG_WPH_N + i] / 1965.0 / std::max<int64_t>(call_steps, 1));

@@ -37,7 +37,7 @@
 #include "mcg_batch.cuh"
 
 #define MCG_WG_MAX 8  // cells per warp group
-#define MCG_WPH_N 15   // phase-timing slots (MCG_PHASE_TIMING)
+#define MCG_WPH_N 16   // phase-timing slots (MCG_PHASE_TIMING)
 
 // optional per-phase cycle accounting: lane 0 of each warp, one row per warp
 __shared__ unsigned long long mcg_wph[8][MCG_WPH_N + 1];
@@ -630,6 +630,7 @@ __device__ void mcg_wg_epoch(const McgDev& D, const McgWarpArgs& A, const McgWar
     }
     if (mine) R[lane].nsp = 0;
   }
+  WPH(15);  // inbox merge and staging done
   // resting synapses' calcium brought to s0 every cu_every epochs, so that a
   // catch-up inside an epoch (delayed calcium, the post-spike hook) spans at
   // most cu_every epochs of multiplications
