@@ -24,7 +24,7 @@ import numpy as np
 from . import _abi as A
 from .engine import Engine, EngineOptions
 from .recipe import par_take
-from .recipe import (CellKindSpec, ConnectionTable, EngineError, HhMembrane, LifMembrane,
+from .recipe import (CellKindSpec, ConnectionSpec, ConnectionTable, EngineError, HhMembrane, LifMembrane,
                      MorphologyError, PlacementSpec, PoissonSource, PoissonWindow, ProbeSpec,
                      ProbeWhat, Recipe, Region, ScriptedSource, Segment, SelectionPolicy,
                      SpeciesSpec, StcParams, StdpParams, SynKind, SynSpec)
@@ -521,6 +521,65 @@ def run_stc_protocols(cfg: StcSingleConfig, protocols: Sequence[int], trials: in
     if errors:
         raise errors[0]
     return out
+
+
+# ---- single neuron driven by plastic + static Poisson inputs (network.hpp:17-41) ----
+
+@dataclass
+class StdpPoissonConfig:  # network.hpp:19-30
+    duration_ms: float = 10000.0
+    dt_ms: float = 0.1
+    seed: int = 0
+    rate_exc_hz: float = 100.0
+    rate_inh_hz: float = 30.0
+    w_inh_uS: float = 1.0
+    tau_syn_ms: float = 5.0
+    e_exc_mV: float = 0.0
+    e_inh_mV: float = -80.0
+    stdp: StdpParams = field(default_factory=StdpParams)
+
+
+def build_stdp_single_neuron(cfg: StdpPoissonConfig) -> Recipe:
+    """network.cpp:43-91: one tiny-cylinder cable LIF neuron (1 uS leak), an
+    STDP conductance synapse driven by an excitatory Poisson source and a
+    static conductance synapse driven by an inhibitory one; the plastic
+    weight is probed every 10 ms."""
+    m = LifMembrane(tau_mem_ms=10.0, r_mem_MOhm=1.0, v_rev_mV=-65.0, v_reset_mV=-70.0, v_thresh_mV=-55.0)
+    exc = SynSpec(kind=SynKind.stdp_cond, tau_syn_ms=cfg.tau_syn_ms, e_rev_mV=cfg.e_exc_mV, stdp=replace(cfg.stdp))
+    inh = SynSpec(kind=SynKind.static_cond, tau_syn_ms=cfg.tau_syn_ms, e_rev_mV=cfg.e_inh_mV)
+    kind = CellKindSpec(segments=[tiny_cylinder()], target_compartment_um=1.0, membrane=m,
+                        placements=[PlacementSpec("exc", exc, 0, 0), PlacementSpec("inh", inh, 0, 0)])
+    r = Recipe(kinds=[kind], cell_kind=[0],
+               sources=[PoissonSource([PoissonWindow(0.0, cfg.duration_ms, cfg.rate_exc_hz)]),
+                        PoissonSource([PoissonWindow(0.0, cfg.duration_ms, cfg.rate_inh_hz)])],
+               connections=[ConnectionSpec(True, 0, 0, "exc", SelectionPolicy.univalent, cfg.stdp.w0_uS, cfg.dt_ms),
+                            ConnectionSpec(True, 1, 0, "inh", SelectionPolicy.univalent, cfg.w_inh_uS, cfg.dt_ms)],
+               probes=[ProbeSpec(0, ProbeWhat.syn_weight, 0, 0, "exc", 0, max(1, int(10.0 / cfg.dt_ms)))])
+    return r
+
+
+@dataclass
+class StdpPoissonResult:  # network.hpp:34-39
+    pre_count: int
+    post_count: int
+    weight_t_s: np.ndarray
+    weight: np.ndarray
+    spikes_t_s: np.ndarray
+    spikes_gid: np.ndarray
+
+
+def run_stdp_poisson(cfg: StdpPoissonConfig, device: int = 0) -> StdpPoissonResult:
+    """network.cpp:93-120 on the device; pre_count re-draws the excitatory
+    source's Bernoulli trials (uniform_for(key(seed, 2^32, 3, 0), s) < rate dt
+    1e-3) for reporting, as the reference does."""
+    eng = Engine(build_stdp_single_neuron(cfg), EngineOptions(cfg.dt_ms, cfg.seed, 1), device=device)
+    eng.advance_to(cfg.duration_ms)
+    tt, w = eng.trace_arrays(0)
+    st, sg = eng.spike_arrays()
+    steps = int(math.ceil(cfg.duration_ms / cfg.dt_ms))
+    u = uniform_stream((cfg.seed, 0x100000000, 3, 0), 0, steps, device)
+    pre = int(np.count_nonzero(u < cfg.rate_exc_hz * cfg.dt_ms * 1e-3))
+    return StdpPoissonResult(pre, len(st), tt * 1e-3, w, st * 1e-3, sg)
 
 
 # ---- busyring (bench.hpp / bench.cpp) ---------------------------------------------
