@@ -3,6 +3,9 @@
 Mirrors (same parameters, same connection order, same random draws):
   build_consolidation_network / run_consolidation   network.cpp:426-639
   build_stc_single / stc_protocol_times / run_stc_protocol   network.cpp:289-399
+  run_stc_protocols (the stc-protocols experiment, experiments.cpp:262-289,
+                     trials batched as the cells of one engine)
+  build_stdp_single_neuron / run_stdp_poisson       network.cpp:43-120
   build_busyring / calibrate_ring_weight / run_bench_once    bench.cpp:31-194
   build_single_neuron_plastic  (config 2 of BASELINE.json; not in the reference)
 and the morphology builders they use (morphology.cpp:67-197).
