@@ -52,6 +52,7 @@ struct McgBatchArgs {
   int32_t fmask_words;     // changed-flag words (fmask)
   int32_t nch_max;         // chain-sweep lanes of a batch (lane descriptor table rows)
   int32_t lean;            // LIF-only launch (compartment block V | SP | rhs_cur)
+  int32_t act_max;         // one cell per CTA: phase-B scratch entries (0: warp path)
   unsigned long long* phase;  // optional per-phase cycle totals (MCG_NPHASE)
   double* log_t;           // spike log of the launch
   uint32_t* log_gid;
@@ -561,6 +562,7 @@ struct McgBatchSm {
   double* nbuf;     // C x 32 background-noise draws
   double* dbuf;     // stc_max SPS fold deltas
   double* stc;      // stc_sm: 4 x stc_max STC state h | z | c | |h-h0| (SoA)
+  double* abuf;     // act_max decayed kernels (kept) or -0.0 (dropped), phase B
   double* ksm;      // staged kind constants
   McgKind* kc;      // C kind records
   McgCellSm* cs;    // C cell records
@@ -568,6 +570,7 @@ struct McgBatchSm {
   McgSpec* spec;    // staged spec table (n_specs_sm entries)
   uint32_t* floc;   // stc_max: (cell << 16) | group of each STC instance slot
   uint32_t* fmask;  // stc_max / 32 changed-flag words
+  int* aidx;        // act_max instance index of each abuf entry
   McgEvSm* evb;     // staged events (ev_cap entries)
   int* lanes;       // nch_max x MCG_LANE_INTS static chain-lane descriptors
   int ksm_o;        // offset of ksm in mcg_smem (doubles)
@@ -583,7 +586,8 @@ __device__ __forceinline__ McgBatchSm mcg_batch_sm(const McgBatchArgs& A) {
   B.nbuf = B.comp + C * A.comp_stride;
   B.dbuf = B.nbuf + C * 32;
   B.stc = B.dbuf + A.stc_max;
-  B.chs_o = C * A.comp_stride + C * 32 + A.stc_max + (A.stc_sm ? 4 * A.stc_max : 0);
+  B.abuf = B.stc + (A.stc_sm ? 4 * A.stc_max : 0);
+  B.chs_o = C * A.comp_stride + C * 32 + A.stc_max + (A.stc_sm ? 4 * A.stc_max : 0) + A.act_max;
   B.ksm_o = B.chs_o + C * A.ch_stride;
   B.ksm = mcg_smem + B.ksm_o;
   B.kc = reinterpret_cast<McgKind*>(B.ksm + A.kind_doubles);
@@ -593,7 +597,8 @@ __device__ __forceinline__ McgBatchSm mcg_batch_sm(const McgBatchArgs& A) {
   B.floc = reinterpret_cast<uint32_t*>(B.spec + A.n_specs_sm);
   B.fmask = B.floc + A.stc_max;
   {
-    B.lanes = reinterpret_cast<int*>(B.fmask + A.fmask_words);
+    B.aidx = reinterpret_cast<int*>(B.fmask + A.fmask_words);
+    B.lanes = B.aidx + A.act_max;
     const uintptr_t e = reinterpret_cast<uintptr_t>(B.lanes + A.nch_max * MCG_LANE_INTS);
     B.evb = reinterpret_cast<McgEvSm*>((e + 15) & ~uintptr_t(15));
   }
@@ -1523,6 +1528,130 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
     MCG_PH(1);
 
     // ---- B. active-list kernels (warp per cell, ordered folds, engine.cpp:578-616)
+    // One staged cell with long active lists (a neuron with many plastic
+    // inputs, A.act_max > 0): every thread decays a share of the kernels, all
+    // its loads in flight together, and leaves the kept value (or -0.0) and the
+    // instance index in shared memory; warp 0 then compacts the lists and
+    // folds them in list order while the other warps run phase C.  Each
+    // group's entries start at a multiple of 32.
+    const bool pb = A.act_max > 0 && nc == 1 && cs[0].has_act;
+    if (pb) {
+      const McgKind& K = kc[0];
+      const int64_t cg0 = D.cg_off[c0];
+      int off = 0;
+      for (int gi = 0; gi < K.n_groups; ++gi) {
+        McgCellGroup* G = &D.cgs[cg0 + gi];
+        const McgSpec& S = specs[G->spec];
+        const int na = G->active_n;
+        const bool cond = S.kind == MCG_SYN_STATIC_COND || S.kind == MCG_SYN_STDP_COND;
+        if (na == 0 || !(cond || S.kind == MCG_SYN_STATIC_CURRENT || S.kind == MCG_SYN_HOMEO_CURRENT))
+          continue;
+        const int64_t base = G->inst;
+        const double f = S.f_decay;
+        for (int a0 = 0; a0 < na; a0 += 4 * T) {
+          int ii[4];
+          double kk[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int a = a0 + u * T + tid;
+            ii[u] = a < na ? D.i_active[base + a] : -1;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) kk[u] = ii[u] >= 0 ? D.i_kernel[base + ii[u]] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (ii[u] < 0) continue;
+            double kv = kk[u] * f;
+            if (cond ? (kv < 1e-30) : (fabs(kv) < 1e-30)) kv = 0.0;
+            D.i_kernel[base + ii[u]] = kv;
+            const int a = off + a0 + u * T + tid;
+            B.abuf[a] = kv != 0.0 ? kv : -0.0;
+            B.aidx[a] = ii[u];
+          }
+        }
+        off += (na + 31) & ~31;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        const McgCellMem M = mcg_cell_mem(D, K, c0, K.n <= m ? mcg_comp_block(A, B, 0) : nullptr);
+        bool hg = false, hc = false;
+        off = 0;
+        for (int gi = 0; gi < K.n_groups; ++gi) {
+          McgCellGroup* G = &D.cgs[cg0 + gi];
+          const McgSpec& S = specs[G->spec];
+          const int na = G->active_n;
+          const bool cond = S.kind == MCG_SYN_STATIC_COND || S.kind == MCG_SYN_STDP_COND;
+          if (na == 0 || !(cond || S.kind == MCG_SYN_STATIC_CURRENT || S.kind == MCG_SYN_HOMEO_CURRENT))
+            continue;
+          if (cond && !hg) {
+            for (int i = lane; i < K.n; i += 32) {
+              M.gsyn[i] = 0.0;
+              M.gsyn_rhs[i] = 0.0;
+            }
+            hg = true;
+            __syncwarp();
+          }
+          const int64_t base = G->inst;
+          const double* v = B.abuf + off;
+          // compaction: kept entries in list order
+          int out = 0;
+          for (int a0 = 0; a0 < na; a0 += 32) {
+            const int a = a0 + lane;
+            const bool keep = a < na && v[a] != 0.0;
+            const unsigned mk = __ballot_sync(MCG_FULL, keep);
+            if (keep) D.i_active[base + out + __popc(mk & mcg_lanemask_lt())] = B.aidx[off + a];
+            out += __popc(mk);
+          }
+          // the fold: one dependent add per entry (-0.0 for dropped kernels, the
+          // identity; a conductance's rhs term v * e_rev of a dropped kernel is
+          // +-0.0, and the running sums, started at +0.0, are never -0.0)
+          if (lane == 0) {
+            double* acc = cond ? M.gsyn : M.rhs_cur;
+            const int comp = S.comp;
+            double r1 = acc[comp];
+            if (cond) {
+              const double erev = S.e_rev;
+              double r2 = M.gsyn_rhs[comp];
+              int i = 0;
+              for (; i + 8 <= na; i += 8) {
+                double x[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) x[u] = v[i + u];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                  r1 += x[u];
+                  r2 += x[u] * erev;
+                }
+              }
+              for (; i < na; ++i) {
+                r1 += v[i];
+                r2 += v[i] * erev;
+              }
+              M.gsyn_rhs[comp] = r2;
+            } else {
+              int i = 0;
+              for (; i + 8 <= na; i += 8) {
+                double x[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) x[u] = v[i + u];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) r1 += x[u];
+              }
+              for (; i < na; ++i) r1 += v[i];
+            }
+            acc[comp] = r1;
+            G->active_n = out;
+          }
+          if (!cond && out > 0) hc = true;
+          off += (na + 31) & ~31;
+          __syncwarp();
+        }
+        if (lane == 0) {
+          cs[0].has_gsyn = hg;
+          cs[0].has_current = hc;
+        }
+      }
+    } else
     for (int k = warp; k < nc; k += nwarps) {
       if (!cs[k].has_act) continue;
       const int c = c0 + k;
@@ -1603,11 +1732,14 @@ __device__ void mcg_batch_epoch(const McgDev& D, const McgBatchArgs& A, int32_t 
           }
         }
       };
-      const int parts = max(1, nwarps / nc);
+      // (warp 0 is folding phase B's kernels when pb)
+      const int w0 = pb ? 1 : 0, nw = nwarps - w0;
+      const int parts = max(1, nw / nc);
       if (parts == 1) {
-        for (int k = warp; k < nc; k += nwarps) stc_cell(k, lane, 32);
+        for (int k = warp - w0; k < nc; k += nw) if (k >= 0) stc_cell(k, lane, 32);
       } else {
-        for (int it = warp; it < nc * parts; it += nwarps) {
+        for (int it = warp - w0; it < nc * parts; it += nw) {
+          if (it < 0) break;
           const int k = it / parts, part = it - k * parts;
           stc_cell(k, part * 32 + lane, 32 * parts);
         }

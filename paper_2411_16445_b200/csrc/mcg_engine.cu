@@ -266,6 +266,7 @@ struct Engine {
   int32_t bc_stride = 0;  // doubles per staged cell's compartment block
   int32_t bc_nch_max = 0;  // chain-sweep lane descriptors per batch
   int32_t bc_lean = 0;
+  int32_t bc_act_max = 0;
   int bc_carve = 100;  // shared-memory carveout (percent) this engine's batch kernel needs
   int32_t bc_kind_doubles = 0, bc_specs_sm = 0, bc_stc_sm = 0;
   size_t bc_smem = 0;
@@ -455,6 +456,27 @@ struct Engine {
     if (std::getenv("MCG_NO_STC_SM")) bc_stc_sm = 0;
     if (bc_stc_sm) bc_smem += size_t(bc_stc_max) * 32;
     bc_fmask_words = static_cast<int32_t>(fmask_words);
+    // one cell per CTA: phase B's scratch (decayed kernel | instance index per
+    // active-list entry, groups padded to 32) when the lists are long enough
+    // to be worth spreading over the CTA
+    bc_act_max = 0;
+    if (bc_cells == 1 && !std::getenv("MCG_NO_PAR_ACTIVE")) {
+      int amax = 0;
+      for (int c = 0; c < nl; ++c) {
+        const McgKind& K = m.kinds[m.cell_kind[c]];
+        int tot = 0;
+        for (int gi = 0; gi < K.n_groups; ++gi) {
+          const McgCellGroup& G = m.cgs[m.cg_off[c] + gi];
+          const int kd = m.specs[G.spec].kind;
+          if (kd == MCG_SYN_STATIC_COND || kd == MCG_SYN_STDP_COND || kd == MCG_SYN_STATIC_CURRENT ||
+              kd == MCG_SYN_HOMEO_CURRENT)
+            tot += (G.size + 31) & ~31;
+        }
+        amax = std::max(amax, tot);
+      }
+      if (amax >= 256 && bc_smem + size_t(amax) * 12 + 64 <= size_t(smem_optin) - 4096) bc_act_max = amax;
+      bc_smem += size_t(bc_act_max) * 12;
+    }
     // staged delivery: the epoch's due events of the resident batch in shared
     // memory (mcg_stage_events), in whatever the opt-in limit leaves
     bc_ev_cap = 0;
@@ -1511,6 +1533,7 @@ struct Engine {
     A.ev_cap = bc_ev_cap;
     A.nch_max = bc_nch_max;
     A.lean = bc_lean;
+    A.act_max = bc_act_max;
     A.fmask_words = bc_fmask_words;
     if (phase_timing) {
       if (!d_phase.p) {
