@@ -304,6 +304,13 @@ mcg_status mcg_partition(const mcg_recipe* recipe, int32_t world, uint32_t* boun
 mcg_status mcg_build_digest(const mcg_recipe* recipe, const mcg_options* opt, int32_t threads,
                             uint64_t out[4]);
 
+/* The same digest from a constructed engine's own layout: the edge records
+ * and instances its build resolved (on the device for recipes without STDP
+ * placements: mcg_resolve.cuh, engine.cpp:357-391).  Equal to
+ * mcg_build_digest of the same recipe and options.  Host-side check only
+ * (downloads the edge records). */
+mcg_status mcg_engine_layout_digest(mcg_engine* eng, uint64_t out[4]);
+
 /* ---- instrumentation (bench.py) -------------------------------------------- */
 
 typedef struct {
@@ -321,7 +328,7 @@ typedef struct {
   double advance_ms;          /* CUDA-event time of advance_to calls (engine stream) */
   int64_t advance_calls;
   int32_t stepping_kernel;    /* 0: k_batch, 1: k_warp, 2: k_point (mcg_engine.cu) */
-  int32_t reserved;
+  int32_t edges_on_device;    /* 1: connections resolved on the device (mcg_resolve.cuh) */
 } mcg_stats;
 mcg_status mcg_get_stats(mcg_engine* eng, mcg_stats* out);
 /* enable/disable CUDA-event timing of the epoch kernel (adds one event pair per epoch) */

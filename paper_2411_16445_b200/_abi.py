@@ -112,7 +112,7 @@ class mcg_stats(C.Structure):
                 ("total_synapses", C.c_int64), ("stc_synapses", C.c_int64),
                 ("hh_comps", C.c_int64), ("species_comps", C.c_int64),
                 ("advance_ms", C.c_double), ("advance_calls", C.c_int64),
-                ("stepping_kernel", C.c_int32), ("reserved", C.c_int32)]
+                ("stepping_kernel", C.c_int32), ("edges_on_device", C.c_int32)]
 
 
 class mcg_gb_params(C.Structure):
@@ -144,7 +144,7 @@ EXPORTS = ("mcg_create", "mcg_destroy", "mcg_last_error", "mcg_abi_version", "mc
            "mcg_trace_len", "mcg_get_trace", "mcg_cell_ncomp", "mcg_cell_ngroups",
            "mcg_group_size", "mcg_cell_parent", "mcg_read_state", "mcg_write_state",
            "mcg_get_stats", "mcg_set_timing", "mcg_device_math",
-           "mcg_er_connect", "mcg_build_digest", "mcg_set_cell_rng", "mcg_shard_spike_cap", "mcg_shard_gid_begin", "mcg_shard_gid_end",
+           "mcg_er_connect", "mcg_build_digest", "mcg_engine_layout_digest", "mcg_set_cell_rng", "mcg_shard_spike_cap", "mcg_shard_gid_begin", "mcg_shard_gid_end",
            "mcg_shard_set_buffers", "mcg_shard_run_epoch", "mcg_partition",
            "mcg_gb_trials", "mcg_gb_dp_curve", "mcg_stdp_window", "mcg_checkpoint", "mcg_restore",
            "mcg_libm_check", "mcg_nccl_unique_id", "mcg_shard_init_nccl", "mcg_shard_advance_to",
@@ -195,6 +195,7 @@ def _declare(L):
         "mcg_shard_run_epoch": (C.c_int32, [eng, C.c_double]),
         "mcg_partition": (C.c_int32, [P(mcg_recipe), C.c_int32, C.c_void_p]),
         "mcg_build_digest": (C.c_int32, [P(mcg_recipe), P(mcg_options), C.c_int32, C.c_void_p]),
+        "mcg_engine_layout_digest": (C.c_int32, [C.c_void_p, C.c_void_p]),
         "mcg_set_cell_rng": (C.c_int32, [eng, C.c_void_p, C.c_void_p]),
         "mcg_nccl_unique_id": (C.c_int32, [C.c_void_p]),
         "mcg_shard_init_nccl": (C.c_int32, [eng, C.c_void_p]),

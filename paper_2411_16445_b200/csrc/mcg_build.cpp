@@ -284,7 +284,7 @@ struct StageTimer {
 };
 }  // namespace
 
-void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m, int threads) {
+void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m, int threads, bool defer_edges) {
   StageTimer tm;
   const double dt = opt.dt_ms;
   m.dt = dt;
@@ -739,8 +739,32 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m, int 
   }
   // ---- rank order: bucket offsets (cell src keys ascending, sources last)
   for (size_t k = 0; k < nk1; ++k) bucket[k + 1] += bucket[k];
-  const int64_t ne = bucket[nk1];
+  int64_t ne = bucket[nk1];
+  m.n_edges = ne;
+  m.edges_deferred = defer_edges && !any_stdp && ne > 0;
+  if (m.edges_deferred) {
+    // per (cell, group): where its connections start in cg order, and what
+    // the device needs to pick instances and form the static-charge payload
+    m.cg_conn_off.assign(cgs + 1, 0);
+    for (int64_t q = 0; q < cgs; ++q) m.cg_conn_off[q + 1] = m.cg_conn_off[q] + cg_conns[q];
+    m.cg_static.assign(cgs, 0);
+    m.cg_count.assign(cgs, 0);
+    m.cg_comp.assign(cgs, -1);
+    m.cg_cf.assign(cgs, 0.0);
+    for (int c = 0; c < nl; ++c) {
+      const McgKind& K = m.kinds[m.cell_kind[c]];
+      for (int gi = 0; gi < K.n_groups; ++gi) {
+        const int64_t cg = m.cg_off[c] + gi;
+        const McgSpec& S = m.specs[m.cgs[cg].spec];
+        m.cg_static[cg] = S.kind == MCG_SYN_STATIC_CHARGE;
+        m.cg_count[cg] = S.count;
+        m.cg_comp[cg] = S.comp;
+        if (S.comp >= 0 && S.comp < K.n) m.cg_cf[cg] = m.k_cf[K.arr + S.comp];
+      }
+    }
+  }
   // every edge slot is written by pass 1 (no fill), but the payload columns
+  if (m.edges_deferred) ne = 0;  // the device writes them
   m.e_dst.resize(ne);
   m.e_group.resize(ne);
   m.e_inst.resize(ne);
@@ -764,8 +788,8 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m, int 
   // split over host threads by what they write (destination cells for the
   // instances, rank buckets for the edges) so that every thread sees its own
   // connections in the reference's order
-  HVec<uint32_t> inst_of(static_cast<size_t>(nconn));  // every local one is written
-  {
+  HVec<uint32_t> inst_of(static_cast<size_t>(m.edges_deferred ? 0 : nconn));  // every local one is written
+  if (!m.edges_deferred) {
     auto instances = [&](int c_lo, int c_hi) {
       std::vector<int32_t> cursor;  // SelectionCursor per (dst, label), cells [c_lo, c_hi)
       const int64_t cg_lo = m.cg_off[c_lo], cg_hi = m.cg_off[c_hi];
@@ -795,7 +819,7 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m, int 
     }
     for (auto& x : th) x.join();
   }
-  {
+  if (!m.edges_deferred) {
     // bucket ranges balanced by edge count; the source bucket (last) with the
     // source CSR goes to the last thread
     auto edges = [&](size_t k_lo, size_t k_hi) {

@@ -133,6 +133,18 @@ struct HostModel {
   std::vector<int64_t> src_edges;           // ranks
   int64_t max_delay_steps = 0;
 
+  // connection resolution left to the device (build_model(..., defer_edges)):
+  // the counts and offsets of pass 0 are here, the instance choice and the
+  // edge records are not (e_* and src_edges empty, i_weight unset) until the
+  // engine resolves them on the device (mcg_resolve.cuh)
+  bool edges_deferred = false;
+  int64_t n_edges = 0;                 // local edges (the length of every e_* array)
+  std::vector<int64_t> cg_conn_off;    // per (cell, group): first local connection, by cg
+  std::vector<uint8_t> cg_static;      // per (cell, group): static-charge placement
+  std::vector<int32_t> cg_count;       // per (cell, group): pre-placed count (0: appended)
+  std::vector<int32_t> cg_comp;        // per (cell, group): the placement's compartment
+  std::vector<double> cg_cf;           // per (cell, group): charge factor of that compartment
+
   std::vector<Source> sources;
   std::vector<McgProbe> probes;
 
@@ -155,7 +167,11 @@ int chain_schedule(int n, const int32_t* parent, std::vector<int32_t>& idx, int&
 
 // Materialize; throws mcg::Error with the reference's messages.
 // threads <= 0: build_threads() (MCG_BUILD_THREADS or the hardware threads)
-void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m, int threads = 0);
+// defer_edges: leave pass 1 (instances, edge records, source CSR) to the
+// device when the recipe allows it (no STDP placement: its weights start from
+// the resolved ones); m.edges_deferred says whether it did
+void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m, int threads = 0,
+                 bool defer_edges = false);
 
 // Shard assignment: contiguous gid ranges balanced by (compartments +
 // synapse instances); identical on every rank.

@@ -31,6 +31,9 @@
 #include "mcg_protocols.cuh"
 #include "mcg_checkpoint.h"
 #include "mcg_build.h"
+#include "mcg_resolve.cuh"
+
+static void layout_digest(const mcg::HostModel& m, uint64_t out[4]);
 
 namespace mcg {
 
@@ -221,6 +224,8 @@ struct Engine {
   DBuf<int32_t> d_e_comp;
   DBuf<double> d_e_wcf;
   DBuf<int64_t> d_e_delay, d_out_begin, d_out_end, d_src_edge_off, d_src_edges;
+  DBuf<uint32_t> d_e_seq;  // device-resolved edges only: their seq, for the host copy
+  bool host_edges = true;  // m.e_* hold the edge records (else only the device does)
   int32_t rank_bits = 1;
   // sources
   DBuf<McgSrcTask> d_tasks;
@@ -783,14 +788,14 @@ struct Engine {
       }
     }
     const auto t0 = std::chrono::steady_clock::now();
-    build_model(r, opt, m);
+    build_model(r, opt, m, 0, !std::getenv("MCG_HOST_RESOLVE"));
     {
       // grow the device pool once to about the engine's size: the uploads
       // below are then served from memory the pool already holds instead of
       // mapping it allocation by allocation (config 5: 1.3 s -> 0.15 s of
       // uploads for the first engine of a process)
-      const size_t ne = m.e_dst.size(), ni = size_t(m.n_inst), nc = m.v.size() + m.species.size();
-      const size_t est = ne * 56 + ni * 112 + nc * 80 + size_t(m.fifo_total) * 32 + (size_t(64) << 20);
+      const size_t ne = size_t(m.n_edges), ni = size_t(m.n_inst), nc = m.v.size() + m.species.size();
+      const size_t est = ne * (m.edges_deferred ? 96 : 56) + ni * 112 + nc * 80 + size_t(m.fifo_total) * 32 + (size_t(64) << 20);
       void* p = nullptr;
       if (cudaMallocAsync(&p, est, 0) == cudaSuccess) {
         cudaFreeAsync(p, 0);
@@ -820,7 +825,7 @@ struct Engine {
       else if (K.dyn == MCG_DYN_HH) b = (L + 1) / 2;
       sp_cap = static_cast<int32_t>(std::max<int64_t>(sp_cap, std::min<int64_t>(b, L)));
     }
-    const int64_t ne = static_cast<int64_t>(m.e_dst.size());
+    const int64_t ne = m.n_edges;
     rank_bits = bits_for(static_cast<uint64_t>(std::max<int64_t>(ne, 1)));
     if (rank_bits > 30) throw Error(MCG_ERR_ENGINE, "too many local edges for the event key");
 
@@ -905,18 +910,22 @@ struct Engine {
     d_stc_nz.alloc(std::max<size_t>(m.i_stc_h.size(), 1));
     if (d_stc_nz.p)
       CK(cudaMemsetAsync(d_stc_nz.p, 0xff, d_stc_nz.n * sizeof(McgNzCache), st));  // tag -1
-    d_e_dst.upload(m.e_dst, st);
-    d_e_group.upload(m.e_group, st);
-    d_e_inst.upload(m.e_inst, st);
-    d_e_weight.upload(m.e_weight, st);
-    d_e_src.upload(m.e_src, st);
-    d_e_comp.upload(m.e_comp, st);
-    d_e_wcf.upload(m.e_wcf, st);
-    d_e_delay.upload(m.e_delay, st);
+    if (m.edges_deferred) {
+      resolve_edges(r);
+    } else {
+      d_e_dst.upload(m.e_dst, st);
+      d_e_group.upload(m.e_group, st);
+      d_e_inst.upload(m.e_inst, st);
+      d_e_weight.upload(m.e_weight, st);
+      d_e_src.upload(m.e_src, st);
+      d_e_comp.upload(m.e_comp, st);
+      d_e_wcf.upload(m.e_wcf, st);
+      d_e_delay.upload(m.e_delay, st);
+      d_src_edges.upload(m.src_edges, st);
+    }
     d_out_begin.upload(m.out_begin, st);
     d_out_end.upload(m.out_end, st);
     d_src_edge_off.upload(m.src_edge_off, st);
-    d_src_edges.upload(m.src_edges, st);
 
     // source tasks: one per Poisson window, one per regular/scripted source
     std::vector<McgSrcTask> tasks;
@@ -1274,6 +1283,158 @@ struct Engine {
   std::vector<uint32_t> gspk_gid;
   bool async_ok = false;             // inboxes sized so that no expansion can overflow
 
+  // connection resolution on the device (mcg_resolve.cuh) after the host's
+  // pass 0 (build_model(..., defer_edges)): d_e_*, d_src_edges and the
+  // appended instances' weights in d_i_weight; the host keeps src_edges and
+  // max_delay_steps, and gets the edge records only when it needs them
+  // (ensure_host_edges: checkpoints)
+  void resolve_edges(const mcg_recipe& r) {
+    using namespace mcg_rs;
+    const int64_t nconn = r.n_connections, ne = m.n_edges;
+    const int64_t n_cg = static_cast<int64_t>(m.cgs.size());
+    if (nconn >= (int64_t(1) << 32) || n_cg >= (int64_t(1) << 31))
+      throw Error(MCG_ERR_ENGINE, "resolve: connection list too long for 32-bit keys");
+    const uint32_t g0 = m.gid_begin, g1 = m.gid_end;
+    // the connection list, as the recipe holds it
+    DBuf<uint8_t> from_src, policy;
+    DBuf<uint32_t> src, dst;
+    DBuf<int32_t> group;
+    DBuf<double> weight, delay;
+    auto up = [&](auto& d, const auto* h) {
+      d.alloc(size_t(std::max<int64_t>(nconn, 1)));
+      CK(cudaMemcpyAsync(d.p, h, size_t(nconn) * sizeof(*h), cudaMemcpyHostToDevice, st));
+    };
+    up(from_src, r.conn_from_source);
+    up(policy, r.conn_policy);
+    up(src, r.conn_src);
+    up(dst, r.conn_dst);
+    up(group, r.conn_group);
+    up(weight, r.conn_weight);
+    up(delay, r.conn_delay_ms);
+    const Conn C{from_src.p, src.p, dst.p, group.p, policy.p, weight.p, delay.p, nconn};
+    DBuf<int64_t> cg_conn_off, cg_off_l;
+    DBuf<int32_t> cg_count, cg_comp;
+    DBuf<uint8_t> cg_static;
+    DBuf<double> cg_cf;
+    DBuf<McgCellGroup> cgs;
+    cg_conn_off.upload(m.cg_conn_off, st);
+    cg_off_l.upload(m.cg_off, st);
+    cg_count.upload(m.cg_count, st);
+    cg_comp.upload(m.cg_comp, st);
+    cg_static.upload(m.cg_static, st);
+    cg_cf.upload(m.cg_cf, st);
+    cgs.upload(m.cgs, st);
+    // keys, then the two stable orders
+    const size_t nc = size_t(nconn);
+    DBuf<uint32_t> key_cg, key_src, val, key_s, perm1, perm2, inst_of;
+    key_cg.alloc(nc);
+    key_src.alloc(nc);
+    val.alloc(nc);
+    key_s.alloc(nc);
+    perm1.alloc(nc);
+    perm2.alloc(nc);
+    inst_of.alloc(nc);
+    k_keys<<<blocks(nconn), 256, 0, st>>>(C, g0, g1, cg_off_l.p, uint32_t(n_cg), uint32_t(r.n_cells), key_cg.p,
+                                         key_src.p, val.p);
+    CK(cudaGetLastError());
+    DBuf<uint8_t> tmp;
+    auto sort = [&](const uint32_t* k_in, uint32_t* k_out, const uint32_t* v_in, uint32_t* v_out, int64_t n,
+                    uint64_t max_key) {
+      size_t tb = 0;
+      const int bits = bits_for(max_key);
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, k_in, k_out, v_in, v_out, n, 0, bits, st));
+      if (tb > tmp.n) tmp.alloc(tb);
+      CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, k_in, k_out, v_in, v_out, n, 0, bits, st));
+    };
+    sort(key_cg.p, key_s.p, val.p, perm1.p, nconn, uint64_t(n_cg));
+    {
+      DBuf<int32_t> flag, scan;
+      flag.alloc(nc);
+      scan.alloc(nc);
+      k_rr_flags<<<blocks(nconn), 256, 0, st>>>(C, perm1.p, ne, flag.p);
+      size_t tb = 0;
+      CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, flag.p, scan.p, nconn, st));
+      if (tb > tmp.n) tmp.alloc(tb);
+      CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, flag.p, scan.p, nconn, st));
+      k_instances<<<blocks(ne), 256, 0, st>>>(C, key_s.p, perm1.p, ne, scan.p, cg_conn_off.p, cg_count.p,
+                                              cgs.p, inst_of.p, d_i_weight.p);
+      CK(cudaGetLastError());
+    }
+    sort(key_src.p, key_s.p, val.p, perm2.p, nconn, uint64_t(r.n_cells) + 1);
+    // the edge records, in rank order
+    const size_t nes = size_t(std::max<int64_t>(ne, 1));
+    d_e_dst.alloc(nes);
+    d_e_group.alloc(nes);
+    d_e_inst.alloc(nes);
+    d_e_weight.alloc(nes);
+    d_e_src.alloc(nes);
+    d_e_comp.alloc(nes);
+    d_e_wcf.alloc(nes);
+    d_e_delay.alloc(nes);
+    const int64_t n_se = static_cast<int64_t>(m.src_edges.size()), src0 = ne - n_se;
+    DBuf<uint32_t> skey, sval, skey_s, sval_s;
+    DBuf<unsigned long long> maxd;
+    skey.alloc(size_t(std::max<int64_t>(n_se, 1)));
+    sval.alloc(size_t(std::max<int64_t>(n_se, 1)));
+    maxd.alloc(1);
+    maxd.zero(st);
+    const Edges E{d_e_dst.p, d_e_group.p, d_e_comp.p, d_e_inst.p, d_e_src.p, nullptr, d_e_weight.p, d_e_wcf.p,
+                  d_e_delay.p};
+    d_e_seq.alloc(nes);
+    Edges E2 = E;
+    E2.seq = d_e_seq.p;
+    k_edges<<<blocks(ne), 256, 0, st>>>(C, perm2.p, ne, g0, m.dt, cg_off_l.p, cg_static.p, cg_comp.p, cg_cf.p,
+                                        inst_of.p, E2, maxd.p, skey.p, sval.p, src0);
+    CK(cudaGetLastError());
+    // per-source CSR of the source bucket: each source's edges in rank order
+    d_src_edges.alloc(size_t(std::max<int64_t>(n_se, 1)));
+    if (n_se > 0) {
+      skey_s.alloc(size_t(n_se));
+      sval_s.alloc(size_t(n_se));
+      sort(skey.p, skey_s.p, sval.p, sval_s.p, n_se, uint64_t(std::max(r.n_sources, 1)));
+      k_u32_to_i64<<<blocks(n_se), 256, 0, st>>>(sval_s.p, n_se, d_src_edges.p);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(m.src_edges.data(), d_src_edges.p, size_t(n_se) * sizeof(int64_t),
+                         cudaMemcpyDeviceToHost, st));
+    }
+    unsigned long long md = 0;
+    CK(cudaMemcpyAsync(&md, maxd.p, sizeof(md), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    m.max_delay_steps = static_cast<int64_t>(md);
+    host_edges = false;
+  }
+
+  // the layout digest of mcg_build_digest from this engine's own layout (the
+  // device-resolved edges and instance weights when the build deferred them)
+  void layout_digest(uint64_t out[4]) {
+    ensure_host_edges();
+    HostModel c = m;
+    const auto w = download(d_i_weight, size_t(m.n_inst));
+    c.i_weight.assign(w.begin(), w.end());
+    ::layout_digest(c, out);
+  }
+
+  // the edge records and appended weights on the host (after resolve_edges)
+  void ensure_host_edges() {
+    if (host_edges) return;
+    const size_t ne = size_t(m.n_edges);
+    auto get = [&](auto& h, const auto& d) {
+      h.resize(ne);
+      if (ne) CK(cudaMemcpyAsync(h.data(), d.p, ne * sizeof(h[0]), cudaMemcpyDeviceToHost, st));
+    };
+    get(m.e_dst, d_e_dst);
+    get(m.e_group, d_e_group);
+    get(m.e_inst, d_e_inst);
+    get(m.e_weight, d_e_weight);
+    get(m.e_src, d_e_src);
+    get(m.e_seq, d_e_seq);
+    get(m.e_comp, d_e_comp);
+    get(m.e_wcf, d_e_wcf);
+    get(m.e_delay, d_e_delay);
+    CK(cudaStreamSynchronize(st));
+    host_edges = true;
+  }
+
   // inbox capacities that no epoch can exceed: per destination, every in-edge
   // delivers at most sp_cap (cell edges) or, from a source, one event per step
   // (Poisson) or per scheduled time (regular / scripted, which may share a
@@ -1282,6 +1443,34 @@ struct Engine {
   bool size_inboxes_for_worst_case(size_t budget_bytes) {
     const int nl = n_local();
     std::vector<int64_t> inc(std::max(nl, 1), 0), pend(std::max(nl, 1), 0);
+    if (!host_edges) {  // the same counts on the device
+      using namespace mcg_rs;
+      DBuf<unsigned long long> di, dp;
+      di.alloc(inc.size());
+      dp.alloc(pend.size());
+      di.zero(st);
+      dp.zero(st);
+      k_worst_cell<<<blocks(std::max<int64_t>(m.n_edges, 1)), 256, 0, st>>>(d_e_dst.p, d_e_src.p, d_e_delay.p,
+                                                                            m.n_edges, sp_cap, L, di.p, dp.p);
+      std::vector<int64_t> per_k(m.src_edges.size());
+      for (size_t q = 0; q < m.sources.size(); ++q) {
+        const Source& S = m.sources[q];
+        const int64_t per = S.type == MCG_SRC_POISSON ? L
+                            : S.type == MCG_SRC_REGULAR ? std::max<int64_t>(S.r_count, 0)
+                                                        : static_cast<int64_t>(S.steps.size());
+        for (int64_t k = m.src_edge_off[q]; k < m.src_edge_off[q + 1]; ++k) per_k[size_t(k)] = per;
+      }
+      DBuf<int64_t> dk;
+      if (!per_k.empty()) {
+        dk.upload(per_k, st);
+        k_worst_src<<<blocks(int64_t(per_k.size())), 256, 0, st>>>(d_e_dst.p, d_e_delay.p, d_src_edges.p, dk.p,
+                                                                   int64_t(per_k.size()), L, di.p, dp.p);
+      }
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(inc.data(), di.p, inc.size() * 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(pend.data(), dp.p, pend.size() * 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    }
     auto add = [&](size_t r, int64_t per) {
       const int c = m.e_dst[r];
       if (c < 0) return;
@@ -1291,7 +1480,7 @@ struct Engine {
     };
     for (size_t r = 0; r < m.e_dst.size(); ++r)
       if (m.e_src[r] != 0xFFFFFFFFu) add(r, sp_cap);
-    for (size_t q = 0; q < m.sources.size(); ++q) {
+    for (size_t q = 0; host_edges && q < m.sources.size(); ++q) {
       const Source& S = m.sources[q];
       const int64_t per = S.type == MCG_SRC_POISSON ? L
                           : S.type == MCG_SRC_REGULAR ? std::max<int64_t>(S.r_count, 0)
@@ -1935,6 +2124,7 @@ struct Engine {
   std::vector<uint8_t> make_checkpoint() {
     if (m.world > 1) throw Error(MCG_ERR_ENGINE, "checkpoint: not supported for a sharded engine");
     ensure_flushed();
+    ensure_host_edges();
     const int nl = n_local();
     const size_t nv = m.v.size(), nsp = m.species.size(), ni = m.i_comp.size();
     const auto v = download(d_v, nv), hm = download(d_hh_m, nv), hh = download(d_hh_h, nv),
@@ -2048,6 +2238,7 @@ struct Engine {
   // Checkpoint::deserialize + Engine::restore (engine.cpp:1095-1140, 1235-1325)
   void restore(const uint8_t* bytes, size_t size) {
     ensure_flushed();  // a rejected checkpoint leaves the current state whole
+    ensure_host_edges();
     lazy_valid = false;
     invalidate_mirror();
     if (m.world > 1) throw Error(MCG_ERR_ENGINE, "checkpoint: not supported for a sharded engine");
@@ -2397,6 +2588,7 @@ mcg_status mcg_get_stats(mcg_engine* eng, mcg_stats* out) {
     eng->e.sync_counters_raw();
     eng->e.stats.events_delivered = static_cast<int64_t>(eng->e.h_ctr[mcg::C_DELIVERED]);
     eng->e.stats.stepping_kernel = eng->e.use_point ? 2 : (eng->e.use_warp ? 1 : 0);
+    eng->e.stats.edges_on_device = eng->e.m.edges_deferred ? 1 : 0;
     *out = eng->e.stats;
   });
 }
@@ -2450,59 +2642,73 @@ mcg_status mcg_partition(const mcg_recipe* recipe, int32_t world, uint32_t* boun
   });
 }
 
+extern "C++" {
+// FNV-1a over the runtime layout: edge records, instances, CSRs, groups, queues
+static void layout_digest(const mcg::HostModel& m, uint64_t out[4]) {
+  uint64_t h = 1469598103934665603ull;  // FNV-1a over the layout
+  auto mix = [&](uint64_t x) {
+    h ^= x;
+    h *= 1099511628211ull;
+  };
+  auto mixd = [&](double x) {
+    uint64_t b;
+    std::memcpy(&b, &x, 8);
+    mix(b);
+  };
+  for (size_t i = 0; i < m.e_dst.size(); ++i) {
+    mix(uint64_t(m.e_dst[i]));
+    mix(uint64_t(m.e_group[i]));
+    mix(m.e_inst[i]);
+    mix(m.e_src[i]);
+    mix(m.e_seq[i]);
+    mix(uint64_t(m.e_delay[i]));
+    mix(uint64_t(int64_t(m.e_comp[i])));
+    mixd(m.e_weight[i]);
+    mixd(m.e_wcf[i]);
+  }
+  for (size_t i = 0; i < m.i_comp.size(); ++i) {
+    mix(uint64_t(m.i_comp[i]));
+    mixd(m.i_weight[i]);
+    mixd(m.i_stc_h[i]);
+  }
+  for (double x : m.i_stdp_w) mixd(x);
+  for (double x : m.i_homeo_w) mixd(x);
+  for (int64_t x : m.src_edge_off) mix(uint64_t(x));
+  for (int64_t x : m.src_edges) mix(uint64_t(x));
+  for (int64_t x : m.out_begin) mix(uint64_t(x));
+  for (int64_t x : m.out_end) mix(uint64_t(x));
+  for (const McgCellGroup& G : m.cgs) {
+    mix(uint64_t(G.inst));
+    mix(uint64_t(G.size));
+    mix(uint64_t(int64_t(G.fifo)));
+  }
+  for (const McgFifo& F : m.fifos) {
+    mix(uint64_t(F.base));
+    mix(uint64_t(F.cap));
+  }
+  mix(uint64_t(m.min_delay_steps));
+  mix(uint64_t(m.max_delay_steps));
+  out[0] = h;
+  out[1] = m.e_dst.size();
+  out[2] = uint64_t(m.n_inst);
+  out[3] = uint64_t(m.min_delay_steps);
+}
+}  // extern "C++"
+
 mcg_status mcg_build_digest(const mcg_recipe* recipe, const mcg_options* opt, int32_t threads,
                             uint64_t out[4]) {
   return guarded([&] {
     if (!recipe || !opt || !out) throw mcg::Error(MCG_ERR_ARGUMENT, "build_digest: null pointer");
     mcg::HostModel m;
     mcg::build_model(*recipe, *opt, m, threads);
-    uint64_t h = 1469598103934665603ull;  // FNV-1a over the layout
-    auto mix = [&](uint64_t x) {
-      h ^= x;
-      h *= 1099511628211ull;
-    };
-    auto mixd = [&](double x) {
-      uint64_t b;
-      std::memcpy(&b, &x, 8);
-      mix(b);
-    };
-    for (size_t i = 0; i < m.e_dst.size(); ++i) {
-      mix(uint64_t(m.e_dst[i]));
-      mix(uint64_t(m.e_group[i]));
-      mix(m.e_inst[i]);
-      mix(m.e_src[i]);
-      mix(m.e_seq[i]);
-      mix(uint64_t(m.e_delay[i]));
-      mix(uint64_t(int64_t(m.e_comp[i])));
-      mixd(m.e_weight[i]);
-      mixd(m.e_wcf[i]);
-    }
-    for (size_t i = 0; i < m.i_comp.size(); ++i) {
-      mix(uint64_t(m.i_comp[i]));
-      mixd(m.i_weight[i]);
-      mixd(m.i_stc_h[i]);
-    }
-    for (double x : m.i_stdp_w) mixd(x);
-    for (double x : m.i_homeo_w) mixd(x);
-    for (int64_t x : m.src_edge_off) mix(uint64_t(x));
-    for (int64_t x : m.src_edges) mix(uint64_t(x));
-    for (int64_t x : m.out_begin) mix(uint64_t(x));
-    for (int64_t x : m.out_end) mix(uint64_t(x));
-    for (const McgCellGroup& G : m.cgs) {
-      mix(uint64_t(G.inst));
-      mix(uint64_t(G.size));
-      mix(uint64_t(int64_t(G.fifo)));
-    }
-    for (const McgFifo& F : m.fifos) {
-      mix(uint64_t(F.base));
-      mix(uint64_t(F.cap));
-    }
-    mix(uint64_t(m.min_delay_steps));
-    mix(uint64_t(m.max_delay_steps));
-    out[0] = h;
-    out[1] = m.e_dst.size();
-    out[2] = uint64_t(m.n_inst);
-    out[3] = uint64_t(m.min_delay_steps);
+    layout_digest(m, out);
+  });
+}
+
+mcg_status mcg_engine_layout_digest(mcg_engine* eng, uint64_t out[4]) {
+  return guarded([&] {
+    if (!eng || !out) throw mcg::Error(MCG_ERR_ARGUMENT, "engine_layout_digest: null pointer");
+    eng->e.layout_digest(out);
   });
 }
 

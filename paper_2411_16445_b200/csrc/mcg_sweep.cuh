@@ -89,11 +89,12 @@ __device__ __forceinline__ double mcg_chain_rinit_reg(const McgChainLane& L, int
 }
 
 // all 32 lanes of the warp must call this (inactive lanes with on = 0).
-// Three passes over the lane's chain side, so that the two dependent chains
+// Two passes over the lane's chain side, so that the two dependent chains
 // carry nothing but their own fp64 operations:
-//   1. r2 of every position, cap*x + rhs (independent: full ILP)
-//   2. elimination, leaf to top: r2[p] += f[c]*r2[c] along the chain
-//   3. the root, then substitution, top to leaf, with the reciprocal quotient
+//   1+2. elimination, leaf to top: r2[p] += f[c]*r2[c] along the chain, with
+//        r2 = cap*x + rhs of the next block formed (off the chain) while the
+//        current block's links run
+//   3.   the root, then substitution, top to leaf, with the reciprocal quotient
 // Each chain loop loads the next block's operands before the current block's
 // links, so the shared-memory latency stays off the chain.
 template <bool kRcBuf = true>
@@ -111,9 +112,12 @@ __device__ __forceinline__ void mcg_chain_lane(const McgChainLane& L) {
   const double x_root = L.on ? S[L.x] : 0.0;
   const double rc_root = kRcBuf ? ((L.on && L.rc >= 0) ? S[L.rc] : 0.0) : (L.rc_node == 0 ? L.rc_val : 0.0);
 
-  // ---- 1. r2 = cap*x + rhs (tree_solver.cpp:57); padding positions +0
-#pragma unroll 1
-  for (int b = 0; b < lp; b += 4) {
+  // ---- 1 + 2. r2 = cap*x + rhs (tree_solver.cpp:57; padding positions +0)
+  // formed for the block ahead while the current block's links run, then the
+  // elimination, leaf to top: r2[p] += f[c]*r2[c] along the chain.  cur = the
+  // final r2 of the last position, fp its f (the child's factor applied to
+  // its parent).  Two register blocks in turn.
+  auto r2_block = [&](int b, double* r, double* f) {
     int nd[4];
     double xv[4], rcv[4], cp[4], gl[4];
 #pragma unroll
@@ -121,6 +125,7 @@ __device__ __forceinline__ void mcg_chain_lane(const McgChainLane& L) {
       nd[u] = PI[ib + b + u];
       cp[u] = S[capb + b + u];
       gl[u] = S[glb + b + u];
+      f[u] = S[fb + b + u];
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -130,32 +135,20 @@ __device__ __forceinline__ void mcg_chain_lane(const McgChainLane& L) {
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const double r = kRcBuf ? mcg_chain_rinit(L, nd[u], cp[u], gl[u], xv[u], rcv[u])
+      const double v = kRcBuf ? mcg_chain_rinit(L, nd[u], cp[u], gl[u], xv[u], rcv[u])
                               : mcg_chain_rinit_reg(L, nd[u], cp[u], gl[u], xv[u], rcv[u]);
-      S[rb + b + u] = nd[u] >= 0 ? r : 0.0;
+      r[u] = nd[u] >= 0 ? v : 0.0;
     }
-  }
-
-  // ---- 2. elimination, leaf side first: cur = final r2 of the last position,
-  // fp its f (the child's factor applied to its parent).  Two register blocks
-  // in turn: one is loaded while the other's links run.
+  };
   double cur = 0.0, fp = -0.0;
   if (lp > 0) {
     double rA[4], fA[4], rB[4], fB[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      rA[u] = S[rb + u];
-      fA[u] = S[fb + u];
-    }
+    r2_block(0, rA, fA);
 #pragma unroll 1
     for (int b = 0; b < lp; b += 8) {
       const bool two = b + 4 < lp;
       const int nb = two ? b + 4 : b;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        rB[u] = S[rb + nb + u];
-        fB[u] = S[fb + nb + u];
-      }
+      r2_block(nb, rB, fB);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const double r = rA[u] + fp * cur;
@@ -165,11 +158,7 @@ __device__ __forceinline__ void mcg_chain_lane(const McgChainLane& L) {
       }
       if (!two) break;
       const int na = b + 8 < lp ? b + 8 : b;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        rA[u] = S[rb + na + u];
-        fA[u] = S[fb + na + u];
-      }
+      r2_block(na, rA, fA);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const double r = rB[u] + fp * cur;
