@@ -1153,6 +1153,15 @@ __device__ void mcg_batch_exit(const McgDev& D, const McgBatchArgs& A, int32_t b
 
 // ---- E2: membrane and species systems of batch b (one step); out of line so
 // its register allocation does not compete with the rest of the step loop
+// the general V solves that a whole warp takes (mcg_solve_tree_warp): the
+// systems mcg_ph_solve would otherwise give mcg_solve_tree_fast
+__device__ __forceinline__ bool mcg_tree_warp_item(const McgKind& K, const McgCellSm& X, int sys) {
+  if (sys != 0 || K.gch_n <= 0) return false;
+  if (K.dyn == MCG_DYN_HH) return true;
+  if (K.dyn == MCG_DYN_LIF) return !X.refractory && !(!X.has_gsyn && K.v_const);
+  return false;
+}
+
 __device__ __noinline__ void mcg_ph_solve(const McgDev& D, const McgBatchArgs& A, int32_t b) {
   const McgBatchSm B = mcg_batch_sm(A);
   const int tid = threadIdx.x, T = blockDim.x;
@@ -1175,6 +1184,9 @@ __device__ __noinline__ void mcg_ph_solve(const McgDev& D, const McgBatchArgs& A
   // cells, so items on separate warps run concurrently instead of taking
   // turns in one warp
   const int wr0 = split >> 5, nwr = (T - split) >> 5;
+  // few items per warp: the general tree solves take a warp each instead of
+  // a lane (the branches of a tree side by side)
+  const bool warp_tree = nc * S1 <= 2 * nwr;
   if (tid < split) {
     for (int t = tid; t < nch; t += split) {
       McgChainLane L{};
@@ -1210,6 +1222,7 @@ __device__ __noinline__ void mcg_ph_solve(const McgDev& D, const McgBatchArgs& A
     const McgCellSm& X = cs[k];
     const McgKind& K = kc[k];
     if (mcg_chain_ok(K, X, sys, m)) continue;
+    if (warp_tree && mcg_tree_warp_item(K, X, sys)) continue;  // below
     const int n = K.n;
     const bool in_sm = n <= m;
     const McgCellMem M = mcg_cell_mem(D, K, c, in_sm ? mcg_comp_block(A, B, k) : nullptr);
@@ -1288,6 +1301,40 @@ __device__ __noinline__ void mcg_ph_solve(const McgDev& D, const McgBatchArgs& A
                       KS.sp_coup + q, KS.par, M.SP + q, M.r2, M.diag, M.rhs_cur);
     }
     if (!ok) atomicOr(D.err, MCG_ERR_FLAG_SINGULAR);
+  }
+  if (warp_tree && split <= tid) {
+    for (int t = warp - wr0; t < nc * S1; t += nwr) {  // warp-uniform items
+      const int k = t / S1, sys = t - k * S1;
+      const McgCellSm& X = cs[k];
+      const McgKind& K = kc[k];
+      if (mcg_chain_ok(K, X, sys, m) || !mcg_tree_warp_item(K, X, sys)) continue;
+      const int c = c0 + k;
+      const int n = K.n;
+      const McgCellMem M = mcg_cell_mem(D, K, c, n <= m ? mcg_comp_block(A, B, k) : nullptr);
+      const McgKindSm KS = mcg_kind_consts(D, K, B.ksm, X.kb);
+      if (K.dyn == MCG_DYN_LIF) {
+        const bool hg = X.has_gsyn, hc = X.has_current;
+        for (int i = lane; i < n; i += 32) {
+          const double gs = KS.gl[i] + (hg ? M.gsyn[i] : 0.0);
+          const double rr = KS.glr[i] + (hg ? M.gsyn_rhs[i] : 0.0) + (hc ? M.rhs_cur[i] : 0.0);
+          M.gsyn[i] = gs;
+          M.gsyn_rhs[i] = rr;
+        }
+        __syncwarp();
+      }
+      bool ok = mcg_solve_tree_warp(D.k_ch_idx + K.gch_arr, KS.par, KS.cap, M.gsyn, KS.ax, M.gsyn_rhs, M.V,
+                                    M.diag, M.r2, lane);
+      if (lane == 0) {
+        if (n > 1 && !K.sp_const)
+          for (int p = 0; p < K.n_species; ++p)
+            ok &= mcg_species_sys(n, p == K.prp_idx, K.prp_comp, X.prod, KS.sp_cap + p * n,
+                                  KS.sp_gs + p * n, KS.sp_coup + p * n, KS.par,
+                                  M.SP + int64_t(p) * n, M.r2 + int64_t(1 + p) * n, M.diag,
+                                  D.s_rhs + D.comp_off[c]);
+        if (!ok) atomicOr(D.err, MCG_ERR_FLAG_SINGULAR);
+      }
+      __syncwarp();
+    }
   }
 }
 

@@ -156,6 +156,59 @@ int build_threads(int64_t nconn) {
   return std::clamp(static_cast<int>(std::thread::hardware_concurrency()), 1, 16);
 }
 
+int tree_chains(int n, const int32_t* parent, std::vector<int32_t>& out) {
+  out.clear();
+  if (n < 2) return 0;
+  std::vector<std::vector<int32_t>> kids(n);
+  for (int i = 1; i < n; ++i) {
+    if (parent[i] < 0 || parent[i] >= i) return 0;
+    kids[parent[i]].push_back(i);  // ascending
+  }
+  struct Chain {
+    std::vector<int32_t> nodes;
+    int level;
+    std::vector<int32_t> child;  // chain ids
+  };
+  std::vector<Chain> ch;
+  std::vector<std::pair<int32_t, int32_t>> todo{{0, -1}};  // (top node, parent chain)
+  for (size_t t = 0; t < todo.size(); ++t) {
+    const int id = static_cast<int>(ch.size());
+    if (id >= 32) return 0;
+    Chain c;
+    c.level = todo[t].second < 0 ? 0 : ch[todo[t].second].level + 1;
+    int x = todo[t].first;
+    c.nodes.push_back(x);
+    while (kids[x].size() == 1) {
+      x = kids[x][0];
+      c.nodes.push_back(x);
+    }
+    if (todo[t].second >= 0) ch[todo[t].second].child.push_back(id);
+    ch.push_back(std::move(c));
+    for (int k : kids[x]) todo.emplace_back(k, id);
+  }
+  int maxlev = 0, maxch = 0;
+  for (Chain& c : ch) {
+    maxlev = std::max(maxlev, c.level);
+    maxch = std::max(maxch, static_cast<int>(c.child.size()));
+    // descending top index: the order solve_tree's loop applies them
+    std::sort(c.child.begin(), c.child.end(),
+              [&](int a, int b) { return ch[a].nodes[0] > ch[b].nodes[0]; });
+  }
+  const int nch = static_cast<int>(ch.size());
+  out = {nch, maxlev, maxch};
+  int off = 0;
+  for (const Chain& c : ch) {
+    out.push_back(off);
+    out.push_back(static_cast<int32_t>(c.nodes.size()));
+    out.push_back(c.level);
+    out.push_back(static_cast<int32_t>(c.child.size()));
+    for (int q = 0; q < maxch; ++q) out.push_back(q < static_cast<int>(c.child.size()) ? c.child[q] : -1);
+    off += static_cast<int>(c.nodes.size());
+  }
+  for (const Chain& c : ch) out.insert(out.end(), c.nodes.begin(), c.nodes.end());
+  return nch;
+}
+
 // v = n copies of x, filled by nthr threads (parallel first touch)
 template <class T, class Al>
 void par_fill(std::vector<T, Al>& v, int64_t n, T x, int nthr) {
@@ -514,6 +567,19 @@ void build_model(const mcg_recipe& r, const mcg_options& opt, HostModel& m, int 
       K.ch_afirst = a_first;
       K.ch_arr = static_cast<int64_t>(m.k_ch_idx.size());
       if (lp > 0) m.k_ch_idx.insert(m.k_ch_idx.end(), idx.begin(), idx.end());
+    }
+    // chains of the general V solve (HH, LIF cable with conductances)
+    K.gch_n = 0;
+    K.gch_pad = 0;
+    K.gch_arr = 0;
+    if (n >= 2 && (K.dyn == MCG_DYN_HH || K.dyn == MCG_DYN_LIF) && !std::getenv("MCG_NO_TREE_WARP")) {
+      std::vector<int32_t> sched;
+      const int nch = tree_chains(n, g.parent.data(), sched);
+      if (nch > 0) {
+        K.gch_n = nch;
+        K.gch_arr = static_cast<int64_t>(m.k_ch_idx.size());
+        m.k_ch_idx.insert(m.k_ch_idx.end(), sched.begin(), sched.end());
+      }
     }
   }
 

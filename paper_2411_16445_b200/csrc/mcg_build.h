@@ -165,6 +165,15 @@ bool eliminate_constant(int n, const int32_t* parent, const double* cap, const d
 // LP and fills idx (2 LP + 1 positions, -1 = padding) and a_first; else 0.
 int chain_schedule(int n, const int32_t* parent, std::vector<int32_t>& idx, int& a_first);
 
+// Chains of a tree for the warp-parallel general solve (mcg_solve_tree_warp):
+// a chain runs from a node down while each node has exactly one child; the
+// children of its bottom node start the chains of the next level.  Layout:
+// [nch, maxlev, maxch, per chain (node offset, length, level, nchild,
+// child chain ids by descending top index, -1 padded to maxch), nodes of
+// every chain top to bottom].  Returns nch, or 0 (more than 32 chains, or a
+// parent index not below its node).
+int tree_chains(int n, const int32_t* parent, std::vector<int32_t>& out);
+
 // Materialize; throws mcg::Error with the reference's messages.
 // threads <= 0: build_threads() (MCG_BUILD_THREADS or the hardware threads)
 // defer_edges: leave pass 1 (instances, edge records, source CSR) to the

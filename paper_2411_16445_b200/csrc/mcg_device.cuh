@@ -361,6 +361,116 @@ __device__ bool mcg_solve_tree_fast(int n, const int32_t* par, const double* cap
   return true;
 }
 
+// solve_tree (tree_solver.cpp:46-74) by a whole warp, one lane per chain of
+// the tree (mcg_build.cpp tree_chains; all 32 lanes call it).  Every node
+// takes the reference's operations in the reference's order: its diagonal
+// gathers cap + gs, its own coupling and its children's couplings in
+// ascending child order (:55-62); in the elimination (:63-70) a node's
+// children contribute in descending index order -- inside a chain the one
+// child below it, at a chain's bottom the child chains' tops, gathered from
+// their lanes by shuffles in that order -- before it is eliminated itself;
+// the substitution (:71-73) runs top to bottom, a chain's top reading its
+// parent from the level above.  What the loop serializes across branches
+// runs side by side: the dependent chain is the deepest path of chains, not
+// the node count.  Quotients as mcg_solve_tree_fast (Markstein from RN(1/d),
+// reciprocals kept in gs_y for the substitution).  Returns false (on every
+// lane) if a diagonal met during elimination is not positive.
+__device__ bool mcg_solve_tree_warp(const int32_t* G, const int32_t* par, const double* cap, double* gs_y,
+                                    const double* coup, const double* rhs, double* v, double* diag,
+                                    double* r2, int lane) {
+  const int nch = G[0], maxlev = G[1], maxch = G[2];
+  const int rec = 4 + maxch;
+  const int32_t* CH = G + 3;
+  const int32_t* ND = CH + nch * rec;
+  const bool on = lane < nch;
+  int off = 0, len = 0, lev = -1, nchild = 0;
+  if (on) {
+    off = CH[lane * rec];
+    len = CH[lane * rec + 1];
+    lev = CH[lane * rec + 2];
+    nchild = CH[lane * rec + 3];
+  }
+  // ---- diag and r2 of my chain's nodes
+  for (int k = 0; k < len; ++k) {
+    const int i = ND[off + k];
+    double d = cap[i] + gs_y[i];
+    if (i >= 1) d += coup[i];
+    if (k + 1 < len) {
+      d += coup[ND[off + k + 1]];
+    } else {
+      for (int q = nchild - 1; q >= 0; --q) {  // child chains, ascending top index
+        const int cc = CH[lane * rec + 4 + q];
+        d += coup[ND[CH[cc * rec]]];
+      }
+    }
+    diag[i] = d;
+    r2[i] = cap[i] * v[i] + rhs[i];
+  }
+  // ---- elimination, deepest chains first
+  bool bad = false;
+  double td = 0.0, tr = 0.0;  // my top's terms for its parent: f*coup, f*r2
+  for (int L = maxlev; L >= 0; --L) {
+    const bool act = lev == L;
+    double cd = 0.0, cr = 0.0;
+    if (act) {
+      const int b = ND[off + len - 1];
+      cd = diag[b];
+      cr = r2[b];
+    }
+    for (int q = 0; q < maxch; ++q) {
+      const bool take = act && q < nchild;
+      const int src = take ? CH[lane * rec + 4 + q] : lane;
+      const double a = __shfl_sync(0xffffffffu, td, src), c = __shfl_sync(0xffffffffu, tr, src);
+      if (take) {
+        cd -= a;  // diag[par[i]] -= f * coup[i]
+        cr += c;  // r2[par[i]] += f * r2[i]
+      }
+    }
+    if (act) {
+      for (int k = len - 1; k >= 0; --k) {
+        const int i = ND[off + k];
+        diag[i] = cd;
+        r2[i] = cr;
+        if (i == 0) break;  // the root is not eliminated
+        if (cd <= 0.0) bad = true;
+        const double ci = coup[i];
+        const double yi = mcg_rcp_or_zero(cd);
+        gs_y[i] = yi;
+        const double f = mcg_div(ci, cd, yi);
+        const double a = f * ci, c = f * cr;
+        if (k > 0) {
+          const int p = ND[off + k - 1];
+          cd = diag[p] - a;
+          cr = r2[p] + c;
+        } else {
+          td = a;
+          tr = c;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  // ---- substitution, root chain first
+  for (int L = 0; L <= maxlev; ++L) {
+    if (lev == L) {
+      double vp = 0.0;
+      for (int k = 0; k < len; ++k) {
+        const int i = ND[off + k];
+        if (i == 0) {
+          if (diag[0] <= 0.0) bad = true;
+          vp = mcg_div(r2[0], diag[0], mcg_rcp_or_zero(diag[0]));
+        } else {
+          const double vpar = k == 0 ? v[par[i]] : vp;
+          vp = mcg_div(r2[i] + coup[i] * vpar, diag[i], gs_y[i]);
+        }
+        v[i] = vp;
+      }
+    }
+    __syncwarp();
+  }
+  return !__any_sync(0xffffffffu, bad);
+}
+
 // solve_tree with a precomputed constant elimination (McgKind::v_const /
 // sp_const): the rhs sweep and back-substitution of tree_solver.cpp:55-73
 // with f[i] = coupling[i]/diag[i] and the eliminated diagonal d[i] taken from

@@ -52,6 +52,11 @@ struct McgKind {
   // k_ch_idx[ch_arr + pos] = node of the position (-1: padding).
   int32_t ch_lp, ch_afirst;
   int64_t ch_arr;
+  // chains of the general (non-constant diagonal) V solve, one lane each
+  // (mcg_solve_tree_warp; mcg_build.cpp tree_chains): gch_n chains (0: none,
+  // the one-thread solve), the schedule at k_ch_idx[gch_arr]
+  int32_t gch_n, gch_pad;
+  int64_t gch_arr;
 };
 
 // SynSpec per kind placement (recipe.hpp:82-98) + hoisted constants
