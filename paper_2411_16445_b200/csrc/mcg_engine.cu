@@ -795,9 +795,24 @@ struct Engine {
       // mapping it allocation by allocation (config 5: 1.3 s -> 0.15 s of
       // uploads for the first engine of a process)
       const size_t ne = size_t(m.n_edges), ni = size_t(m.n_inst), nc = m.v.size() + m.species.size();
-      const size_t est = ne * (m.edges_deferred ? 96 : 56) + ni * 112 + nc * 80 + size_t(m.fifo_total) * 32 + (size_t(64) << 20);
+      // (device-resolved edges: plus the resolution's transient buffers)
+      const size_t est = ne * (m.edges_deferred ? 128 : 56) + ni * 112 + nc * 80 + size_t(m.fifo_total) * 32 +
+                         (size_t(64) << 20);
+      // skipped when the pool already holds that much free (an earlier
+      // engine's memory): a second growth would map memory the pool has
+      size_t have = 0;
+      {
+        cudaMemPool_t pool;
+        uint64_t reserved = 0, used = 0;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess &&
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && reserved > used)
+          have = size_t(reserved - used);
+        cudaGetLastError();
+      }
       void* p = nullptr;
-      if (cudaMallocAsync(&p, est, 0) == cudaSuccess) {
+      if (have >= est) {
+      } else if (cudaMallocAsync(&p, est, 0) == cudaSuccess) {
         cudaFreeAsync(p, 0);
         cudaStreamSynchronize(0);
       } else {
