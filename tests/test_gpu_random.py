@@ -4,6 +4,8 @@ STDP, homeostasis, STC), species with PRP synthesis, all three source kinds,
 all selection policies and every probe kind, run through the reference
 (oracle/_ref) and the B200 engine; spikes, state of every cell and group, and
 traces must be bitwise equal (or both engines raise the same error)."""
+import sys
+
 import numpy as np
 import pytest
 
@@ -158,6 +160,28 @@ def test_random_recipe_bitwise(gpu, seed):
         a, b = r.trace_arrays(p), g.trace_arrays(p)
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]), f"probe {p}"
     assert g.make_checkpoint().data == r.make_checkpoint()
+
+
+def _wide_segments(rng, n):
+    """Branchy trees: 6-40 segments, branches leaving their parent at 30 %, 50 %
+    or 100 % of its length (nodes with several children inside a segment)."""
+    n = int(rng.integers(6, 41))
+    segs = [Segment(-1, float(rng.uniform(8, 20)), float(rng.uniform(3, 8)), 1, 1.0)]
+    for i in range(1, n):
+        segs.append(Segment(int(rng.integers(0, i)), float(rng.uniform(4, 30)),
+                            float(rng.uniform(0.4, 1.5)), 3, float(rng.choice([0.3, 0.5, 1.0]))))
+    return segs
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_trees_bitwise(gpu, monkeypatch, seed):
+    """HH and conductance-driven cable cells on branchy random trees through the
+    warp-parallel general solve (mcg_solve_tree_warp: one lane per chain,
+    children gathered in descending index order) and, above 32 chains, the
+    one-thread solve: spikes, state, probes and checkpoint bytes equal the
+    reference's."""
+    monkeypatch.setattr(sys.modules[__name__], "_segments", _wide_segments)
+    test_random_recipe_bitwise(gpu, 1000 + seed)
 
 
 @pytest.mark.parametrize("seed", range(6))
