@@ -427,25 +427,33 @@ __device__ bool mcg_solve_tree_warp(const int32_t* G, const int32_t* par, const 
       }
     }
     if (act) {
-      for (int k = len - 1; k >= 0; --k) {
-        const int i = ND[off + k];
+      // the nodes below the top: each one's parent is the next one up
+      int i = ND[off + len - 1];
+      for (int k = len - 1; k >= 1; --k) {
+        const int p = ND[off + k - 1];
+        const double pd = diag[p], pr = r2[p], ci = coup[i];
         diag[i] = cd;
         r2[i] = cr;
-        if (i == 0) break;  // the root is not eliminated
-        if (cd <= 0.0) bad = true;
+        bad |= cd <= 0.0;
+        const double yi = mcg_rcp_or_zero(cd);
+        gs_y[i] = yi;
+        const double f = mcg_div(ci, cd, yi);
+        cd = pd - f * ci;
+        cr = pr + f * cr;
+        i = p;
+      }
+      // the top: the root is not eliminated; any other top's terms go to
+      // its parent's lane
+      diag[i] = cd;
+      r2[i] = cr;
+      if (i != 0) {
+        bad |= cd <= 0.0;
         const double ci = coup[i];
         const double yi = mcg_rcp_or_zero(cd);
         gs_y[i] = yi;
         const double f = mcg_div(ci, cd, yi);
-        const double a = f * ci, c = f * cr;
-        if (k > 0) {
-          const int p = ND[off + k - 1];
-          cd = diag[p] - a;
-          cr = r2[p] + c;
-        } else {
-          td = a;
-          tr = c;
-        }
+        td = f * ci;
+        tr = f * cr;
       }
     }
     __syncwarp();
@@ -453,16 +461,20 @@ __device__ bool mcg_solve_tree_warp(const int32_t* G, const int32_t* par, const 
   // ---- substitution, root chain first
   for (int L = 0; L <= maxlev; ++L) {
     if (lev == L) {
-      double vp = 0.0;
-      for (int k = 0; k < len; ++k) {
-        const int i = ND[off + k];
-        if (i == 0) {
-          if (diag[0] <= 0.0) bad = true;
-          vp = mcg_div(r2[0], diag[0], mcg_rcp_or_zero(diag[0]));
-        } else {
-          const double vpar = k == 0 ? v[par[i]] : vp;
-          vp = mcg_div(r2[i] + coup[i] * vpar, diag[i], gs_y[i]);
-        }
+      // the top (the root, or a node whose parent the level above solved),
+      // then the nodes below it, each from the one just solved
+      int i = ND[off];
+      double vp;
+      if (i == 0) {
+        bad |= diag[0] <= 0.0;
+        vp = mcg_div(r2[0], diag[0], mcg_rcp_or_zero(diag[0]));
+      } else {
+        vp = mcg_div(r2[i] + coup[i] * v[par[i]], diag[i], gs_y[i]);
+      }
+      v[i] = vp;
+      for (int k = 1; k < len; ++k) {
+        i = ND[off + k];
+        vp = mcg_div(r2[i] + coup[i] * vp, diag[i], gs_y[i]);
         v[i] = vp;
       }
     }
